@@ -1,0 +1,226 @@
+/* fsx.h — C ABI of the B200-native FreeScale embedding hot path (libfsx.so).
+ *
+ * Plain pointers and sizes only: no torch, no C++ types. Device pointers are
+ * CUDA device addresses on the context's device; host pointers are ordinary
+ * (preferably pinned) host memory. Streams are cudaStream_t passed as void*.
+ * Every entry point returns an int status (FSX_OK or a negative class code);
+ * fsx_last_error() returns the message of the calling thread's last failure.
+ * The status classes map 1:1 onto the reference's exception classes so the
+ * C++ and Python shims rethrow the same class with the same text
+ * (SURVEY §8(b) "Errors").
+ *
+ * Reference interfaces replaced (paths under /root/reference/proj):
+ *   table   — embedding::ShardView                 include/freescale/embedding.hpp:59-90
+ *   sort    — sorted_unique / IndexSet::shard_major src/embedding.cpp:12-16, 66-80
+ *   collide — compute_collision / collision_pct    include/freescale/embedding.hpp:51-57
+ *   route   — route_to_shard_major                 include/freescale/embedding.hpp:107-110
+ *   engine  — SynchronizedEmbedding / PrioritizedEmbedding
+ *                                                  include/freescale/embedding.hpp:126-189
+ *   a2a     — comm::Communicator::all_to_all       include/freescale/comm.hpp:126-128
+ *   partition — fbs_partition / vbs_partition / autotune_update / identity
+ *                                                  include/freescale/partition.hpp:50-74
+ *   cost    — sim::CostModel::compute_time_for_lengths  include/freescale/sim.hpp:24-35
+ */
+#ifndef FSX_H
+#define FSX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (reference exception class in brackets) --------------- */
+#define FSX_OK 0
+#define FSX_ERR_INVALID_ARGUMENT (-1) /* std::invalid_argument           */
+#define FSX_ERR_DOMAIN (-2)           /* std::domain_error               */
+#define FSX_ERR_OUT_OF_RANGE (-3)     /* std::out_of_range               */
+#define FSX_ERR_PROTOCOL (-4)         /* freescale::ProtocolError        */
+#define FSX_ERR_COLLECTIVE (-5)       /* freescale::CollectiveError      */
+#define FSX_ERR_CONFIG (-6)           /* freescale::ConfigError          */
+#define FSX_ERR_CUDA (-7)             /* CUDA runtime/driver failure     */
+#define FSX_ERR_NOMEM (-8)            /* device allocation failed        */
+
+/* element type of table values, rows and gradients */
+#define FSX_F32 0
+#define FSX_F64 1
+
+/* engine protocol (embedding.hpp:126-189) */
+#define FSX_MODE_SYNC 0 /* SynchronizedEmbedding: blocking, per-occurrence traffic */
+#define FSX_MODE_PRIO 1 /* PrioritizedEmbedding: collision-first, side lanes      */
+
+/* engine transport for N > 1 ranks */
+#define FSX_TRANSPORT_CE 0   /* copy-engine peer copies + stream mem-op flags, 0 SMs */
+#define FSX_TRANSPORT_NCCL 1 /* NCCL send/recv kernels (baseline only)               */
+
+const char* fsx_last_error(void);
+/* library build string: arch, git-less version, compile flags */
+const char* fsx_version(void);
+
+/* ---- context: one per rank (= one per GPU in production) ------------------ */
+typedef struct fsx_ctx fsx_ctx;
+
+int fsx_ctx_create(int device, int rank, int world, fsx_ctx** out);
+int fsx_ctx_destroy(fsx_ctx* ctx);
+/* Synchronize the context's device and surface any kernel-raised error
+ * (out-of-range / not-owned row ids, non-finite updates, protocol breaks)
+ * with the reference's exception class and message. */
+int fsx_ctx_sync(fsx_ctx* ctx);
+/* number of kernels this context has launched (for bench gpu_launches) */
+uint64_t fsx_ctx_launches(const fsx_ctx* ctx);
+
+/* ---- primitives (hot-path kernels, exposed for parity tests) -------------- */
+
+/* K1+K2: sorted unique of n u64 keys. Writes the unique keys ascending to
+ * d_unique (capacity n), optionally each input's slot in d_unique to
+ * d_inverse (u32, capacity n), and the unique count to *h_num_unique.
+ * Synchronous on `stream`. Replaces sorted_unique (embedding.cpp:12-16). */
+int fsx_sort_unique_u64(fsx_ctx* ctx, const uint64_t* d_keys, uint64_t n, uint64_t* d_unique,
+                        uint32_t* d_inverse, uint64_t* h_num_unique, void* stream);
+
+/* K3: compute_collision (embedding.cpp:82-93) on two raw shard-major id
+ * lists: both are sorted+uniqued on the device, then split into
+ * co = U(cur) ∩ U(next), ex_cur = U(cur) \ co, ex_next = U(next) \ co, all
+ * ascending. Capacities: d_co, d_ex_cur >= n_cur; d_ex_next >= n_next.
+ * h_counts[0..4] = |co|, |ex_cur|, |ex_next|, |U(cur)|, |U(next)|. */
+int fsx_collision_split(fsx_ctx* ctx, const uint64_t* d_cur, uint64_t n_cur,
+                        const uint64_t* d_next, uint64_t n_next, uint64_t* d_co,
+                        uint64_t* d_ex_cur, uint64_t* d_ex_next, uint64_t* h_counts,
+                        void* stream);
+
+/* K4: the requester half of route_to_shard_major (embedding.cpp:194-204):
+ * stable partition of n ids by owner = id mod num_shards. Writes the ids
+ * grouped by owner in original order to d_send_ids, their flat positions to
+ * d_send_pos, per-owner counts to h_send_counts[num_shards]. Raises
+ * FSX_ERR_DOMAIN ("embedding: row id X out of range ...") for ids >= total_rows. */
+int fsx_route_by_owner(fsx_ctx* ctx, const uint64_t* d_ids, uint64_t n, uint64_t total_rows,
+                       int num_shards, uint64_t* d_send_ids, uint32_t* d_send_pos,
+                       uint64_t* h_send_counts, void* stream);
+
+/* ---- table: one shard of a row-wise sharded table (ShardView) -------------- */
+typedef struct fsx_table fsx_table;
+
+/* ShardView ctor (embedding.cpp:108-119): allocates local_rows x dim values
+ * on the device and fills them with initial_value(seed, global_row, d)
+ * (splitmix64, exact in f64; FSX_F32 rounds that value once). */
+int fsx_table_create(fsx_ctx* ctx, uint64_t total_rows, uint32_t dim, int num_shards, int shard,
+                     double learning_rate, uint64_t seed, int dtype, fsx_table** out);
+int fsx_table_destroy(fsx_table* t);
+uint64_t fsx_table_local_rows(const fsx_table* t);
+/* device address of the local_rows x dim value array (row-major) */
+void* fsx_table_values(fsx_table* t);
+
+/* K5: ShardView::lookup (embedding.cpp:139-146): d_out[k] = row(ids[k]).
+ * Out-of-range / not-owned ids raise FSX_ERR_DOMAIN at the next sync point
+ * (this call synchronizes when `sync` != 0). */
+int fsx_table_gather(fsx_table* t, const uint64_t* d_ids, uint64_t n, void* d_out, void* stream,
+                     int sync);
+
+/* K8: ShardView::apply_gradients (embedding.cpp:148-181): each row's
+ * gradients summed in occurrence order, then row -= lr*acc, non-finite check.
+ * Optional outputs: sorted unique ids (d_unique, capacity n) and their
+ * post-update rows (d_rows, capacity n*dim); *h_num_unique if non-null.
+ * Synchronous. */
+int fsx_table_sgd_update(fsx_table* t, const uint64_t* d_ids, uint64_t n, const void* d_grads,
+                         uint64_t* d_unique, void* d_rows, uint64_t* h_num_unique, void* stream);
+
+/* values() as f64 host array [local_rows x dim] (lazy D2H mirror). */
+int fsx_table_download(fsx_table* t, double* h_values);
+/* overwrite the shard from a host f64 array (test / checkpoint-restore aid) */
+int fsx_table_upload(fsx_table* t, const double* h_values);
+
+/* ---- engines: Synchronized / Prioritized embedding ------------------------ */
+typedef struct fsx_engine fsx_engine;
+
+typedef struct fsx_engine_config {
+  int mode;                  /* FSX_MODE_SYNC | FSX_MODE_PRIO */
+  int transport;             /* FSX_TRANSPORT_CE | FSX_TRANSPORT_NCCL (N>1) */
+  uint64_t max_occurrences;  /* capacity: ids per rank per iteration */
+  uint32_t reduce_chunk;     /* 0: reference order (one sequential sum per
+                                row); k>0: rows with more than k occurrences
+                                are summed as fixed k-occurrence chunks, then
+                                chunk partials in order (deterministic, shared
+                                by both modes) */
+} fsx_engine_config;
+
+int fsx_engine_create(fsx_ctx* ctx, fsx_table* table, const fsx_engine_config* cfg,
+                      fsx_engine** out);
+int fsx_engine_destroy(fsx_engine* e);
+
+/* Peer wiring (N > 1). In-process ranks connect directly; separate
+ * processes exchange the opaque blob from fsx_engine_export (CUDA IPC
+ * handles of the receive windows) through any out-of-band channel. Every
+ * rank must connect every peer before the first forward. */
+int fsx_engine_connect_local(fsx_engine* e, int peer, fsx_engine* peer_engine);
+int fsx_engine_export(fsx_engine* e, void* blob, uint64_t* len); /* blob capacity >= 4096 */
+int fsx_engine_connect_ipc(fsx_engine* e, int peer, const void* blob, uint64_t len);
+/* NCCL baseline transport: 128-byte ncclUniqueId from rank 0, shared by all */
+int fsx_nccl_unique_id(void* id128);
+int fsx_engine_connect_nccl(fsx_engine* e, const void* id128);
+
+/* forward (embedding.hpp:129, 181): ids of this iteration (d_ids_cur, n_cur)
+ * and, for the prioritized engine, of the next one (d_ids_next, n_next; pass
+ * NULL on the final iteration). Writes n_cur x dim rows batch-major to d_out
+ * on `stream` (the caller's compute stream). Host returns once the work is
+ * enqueued; device-side errors surface at fsx_ctx_sync / later calls. */
+int fsx_engine_forward(fsx_engine* e, const uint64_t* d_ids_cur, uint64_t n_cur,
+                       const uint64_t* d_ids_next, uint64_t n_next, void* d_out, void* stream);
+/* backward: n_cur x dim gradients of the last forward, on `stream`. */
+int fsx_engine_backward(fsx_engine* e, const void* d_grads, void* stream);
+/* flush deferred exclusive gradients after the last backward (prioritized) */
+int fsx_engine_finalize(fsx_engine* e, void* stream);
+/* IterationStats of iteration `iter` (embedding.hpp:119-124): [collision_rows,
+ * unique_next_rows, blocking_bytes]; synchronizes. Returns FSX_ERR_OUT_OF_RANGE
+ * past the last forward. */
+int fsx_engine_stats(fsx_engine* e, int iter, uint64_t* out3);
+/* exposed wait of the last iteration: ms the caller's stream spent waiting
+ * on embedding traffic (event pairs around each wait), synchronizes */
+int fsx_engine_exposed_ms(fsx_engine* e, double* ms);
+
+/* ---- load balancer (partition.cpp, sim.hpp) -------------------------------- */
+
+/* K12: CostModel::compute_time_for_lengths (sim.hpp:24-35) for each of
+ * `num_groups` consecutive groups of lengths (group g = lens[offsets[g] ..
+ * offsets[g+1])): h_out[g] = c0 + c1*sum(L) + c2*sum(L^2), bit-exact f64. */
+int fsx_cost_estimate(fsx_ctx* ctx, const uint64_t* d_lens, const uint64_t* h_offsets,
+                      int num_groups, double c0, double c1, double c2, double* h_out,
+                      void* stream);
+
+/* K13: fbs_partition (partition.cpp:157-176). Samples g = 0..m-1 carry
+ * (uih_len, origin_rank, local_index). Outputs: h_assignment[m] (rank of g),
+ * h_order[m] = receive_order flattened rank-major (each rank m/n entries). */
+int fsx_fbs_partition(fsx_ctx* ctx, const uint64_t* h_lens, const int32_t* h_origin,
+                      const int32_t* h_local, uint64_t m, int num_ranks, int32_t* h_assignment,
+                      uint64_t* h_order, void* stream);
+
+/* K14: vbs_partition (partition.cpp:178-209) without autotune state, or with
+ * an initialized one when h_tuned_sizes != NULL (sizes summing to m).
+ * alpha: exact device weights for alpha in {1,2}; otherwise pass the
+ * per-sorted-position weights in h_weights (host std::pow, NULL for 1/2).
+ * h_sizes_out[num_ranks] receives the segment sizes used. */
+int fsx_vbs_partition(fsx_ctx* ctx, const uint64_t* h_lens, const int32_t* h_origin,
+                      const int32_t* h_local, uint64_t m, int num_ranks, double alpha,
+                      const int32_t* h_tuned_sizes, int32_t* h_sizes_out, int32_t* h_assignment,
+                      uint64_t* h_order, void* stream);
+
+/* autotune_update (partition.cpp:211-269) — n <= 64, host f64, no FMA */
+int fsx_autotune_update(int n, int32_t* sizes, double* ema_local, double* ema_global, int step,
+                        double delta, double decay, const double* local_times);
+
+/* ---- raw copy-engine all-to-all (comm.cpp:308-365 analogue) ---------------- */
+/* Each engine also exposes its transport as a plain byte all-to-all over the
+ * engine's windows: send_bytes[d] bytes from d_send + send_offsets[d] go to
+ * rank d; on return d_recv + d * slot_bytes holds what rank d sent here and
+ * h_recv_bytes[d] its size. Collective: every rank calls it. Capacity:
+ * slot_bytes <= the engine's window slot (max_occurrences * 8 * dim... see
+ * fsx_engine_slot_bytes). Used by the balancer's stage-3 sample shuffle. */
+uint64_t fsx_engine_slot_bytes(const fsx_engine* e);
+int fsx_a2a_ce(fsx_engine* e, const void* d_send, const uint64_t* h_send_offsets,
+               const uint64_t* h_send_bytes, void* d_recv, uint64_t slot_bytes,
+               uint64_t* h_recv_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FSX_H */

@@ -1,0 +1,421 @@
+// Hot-path kernels of the embedding shard (K1-K11 in SURVEY §2.3).
+//
+// Layout in HBM: a shard is one row-major [local_rows x dim] array of T
+// (float or double), global row g at local row g / p (embedding.hpp:20-21).
+// Ids are u64; occurrence indices and positions are u32.
+//
+// Roofline: every kernel here is HBM/L2-bandwidth or latency bound; none is a
+// dense contraction (no tensor cores). Row copies use 16-byte vector loads
+// (ld.global.nc.v4) and stores, one warp per row, several rows in flight per
+// warp so each lane keeps >= 4 independent 16-B requests outstanding.
+#pragma once
+
+#include "radix.cuh"
+
+namespace fsx {
+
+// ---- shard geometry on the device -------------------------------------------
+struct ShardGeom {
+  uint64_t total_rows;
+  uint64_t local_rows;
+  uint32_t dim;
+  int p;
+  int shard;
+  __host__ __device__ bool owns(uint64_t g) const {
+    return g < total_rows && static_cast<int>(g % static_cast<uint64_t>(p)) == shard;
+  }
+};
+
+// ---- splitmix64 table init (embedding.cpp:59-64, 108-119) --------------------
+__device__ __forceinline__ uint64_t splitmix(uint64_t& s) {
+  s += 0x9e3779b97f4a7c15ULL;
+  uint64_t z = s;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ double initial_value_dev(uint64_t seed, uint64_t row, uint32_t d) {
+  uint64_t st = seed + row * 0x9e3779b97f4a7c15ULL + (static_cast<uint64_t>(d) + 1) * 0xbf58476d1ce4e5b9ULL;
+  splitmix(st);
+  const double u = __dmul_rn(static_cast<double>(splitmix(st) >> 11), 0x1.0p-53);
+  return __dmul_rn(__dsub_rn(u, 0.5), 0.2);
+}
+
+template <class T>
+__global__ void k_init_table(T* __restrict__ vals, ShardGeom g, uint64_t seed) {
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  const uint64_t wid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const unsigned lane = threadIdx.x & 31u;
+  for (uint64_t l = wid; l < g.local_rows; l += warps) {
+    const uint64_t row = static_cast<uint64_t>(g.shard) + l * static_cast<uint64_t>(g.p);
+    T* dst = vals + l * g.dim;
+    for (uint32_t d = lane; d < g.dim; d += 32) dst[d] = static_cast<T>(initial_value_dev(seed, row, d));
+  }
+}
+
+// ---- vectorised row copy ------------------------------------------------------
+template <int VB>
+struct VecT;
+template <>
+struct VecT<16> { using type = uint4; };
+template <>
+struct VecT<8> { using type = uint2; };
+template <>
+struct VecT<4> { using type = uint32_t; };
+
+__device__ __forceinline__ uint4 ldg_nc(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint2 ldg_nc(const uint2* p) { return __ldg(p); }
+__device__ __forceinline__ uint32_t ldg_nc(const uint32_t* p) { return __ldg(p); }
+// plain (coherent) loads for buffers written earlier in the same kernel chain
+// by another stream / peer: .nc is only safe for data read-only during the
+// kernel, which every caller guarantees.
+
+// Copy `row_bytes` for each item i in [0, n): dst(i) <- src(i). A Map returns
+// nullptr from src() to skip an item. One warp per item, kRowsPerWarp items in
+// flight per warp.
+constexpr int kRowsPerWarp = 4;
+
+template <class Map, int VB>
+__global__ void __launch_bounds__(256) k_copy_rows(Map map, uint64_t n_cap, const uint64_t* d_n,
+                                                   uint32_t row_bytes) {
+  using V = typename VecT<VB>::type;
+  const uint64_t n = scan_n(n_cap, d_n);
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  const uint64_t wid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const unsigned lane = threadIdx.x & 31u;
+  const uint32_t nvec = row_bytes / VB;
+  for (uint64_t i0 = wid * kRowsPerWarp; i0 < n; i0 += warps * kRowsPerWarp) {
+    const V* src[kRowsPerWarp];
+    V* dst[kRowsPerWarp];
+#pragma unroll
+    for (int r = 0; r < kRowsPerWarp; ++r) {
+      const uint64_t i = i0 + r;
+      src[r] = nullptr;
+      dst[r] = nullptr;
+      if (i < n) {
+        src[r] = reinterpret_cast<const V*>(map.src(i));
+        if (src[r]) dst[r] = reinterpret_cast<V*>(map.dst(i));
+      }
+    }
+    for (uint32_t c = lane; c < nvec; c += 32) {
+      V v[kRowsPerWarp];
+#pragma unroll
+      for (int r = 0; r < kRowsPerWarp; ++r)
+        if (src[r]) v[r] = ldg_nc(src[r] + c);
+#pragma unroll
+      for (int r = 0; r < kRowsPerWarp; ++r)
+        if (src[r]) dst[r][c] = v[r];
+    }
+  }
+}
+
+inline int vec_bytes_for(uint32_t row_bytes) {
+  if (row_bytes % 16 == 0) return 16;
+  if (row_bytes % 8 == 0) return 8;
+  return 4;
+}
+
+template <class Map>
+void launch_copy_rows(Ctx* ctx, const Map& map, uint64_t n_cap, const uint64_t* d_n,
+                      uint32_t row_bytes, cudaStream_t s) {
+  if (n_cap == 0) return;
+  const unsigned grid = grid_for(ctx, n_cap, 8 * kRowsPerWarp, 8);
+  switch (vec_bytes_for(row_bytes)) {
+    case 16: FSX_LAUNCH(ctx, (k_copy_rows<Map, 16>), grid, 256, 0, s, map, n_cap, d_n, row_bytes); break;
+    case 8: FSX_LAUNCH(ctx, (k_copy_rows<Map, 8>), grid, 256, 0, s, map, n_cap, d_n, row_bytes); break;
+    default: FSX_LAUNCH(ctx, (k_copy_rows<Map, 4>), grid, 256, 0, s, map, n_cap, d_n, row_bytes); break;
+  }
+}
+
+// lookup (embedding.cpp:139-146): out[k] = row(ids[k]); bad ids flagged.
+struct GatherByIdMap {
+  const char* table;
+  const uint64_t* ids;
+  char* out;
+  uint32_t row_bytes;
+  ShardGeom g;
+  DevErr* err;
+  __device__ const char* src(uint64_t i) const {
+    const uint64_t id = ids[i];
+    if (!g.owns(id)) {
+      report(err, id >= g.total_rows ? kErrRowRange : kErrNotOwned, id,
+             id >= g.total_rows ? g.total_rows : static_cast<unsigned long long>(g.shard));
+      return nullptr;
+    }
+    return table + (id / static_cast<uint64_t>(g.p)) * row_bytes;
+  }
+  __device__ char* dst(uint64_t i) const { return out + i * row_bytes; }
+};
+
+// ---- sort + unique -----------------------------------------------------------
+// After a stable sort: flag the first occurrence of each key, emit the unique
+// keys, segment starts and every item's slot.
+template <class K>
+struct UniqueOp {
+  static constexpr int NC = 1;
+  const K* keys;          // sorted
+  const uint32_t* perm;   // sorted payload (original index), nullable
+  const uint64_t* d_n;    // live item count (device)
+  uint64_t* uniq;         // nullable: unique keys (widened)
+  uint64_t* uniq_g;       // nullable: unique keys mapped key*mul + add
+  uint64_t mul, add;
+  uint32_t* seg_start;    // nullable, capacity U+1
+  uint32_t* inverse;      // nullable: inverse[perm[k]] = slot
+  __device__ void count(uint64_t k, uint32_t (&c)[1]) const {
+    c[0] = (k == 0 || keys[k] != keys[k - 1]) ? 1u : 0u;
+  }
+  __device__ void emit(uint64_t k, const uint32_t (&ex)[1], const uint32_t (&c)[1]) const {
+    const uint32_t slot = ex[0] + c[0] - 1;
+    if (c[0]) {
+      const uint64_t key = static_cast<uint64_t>(keys[k]);
+      if (uniq) uniq[slot] = key;
+      if (uniq_g) uniq_g[slot] = key * mul + add;
+      if (seg_start) seg_start[slot] = static_cast<uint32_t>(k);
+    }
+    if (inverse) inverse[perm ? perm[k] : k] = slot;
+    if (seg_start && k + 1 == *d_n) seg_start[slot + 1] = static_cast<uint32_t>(k + 1);
+  }
+};
+
+// ---- owner partition (route_to_shard_major requester half, :194-204) --------
+template <int NC_>
+struct OwnerPartitionOp {
+  static constexpr int NC = NC_;
+  static_assert(NC <= 16, "world too large");
+  const uint64_t* ids;
+  uint64_t total_rows;
+  int p;
+  const uint64_t* totals;  // filled by the scan's phase 2 before emit runs
+  uint64_t* send_ids;
+  uint32_t* send_pos;
+  DevErr* err;
+  __device__ void count(uint64_t i, uint32_t (&c)[NC]) const {
+    const uint64_t id = ids[i];
+    const int o = static_cast<int>(id % static_cast<uint64_t>(p));
+#pragma unroll
+    for (int q = 0; q < NC; ++q) c[q] = (q == o && id < total_rows) ? 1u : 0u;
+  }
+  __device__ void emit(uint64_t i, const uint32_t (&ex)[NC], const uint32_t (&c)[NC]) const {
+    const uint64_t id = ids[i];
+    if (id >= total_rows) {
+      report(err, kErrRowRange, id, total_rows);
+      return;
+    }
+    const int o = static_cast<int>(id % static_cast<uint64_t>(p));
+    uint64_t base = 0;
+    for (int q = 0; q < o; ++q) base += totals[q];
+    uint32_t r = 0;
+#pragma unroll
+    for (int q = 0; q < NC; ++q)
+      if (q == o) r = ex[q];
+    send_ids[base + r] = id;
+    send_pos[base + r] = static_cast<uint32_t>(i);
+  }
+};
+
+// ---- collision (embedding.cpp:82-93) -----------------------------------------
+// a, b sorted unique. flag_a[i] = a[i] in b; flag_b[j] = b[j] in a.
+__global__ void k_intersect_flags(const uint64_t* __restrict__ a, const uint64_t* d_na,
+                                  const uint64_t* __restrict__ b, const uint64_t* d_nb,
+                                  uint8_t* __restrict__ flag_a, uint8_t* __restrict__ flag_b);
+
+// compaction of a sorted list by a byte flag: out_true / out_false keep order
+struct SplitByFlagOp {
+  static constexpr int NC = 2;
+  const uint64_t* v;
+  const uint8_t* flag;
+  uint64_t* out_true;   // nullable
+  uint64_t* out_false;  // nullable
+  __device__ void count(uint64_t i, uint32_t (&c)[2]) const {
+    const uint32_t f = flag[i] ? 1u : 0u;
+    c[0] = f;
+    c[1] = 1u - f;
+  }
+  __device__ void emit(uint64_t i, const uint32_t (&ex)[2], const uint32_t (&c)[2]) const {
+    if (c[0]) {
+      if (out_true) out_true[ex[0]] = v[i];
+    } else if (out_false) {
+      out_false[ex[1]] = v[i];
+    }
+  }
+};
+
+// ---- deterministic segmented reduce + SGD (embedding.cpp:148-181) -------------
+// Rows are segments of a stable sort of occurrences by id, so within a segment
+// occurrences are in (source rank, position) order. Each row's gradient is
+// summed in f64 in that order (chunk == 0), or, for rows longer than `chunk`
+// occurrences, as ceil(len/chunk) sequential chunk sums added in chunk order
+// (fixed association, identical in both engine modes). Then
+//   row = row - lr * acc      (f64, no FMA; one rounding to T for f32 tables)
+// and a non-finite result is flagged.
+// Gradient row of occurrence j: base + src_off(j) + idx(j) * row_bytes. With
+// occ_src == nullptr and occ_idx == nullptr this is a plain [M x dim] array.
+template <class T>
+struct GradRows {
+  const char* base;
+  uint64_t slot_bytes;      // stride between per-source receive slots
+  const uint8_t* occ_src;   // nullable: source slot of occurrence j
+  const uint32_t* occ_idx;  // nullable: row of occurrence j inside its slot
+  uint32_t row_bytes;
+  __device__ __forceinline__ const T* row(uint32_t j) const {
+    const uint64_t off = occ_src ? static_cast<uint64_t>(occ_src[j]) * slot_bytes : 0;
+    const uint64_t r = occ_idx ? occ_idx[j] : j;
+    return reinterpret_cast<const T*>(base + off + r * row_bytes);
+  }
+};
+
+struct RowSegments {
+  const uint64_t* uniq_local;  // sorted local row index per slot
+  const uint32_t* seg_start;   // [U+1] into the sorted occurrence order
+  const uint32_t* perm;        // sorted position -> occurrence j
+  const uint64_t* d_u;         // live row count U (device)
+  const uint8_t* select;       // nullable: update only rows with select[u] == want
+  uint8_t want;
+};
+
+// Work list: every selected row contributes ceil(len / chunk) items (1 when
+// chunk == 0); multi-chunk rows are also listed for the combine pass.
+struct SgdPlanOp {
+  static constexpr int NC = 2;
+  RowSegments rs;
+  uint32_t chunk;
+  uint2* work;          // (row, chunk index)
+  uint32_t* multi;      // rows with > 1 chunk
+  uint32_t* part_base;  // first work item of row u (indexes partials)
+  __device__ uint32_t nchunks(uint64_t u) const {
+    if (rs.select && rs.select[u] != rs.want) return 0;
+    const uint32_t len = rs.seg_start[u + 1] - rs.seg_start[u];
+    if (chunk == 0 || len <= chunk) return 1;
+    return (len + chunk - 1) / chunk;
+  }
+  __device__ void count(uint64_t u, uint32_t (&c)[2]) const {
+    const uint32_t k = nchunks(u);
+    c[0] = k;
+    c[1] = k > 1 ? 1u : 0u;
+  }
+  __device__ void emit(uint64_t u, const uint32_t (&ex)[2], const uint32_t (&c)[2]) const {
+    for (uint32_t q = 0; q < c[0]; ++q) work[ex[0] + q] = make_uint2(static_cast<uint32_t>(u), q);
+    if (c[1]) {
+      multi[ex[1]] = static_cast<uint32_t>(u);
+      part_base[u] = ex[0];
+    }
+  }
+};
+
+template <class T>
+struct SgdArgs {
+  T* table;
+  ShardGeom g;
+  double lr;
+  RowSegments rs;
+  GradRows<T> gr;
+  uint32_t chunk;
+  const uint2* work;
+  const uint64_t* d_work_n;   // device: number of work items (scan total 0)
+  const uint32_t* multi;
+  const uint64_t* d_multi_n;  // device: number of multi-chunk rows (scan total 1)
+  const uint32_t* part_base;
+  double* partials;           // [work items x dim] f64
+  T* rows_out;                // nullable: post-update rows by slot [U x dim]
+  DevErr* err;
+};
+
+template <class T>
+__device__ __forceinline__ void sgd_apply(const SgdArgs<T>& a, uint32_t u, uint32_t d, double acc) {
+  const uint64_t l = a.rs.uniq_local[u];
+  if (l >= a.g.local_rows) return;  // never write outside the shard
+  T* cell = a.table + l * a.g.dim + d;
+  const double v = __dsub_rn(static_cast<double>(*cell), __dmul_rn(a.lr, acc));
+  const T out = static_cast<T>(v);
+  *cell = out;
+  if (a.rows_out) a.rows_out[static_cast<uint64_t>(u) * a.g.dim + d] = out;
+  if (!isfinite(static_cast<double>(out)))
+    report(a.err, kErrNonFinite, l * static_cast<uint64_t>(a.g.p) + a.g.shard, 0);
+}
+
+// One warp per work item; lanes stride the dimension; the occurrence loop is
+// unrolled 4-wide (independent loads first, then the in-order f64 adds).
+template <class T>
+__global__ void __launch_bounds__(256) k_sgd_chunks(SgdArgs<T> a) {
+  const uint64_t nwork = *a.d_work_n;
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  const uint64_t wid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const unsigned lane = threadIdx.x & 31u;
+  const uint32_t dim = a.g.dim;
+  for (uint64_t w = wid; w < nwork; w += warps) {
+    const uint2 item = a.work[w];
+    const uint32_t u = item.x;
+    const uint32_t s = a.rs.seg_start[u], e = a.rs.seg_start[u + 1];
+    const bool single = a.chunk == 0 || e - s <= a.chunk;
+    const uint32_t kb = single ? s : s + item.y * a.chunk;
+    const uint32_t ke = single ? e : min(e, kb + a.chunk);
+    for (uint32_t d0 = 0; d0 < dim; d0 += 32 * 4) {
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      uint32_t k = kb;
+      for (; k + 4 <= ke; k += 4) {
+        const T* g[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) g[q] = a.gr.row(a.rs.perm[k + q]);
+        T v[4][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint32_t d = d0 + c * 32 + lane;
+            v[q][c] = d < dim ? g[q][d] : T(0);
+          }
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[c] = __dadd_rn(acc[c], static_cast<double>(v[q][c]));
+      }
+      for (; k < ke; ++k) {
+        const T* g = a.gr.row(a.rs.perm[k]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t d = d0 + c * 32 + lane;
+          if (d < dim) acc[c] = __dadd_rn(acc[c], static_cast<double>(g[d]));
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const uint32_t d = d0 + c * 32 + lane;
+        if (d >= dim) continue;
+        if (single) {
+          sgd_apply(a, u, d, acc[c]);
+        } else {
+          a.partials[w * dim + d] = acc[c];
+        }
+      }
+    }
+  }
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) k_sgd_combine(SgdArgs<T> a) {
+  const uint64_t nm = *a.d_multi_n;
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  const uint64_t wid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const unsigned lane = threadIdx.x & 31u;
+  const uint32_t dim = a.g.dim;
+  for (uint64_t m = wid; m < nm; m += warps) {
+    const uint32_t u = a.multi[m];
+    const uint32_t len = a.rs.seg_start[u + 1] - a.rs.seg_start[u];
+    const uint32_t nch = (len + a.chunk - 1) / a.chunk;
+    const uint64_t b = a.part_base[u];
+    for (uint32_t d = lane; d < dim; d += 32) {
+      double acc = 0.0;
+      for (uint32_t q = 0; q < nch; ++q) acc = __dadd_rn(acc, a.partials[(b + q) * dim + d]);
+      sgd_apply(a, u, d, acc);
+    }
+  }
+}
+
+}  // namespace fsx

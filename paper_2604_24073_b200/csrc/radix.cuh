@@ -1,0 +1,162 @@
+// Stable LSD radix sort of (key, u32 payload) pairs, 8-bit digits.
+//
+// Per digit pass, three launches:
+//   k_radix_hist    per-2048-key tile digit histogram; equal digits inside a
+//                   warp are aggregated with __match_any_sync so Zipf-hot keys
+//                   cost one shared atomic per warp, not one per key
+//   k_scan_u32      exclusive scan of the [digit][tile] count table (one CTA)
+//   k_radix_scatter stable rank inside the tile: each warp walks its
+//                   contiguous 256-key chunk in 32-key rounds; match_any gives
+//                   the equal-digit peers, popc(peers & lanemask_lt) the rank
+//                   among them, a per-warp shared counter the running offset;
+//                   a per-digit prefix over warps then orders the warps.
+// Stability (index order is preserved inside every digit bucket) is what makes
+// the owner's per-row gradient order equal the reference's (source, position)
+// order (embedding.cpp:159-166).
+// Only the significant bits are sorted: callers pass nbits (e.g. 27 for the
+// local row index of an 80M-row shard), giving ceil(nbits/8) passes.
+#pragma once
+
+#include "scan.cuh"
+
+namespace fsx {
+
+constexpr int kRadixThreads = 256;
+constexpr int kRadixWarps = kRadixThreads / 32;
+constexpr int kRadixWarpItems = 256;  // per warp per tile
+constexpr int kRadixTile = kRadixWarps * kRadixWarpItems;
+constexpr int kRadixRounds = kRadixWarpItems / 32;
+
+template <class K>
+__global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const K* __restrict__ keys,
+                                                              uint64_t n_cap, const uint64_t* d_n,
+                                                              int shift, uint32_t* counts,
+                                                              unsigned tiles) {
+  __shared__ uint32_t hist[256];
+  const uint64_t n = scan_n(n_cap, d_n);
+  hist[threadIdx.x] = 0;
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kRadixTile + warp * kRadixWarpItems;
+#pragma unroll 4
+  for (int r = 0; r < kRadixRounds; ++r) {
+    const uint64_t i = base + r * 32 + lane;
+    const unsigned d = i < n ? static_cast<unsigned>((keys[i] >> shift) & 0xffu) : 256u;
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    if (d < 256u && (peers & lanemask_lt()) == 0) atomicAdd(&hist[d], __popc(peers));
+  }
+  __syncthreads();
+  counts[static_cast<uint64_t>(threadIdx.x) * tiles + blockIdx.x] = hist[threadIdx.x];
+}
+
+template <class K>
+__global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(
+    const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
+    uint32_t* __restrict__ vout, uint64_t n_cap, const uint64_t* d_n, int shift,
+    const uint32_t* __restrict__ offsets, unsigned tiles) {
+  __shared__ uint32_t wcount[kRadixWarps][256];
+  __shared__ uint32_t tile_off[256];
+  const uint64_t n = scan_n(n_cap, d_n);
+  const uint64_t tile_base = static_cast<uint64_t>(blockIdx.x) * kRadixTile;
+  if (tile_base >= n) return;
+  for (int w = 0; w < kRadixWarps; ++w) wcount[w][threadIdx.x] = 0;
+  tile_off[threadIdx.x] = offsets[static_cast<uint64_t>(threadIdx.x) * tiles + blockIdx.x];
+  __syncthreads();
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const uint64_t base = tile_base + warp * kRadixWarpItems;
+  K k[kRadixRounds];
+  uint32_t v[kRadixRounds], rk[kRadixRounds];
+  unsigned dg[kRadixRounds];
+#pragma unroll
+  for (int r = 0; r < kRadixRounds; ++r) {
+    const uint64_t i = base + r * 32 + lane;
+    const bool valid = i < n;
+    k[r] = valid ? kin[i] : K(0);
+    v[r] = valid ? (vin ? vin[i] : static_cast<uint32_t>(i)) : 0u;
+    dg[r] = valid ? static_cast<unsigned>((k[r] >> shift) & 0xffu) : 256u;
+  }
+#pragma unroll
+  for (int r = 0; r < kRadixRounds; ++r) {
+    const unsigned d = dg[r];
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const unsigned before = __popc(peers & lanemask_lt());
+    uint32_t run = d < 256u ? wcount[warp][d] : 0u;
+    rk[r] = run + before;
+    __syncwarp();
+    if (d < 256u && before == 0) wcount[warp][d] = run + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  {
+    uint32_t run = 0;
+    for (int w = 0; w < kRadixWarps; ++w) {
+      uint32_t x = wcount[w][threadIdx.x];
+      wcount[w][threadIdx.x] = run;
+      run += x;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kRadixRounds; ++r) {
+    const unsigned d = dg[r];
+    if (d < 256u) {
+      const uint32_t pos = tile_off[d] + wcount[warp][d] + rk[r];
+      kout[pos] = k[r];
+      vout[pos] = v[r];
+    }
+  }
+}
+
+struct RadixScratch {
+  DevBuf<uint32_t> counts;
+};
+
+// Sorts (keys, vals) by bits [0, nbits) stably. `vals` may be null: payload
+// is then the input index. Ping-pongs between (k0,v0) and (k1,v1); returns
+// the pair holding the result via out pointers. n_cap sizes the grid, d_n is
+// the live count (nullable).
+template <class K>
+void radix_sort_pairs(Ctx* ctx, K* k0, uint32_t* v0, K* k1, uint32_t* v1, uint64_t n_cap,
+                      const uint64_t* d_n, int nbits, RadixScratch& s, cudaStream_t stream,
+                      K** k_out, uint32_t** v_out, const uint32_t* v_init = nullptr) {
+  if (nbits < 1) nbits = 1;
+  const int passes = (nbits + 7) / 8;
+  const unsigned tiles = ceil_div(n_cap > 0 ? n_cap : 1, kRadixTile);
+  s.counts.ensure(static_cast<size_t>(tiles) * 256);
+  K* kin = k0;
+  K* kout = k1;
+  const uint32_t* vin = v_init;
+  uint32_t* vbuf_in = v0;
+  uint32_t* vout = v1;
+  if (n_cap == 0) {
+    *k_out = k0;
+    *v_out = v0;
+    return;
+  }
+  for (int p = 0; p < passes; ++p) {
+    const int shift = 8 * p;
+    FSX_LAUNCH(ctx, k_radix_hist<K>, tiles, kRadixThreads, 0, stream, kin, n_cap, d_n, shift,
+               s.counts.p, tiles);
+    FSX_LAUNCH(ctx, k_scan_u32, 1, 1024, 0, stream, s.counts.p, static_cast<uint64_t>(tiles) * 256);
+    FSX_LAUNCH(ctx, k_radix_scatter<K>, tiles, kRadixThreads, 0, stream, kin, vin, kout, vout,
+               n_cap, d_n, shift, s.counts.p, tiles);
+    // next pass reads what this one wrote
+    K* kt = kin;
+    kin = kout;
+    kout = kt;
+    vin = vout;
+    uint32_t* vt = vbuf_in;
+    vbuf_in = vout;
+    vout = vt;
+  }
+  *k_out = kin;
+  *v_out = vbuf_in;
+}
+
+inline int bits_for(uint64_t max_value) {
+  int b = 0;
+  while (b < 64 && (max_value >> b) != 0) ++b;
+  return b > 0 ? b : 1;
+}
+
+}  // namespace fsx

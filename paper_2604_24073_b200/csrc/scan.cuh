@@ -1,0 +1,233 @@
+// Multi-counter stream compaction / exclusive scan.
+//
+// Most hot-path bookkeeping is "for every item, emit it at its rank among the
+// items of the same category": unique-after-sort, owner compaction, per-source
+// pack lists, co/ex gradient splits. One primitive covers them all: an Op gives
+// each item a small vector of NC counts; the primitive computes, for every
+// item, the exclusive prefix of those vectors over the item order and calls
+// Op::emit with it. Three launches, no host round trip, no spin waits:
+//   1. k_tile_reduce : per-tile sums            (one CTA per 2048-item tile)
+//   2. k_scan_tiles  : exclusive scan of tile sums + grand totals (one CTA)
+//   3. k_tile_emit   : re-count, block scan (warp shuffles), emit
+// Item counts may live on the device (d_n); grids are sized by capacity and
+// tiles beyond *d_n exit early, so chains of these never need a host sync.
+#pragma once
+
+#include "common.cuh"
+
+namespace fsx {
+
+constexpr int kScanThreads = 256;
+constexpr int kScanIPT = 8;
+constexpr int kScanTile = kScanThreads * kScanIPT;
+
+__device__ __forceinline__ uint64_t scan_n(uint64_t n_cap, const uint64_t* d_n) {
+  if (d_n == nullptr) return n_cap;
+  uint64_t n = *d_n;
+  return n < n_cap ? n : n_cap;
+}
+
+// Block-wide exclusive scan of NC counters held by each thread; returns the
+// exclusive prefix in `v` and the block total in `total`.
+template <int NC>
+__device__ __forceinline__ void block_exclusive_scan(uint32_t (&v)[NC], uint32_t (&total)[NC]) {
+  __shared__ uint32_t warp_tot[kScanThreads / 32][NC];
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint32_t incl[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    uint32_t x = v[c];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= static_cast<unsigned>(o)) x += y;
+    }
+    incl[c] = x;
+  }
+  if (lane == 31) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) warp_tot[warp][c] = incl[c];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    uint32_t before = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < kScanThreads / 32; ++w) {
+      uint32_t t = warp_tot[w][c];
+      if (w < static_cast<int>(warp)) before += t;
+      all += t;
+    }
+    v[c] = before + incl[c] - v[c];
+    total[c] = all;
+  }
+  __syncthreads();
+}
+
+template <class Op>
+__global__ void __launch_bounds__(kScanThreads) k_tile_reduce(Op op, uint64_t n_cap,
+                                                              const uint64_t* d_n,
+                                                              uint32_t* tile_sums) {
+  constexpr int NC = Op::NC;
+  const uint64_t n = scan_n(n_cap, d_n);
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile;
+  uint32_t acc[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) acc[c] = 0;
+  if (base < n) {
+    const uint64_t first = base + static_cast<uint64_t>(threadIdx.x) * kScanIPT;
+#pragma unroll
+    for (int q = 0; q < kScanIPT; ++q) {
+      const uint64_t i = first + q;
+      if (i < n) {
+        uint32_t cnt[NC];
+        op.count(i, cnt);
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[c] += cnt[c];
+      }
+    }
+  }
+  uint32_t total[NC];
+  block_exclusive_scan<NC>(acc, total);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int c = 0; c < NC; ++c) tile_sums[static_cast<uint64_t>(blockIdx.x) * NC + c] = total[c];
+  }
+}
+
+// Block-wide (1024 threads) exclusive scan of one u32 per thread; returns
+// the block total.
+__device__ __forceinline__ uint32_t block1024_exclusive(uint32_t& v) {
+  __shared__ uint32_t wt[32];
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= static_cast<unsigned>(o)) x += y;
+  }
+  if (lane == 31) wt[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t t = lane < (blockDim.x >> 5) ? wt[lane] : 0;
+    uint32_t s = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= static_cast<unsigned>(o)) s += y;
+    }
+    wt[lane] = s - t;  // exclusive base of warp `lane`
+  }
+  __syncthreads();
+  uint32_t excl = wt[warp] + x - v;
+  __shared__ uint32_t total;
+  if (threadIdx.x == blockDim.x - 1) total = excl + v;
+  __syncthreads();
+  uint32_t tot = total;
+  v = excl;
+  __syncthreads();
+  return tot;
+}
+
+// One CTA: in-place exclusive scan of n u32 (each thread a contiguous chunk).
+// Returns nothing; used for radix tile-offset tables.
+__global__ void __launch_bounds__(1024) k_scan_u32(uint32_t* data, uint64_t n) {
+  const uint64_t per = (n + blockDim.x - 1) / blockDim.x;
+  const uint64_t lo = threadIdx.x * per;
+  const uint64_t hi = lo + per < n ? lo + per : n;
+  uint32_t s = 0;
+  for (uint64_t t = lo; t < hi; ++t) s += data[t];
+  block1024_exclusive(s);
+  for (uint64_t t = lo; t < hi; ++t) {
+    uint32_t x = data[t];
+    data[t] = s;
+    s += x;
+  }
+}
+
+// One CTA: exclusive scan over `tiles` rows of NC counters (in place), grand
+// totals to `totals` (device) as u64.
+template <int NC>
+__global__ void __launch_bounds__(1024) k_scan_tiles(uint32_t* tile_sums, unsigned tiles,
+                                                     uint64_t* totals) {
+  const unsigned per = (tiles + blockDim.x - 1) / blockDim.x;
+  const unsigned lo = threadIdx.x * per;
+  const unsigned hi = min(tiles, lo + per);
+  for (int c = 0; c < NC; ++c) {
+    uint32_t s = 0;
+    for (unsigned t = lo; t < hi; ++t) s += tile_sums[static_cast<uint64_t>(t) * NC + c];
+    const uint32_t tot = block1024_exclusive(s);
+    if (totals && threadIdx.x == 0) totals[c] = tot;
+    for (unsigned t = lo; t < hi; ++t) {
+      uint32_t x = tile_sums[static_cast<uint64_t>(t) * NC + c];
+      tile_sums[static_cast<uint64_t>(t) * NC + c] = s;
+      s += x;
+    }
+  }
+}
+
+template <class Op>
+__global__ void __launch_bounds__(kScanThreads) k_tile_emit(Op op, uint64_t n_cap,
+                                                            const uint64_t* d_n,
+                                                            const uint32_t* tile_prefix) {
+  constexpr int NC = Op::NC;
+  const uint64_t n = scan_n(n_cap, d_n);
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile;
+  if (base >= n) return;  // whole CTA exits together: no barrier hazard
+  const uint64_t first = base + static_cast<uint64_t>(threadIdx.x) * kScanIPT;
+  uint32_t run[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) run[c] = 0;
+#pragma unroll
+  for (int q = 0; q < kScanIPT; ++q) {
+    const uint64_t i = first + q;
+    if (i < n) {
+      uint32_t cnt[NC];
+      op.count(i, cnt);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) run[c] += cnt[c];
+    }
+  }
+  uint32_t total[NC];
+  block_exclusive_scan<NC>(run, total);
+#pragma unroll
+  for (int c = 0; c < NC; ++c) run[c] += tile_prefix[static_cast<uint64_t>(blockIdx.x) * NC + c];
+#pragma unroll
+  for (int q = 0; q < kScanIPT; ++q) {
+    const uint64_t i = first + q;
+    if (i < n) {
+      uint32_t cnt[NC];
+      op.count(i, cnt);
+      op.emit(i, run, cnt);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) run[c] += cnt[c];
+    }
+  }
+}
+
+// Scratch for one scan of up to `n_cap` items with NC counters.
+struct ScanScratch {
+  DevBuf<uint32_t> tiles;
+  void ensure(uint64_t n_cap, int nc) {
+    tiles.ensure(static_cast<size_t>(ceil_div(n_cap > 0 ? n_cap : 1, kScanTile)) * nc);
+  }
+};
+
+// Run the three phases on `stream`. d_totals (nullable, device, NC u64) gets
+// the grand totals. n_cap bounds the grid; d_n (nullable) is the live count.
+template <class Op>
+void run_scan(Ctx* ctx, const Op& op, uint64_t n_cap, const uint64_t* d_n, ScanScratch& s,
+              uint64_t* d_totals, cudaStream_t stream) {
+  constexpr int NC = Op::NC;
+  if (n_cap == 0) {
+    if (d_totals) FSX_CUDA(cudaMemsetAsync(d_totals, 0, sizeof(uint64_t) * NC, stream));
+    return;
+  }
+  s.ensure(n_cap, NC);
+  const unsigned tiles = ceil_div(n_cap, kScanTile);
+  FSX_LAUNCH(ctx, k_tile_reduce<Op>, tiles, kScanThreads, 0, stream, op, n_cap, d_n, s.tiles.p);
+  FSX_LAUNCH(ctx, k_scan_tiles<NC>, 1, 1024, 0, stream, s.tiles.p, tiles, d_totals);
+  FSX_LAUNCH(ctx, k_tile_emit<Op>, tiles, kScanThreads, 0, stream, op, n_cap, d_n, s.tiles.p);
+}
+
+}  // namespace fsx

@@ -1,0 +1,63 @@
+// One shard of a row-wise sharded embedding table on the device (ShardView,
+// embedding.hpp:59-90) and its update machinery.
+#pragma once
+
+#include "sorter.cuh"
+
+namespace fsx {
+
+struct SgdScratch {
+  DevBuf<uint2> work;
+  DevBuf<uint32_t> multi, part_base;
+  DevBuf<double> partials;
+  DevBuf<uint64_t> d_tot;  // [0] work items, [1] multi rows
+  ScanScratch scan;
+  uint64_t cap_rows = 0, cap_work = 0;
+  uint32_t dim = 0;
+  void reserve(uint64_t rows, uint64_t occ, uint32_t d, uint32_t chunk) {
+    const uint64_t w = rows + (chunk ? occ / chunk + 1 : 0);
+    if (rows > cap_rows || w > cap_work || d != dim) {
+      cap_rows = rows > cap_rows ? rows : cap_rows;
+      cap_work = w > cap_work ? w : cap_work;
+      dim = d;
+      work.alloc(cap_work); multi.alloc(cap_rows); part_base.alloc(cap_rows);
+      partials.alloc(chunk ? cap_work * d : 1);
+    }
+    if (!d_tot.p) d_tot.alloc(2);
+  }
+};
+
+struct Table {
+  Ctx* ctx = nullptr;
+  ShardGeom g{};
+  int dtype = FSX_F32;
+  double lr = 0.0;
+  uint64_t seed = 0;
+  void* values = nullptr;
+  size_t elem = 4;
+  uint32_t row_bytes() const { return static_cast<uint32_t>(g.dim * elem); }
+  int key_bits() const { return bits_for(g.local_rows > 0 ? g.local_rows - 1 : 0); }
+
+  ~Table() {
+    if (values) cudaFree(values);
+  }
+};
+
+// Segmented deterministic SGD over the rows of `rs` (selected rows only),
+// gradients from `gr`. Issues plan scan + chunk kernel + combine kernel.
+template <class T>
+void sgd_update_rows(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_cap,
+                     uint64_t occ_cap, const GradRows<T>& gr, uint32_t chunk, SgdScratch& s,
+                     T* rows_out, cudaStream_t stream) {
+  if (rows_cap == 0) return;
+  s.reserve(rows_cap, occ_cap, t.g.dim, chunk);
+  SgdPlanOp plan{rs, chunk, s.work.p, s.multi.p, s.part_base.p};
+  run_scan(ctx, plan, rows_cap, rs.d_u, s.scan, s.d_tot.p, stream);
+  SgdArgs<T> a{static_cast<T*>(t.values), t.g, t.lr, rs, gr, chunk, s.work.p, s.d_tot.p,
+               s.multi.p, s.d_tot.p + 1, s.part_base.p, s.partials.p, rows_out, ctx->d_err};
+  const uint64_t work_cap = rows_cap + (chunk ? occ_cap / chunk + 1 : 0);
+  FSX_LAUNCH(ctx, k_sgd_chunks<T>, grid_for(ctx, work_cap, 8, 16), 256, 0, stream, a);
+  if (chunk) FSX_LAUNCH(ctx, k_sgd_combine<T>, grid_for(ctx, rows_cap, 8, 8), 256, 0, stream, a);
+}
+
+}  // namespace fsx

@@ -1,0 +1,272 @@
+"""Python mirror of the reference embedding API (proj/include/freescale/
+embedding.hpp) over libfsx's C ABI. Same names, argument meaning and error
+classes as the C++ reference, so the parity tests read like its own tests
+(tests/test_embedding.cpp). All computation runs in libfsx's CUDA kernels;
+torch is only used for device memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import InvalidArgument, ProtocolError
+
+_DTYPES = {"f32": (_lib.FSX_F32, torch.float32), "f64": (_lib.FSX_F64, torch.float64)}
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _dev_u64(x, device) -> torch.Tensor:
+    if isinstance(x, torch.Tensor):
+        t = x.to(device=device, dtype=torch.int64)
+    else:
+        a = np.ascontiguousarray(np.asarray(x, dtype=np.uint64).reshape(-1))
+        t = torch.from_numpy(a.view(np.int64)).to(device)
+    return t.contiguous()
+
+
+def _np_u64(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().numpy().view(np.uint64).copy()
+
+
+@dataclass(frozen=True)
+class TableGeometry:
+    """embedding.hpp:13-26: row g lives on shard g mod p at local index g div p."""
+    total_rows: int = 0
+    dim: int = 1
+    num_shards: int = 1
+
+    def owner(self, g: int) -> int:
+        return int(g % self.num_shards)
+
+    def local_index(self, g: int) -> int:
+        return int(g // self.num_shards)
+
+    def local_rows(self, shard: int) -> int:
+        return (self.total_rows - 1 - shard) // self.num_shards + 1 if self.total_rows > shard else 0
+
+
+class Context:
+    """One libfsx context (= one rank on one GPU)."""
+
+    def __init__(self, device: int = 0, rank: int = 0, world: int = 1):
+        self.device = device
+        self.rank = rank
+        self.world = world
+        h = C.c_void_p()
+        _lib.call("fsx_ctx_create", device, rank, world, C.byref(h))
+        self.h = h
+
+    @property
+    def torch_device(self) -> torch.device:
+        return torch.device("cuda", self.device)
+
+    def sync(self) -> None:
+        _lib.call("fsx_ctx_sync", self.h)
+
+    def launches(self) -> int:
+        return int(_lib.lib().fsx_ctx_launches(self.h))
+
+    def close(self) -> None:
+        if self.h:
+            _lib.lib().fsx_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+_default_ctx: dict[int, Context] = {}
+
+
+def default_context(device: int | None = None) -> Context:
+    dev = torch.cuda.current_device() if device is None else device
+    if dev not in _default_ctx:
+        _default_ctx[dev] = Context(dev)
+    return _default_ctx[dev]
+
+
+@dataclass
+class CollisionSplit:
+    """embedding.hpp:45-49"""
+    collision: np.ndarray
+    exclusive_cur: np.ndarray
+    exclusive_next: np.ndarray
+
+
+def sorted_unique(ids, ctx: Context | None = None) -> tuple[np.ndarray, np.ndarray]:
+    """sorted_unique (embedding.cpp:12-16) on the device; also each input's slot."""
+    ctx = ctx or default_context()
+    d = _dev_u64(ids, ctx.torch_device)
+    n = d.numel()
+    out = torch.empty(max(n, 1), dtype=torch.int64, device=d.device)
+    inv = torch.empty(max(n, 1), dtype=torch.int32, device=d.device)
+    nu = C.c_uint64()
+    _lib.call("fsx_sort_unique_u64", ctx.h, _ptr(d), n, _ptr(out), _ptr(inv), C.byref(nu), _stream())
+    return _np_u64(out[:nu.value]), inv[:n].cpu().numpy().astype(np.uint32)
+
+
+def compute_collision(cur, nxt, ctx: Context | None = None) -> CollisionSplit:
+    """compute_collision (embedding.cpp:82-93) on two shard-major id lists."""
+    ctx = ctx or default_context()
+    a = _dev_u64(cur, ctx.torch_device)
+    b = _dev_u64(nxt, ctx.torch_device)
+    co = torch.empty(max(a.numel(), 1), dtype=torch.int64, device=a.device)
+    exc = torch.empty(max(a.numel(), 1), dtype=torch.int64, device=a.device)
+    exn = torch.empty(max(b.numel(), 1), dtype=torch.int64, device=a.device)
+    cnt = (C.c_uint64 * 5)()
+    _lib.call("fsx_collision_split", ctx.h, _ptr(a), a.numel(), _ptr(b), b.numel(), _ptr(co),
+              _ptr(exc), _ptr(exn), cnt, _stream())
+    return CollisionSplit(_np_u64(co[:cnt[0]]), _np_u64(exc[:cnt[1]]), _np_u64(exn[:cnt[2]]))
+
+
+def collision_pct(cur, nxt, ctx: Context | None = None) -> float:
+    """collision_pct (embedding.cpp:95-104)."""
+    ctx = ctx or default_context()
+    a = _dev_u64(cur, ctx.torch_device)
+    b = _dev_u64(nxt, ctx.torch_device)
+    co = torch.empty(max(a.numel(), 1), dtype=torch.int64, device=a.device)
+    exc = torch.empty(max(a.numel(), 1), dtype=torch.int64, device=a.device)
+    exn = torch.empty(max(b.numel(), 1), dtype=torch.int64, device=a.device)
+    cnt = (C.c_uint64 * 5)()
+    _lib.call("fsx_collision_split", ctx.h, _ptr(a), a.numel(), _ptr(b), b.numel(), _ptr(co),
+              _ptr(exc), _ptr(exn), cnt, _stream())
+    if cnt[4] == 0:
+        raise InvalidArgument("collision_pct: next iteration uses no rows")
+    return cnt[0] / cnt[4]
+
+
+def route_by_owner(ids, total_rows: int, num_shards: int, ctx: Context | None = None):
+    """Requester half of route_to_shard_major (embedding.cpp:194-204): per owner,
+    the ids and their flat positions in original order."""
+    ctx = ctx or default_context()
+    d = _dev_u64(ids, ctx.torch_device)
+    n = d.numel()
+    sid = torch.empty(max(n, 1), dtype=torch.int64, device=d.device)
+    spos = torch.empty(max(n, 1), dtype=torch.int32, device=d.device)
+    cnt = (C.c_uint64 * num_shards)()
+    _lib.call("fsx_route_by_owner", ctx.h, _ptr(d), n, total_rows, num_shards, _ptr(sid),
+              _ptr(spos), cnt, _stream())
+    ids_np, pos_np = _np_u64(sid[:n]), spos[:n].cpu().numpy().astype(np.uint32)
+    out, at = [], 0
+    for s in range(num_shards):
+        k = int(cnt[s])
+        out.append((ids_np[at:at + k], pos_np[at:at + k]))
+        at += k
+    return out
+
+
+@dataclass
+class UpdateResult:
+    """ShardView::UpdateResult (embedding.hpp:77-80)."""
+    unique_ids: np.ndarray
+    rows: torch.Tensor  # |unique_ids| x dim, on the device
+
+
+class ShardView:
+    """One rank's shard (embedding.hpp:59-90), resident in HBM."""
+
+    def __init__(self, geom: TableGeometry, shard_id: int, learning_rate: float, seed: int,
+                 dtype: str = "f32", ctx: Context | None = None):
+        self.geom = geom
+        self.shard_id = shard_id
+        self.learning_rate = learning_rate
+        self.seed = seed
+        self.ctx = ctx or default_context()
+        self.dtype_code, self.torch_dtype = _DTYPES[dtype]
+        h = C.c_void_p()
+        _lib.call("fsx_table_create", self.ctx.h, geom.total_rows, geom.dim, geom.num_shards,
+                  shard_id, learning_rate, seed, self.dtype_code, C.byref(h))
+        self.h = h
+
+    def geometry(self) -> TableGeometry:
+        return self.geom
+
+    def local_rows(self) -> int:
+        return int(_lib.lib().fsx_table_local_rows(self.h))
+
+    def values(self) -> np.ndarray:
+        """f64 host mirror [local_rows x dim] (lazy D2H)."""
+        n = self.local_rows() * self.geom.dim
+        out = np.zeros(max(n, 1), np.float64)
+        _lib.call("fsx_table_download", self.h, out.ctypes.data)
+        return out[:n].reshape(self.local_rows(), self.geom.dim)
+
+    def device_values(self) -> torch.Tensor:
+        """Zero-copy view of the shard in HBM."""
+        ptr = _lib.lib().fsx_table_values(self.h)
+        n = self.local_rows() * self.geom.dim
+        return _wrap_device(ptr, n, self.torch_dtype, self.ctx.device).view(self.local_rows(), self.geom.dim)
+
+    def upload(self, values: np.ndarray) -> None:
+        v = np.ascontiguousarray(np.asarray(values, np.float64).reshape(-1))
+        if v.size != self.local_rows() * self.geom.dim:
+            raise InvalidArgument("embedding: upload shape mismatch")
+        _lib.call("fsx_table_upload", self.h, v.ctypes.data)
+
+    def row(self, global_id: int) -> np.ndarray:
+        return self.lookup([global_id]).double().cpu().numpy()[0]
+
+    def lookup(self, ids) -> torch.Tensor:
+        """embedding.cpp:139-146: rows in id order, duplicates duplicated."""
+        d = _dev_u64(ids, self.ctx.torch_device)
+        out = torch.empty((d.numel(), self.geom.dim), dtype=self.torch_dtype, device=d.device)
+        if d.numel():
+            _lib.call("fsx_table_gather", self.h, _ptr(d), d.numel(), _ptr(out), _stream(), 1)
+        return out
+
+    def apply_gradients(self, ids, grads) -> UpdateResult:
+        """embedding.cpp:148-181."""
+        d = _dev_u64(ids, self.ctx.torch_device)
+        g = grads if isinstance(grads, torch.Tensor) else torch.as_tensor(np.asarray(grads, np.float64))
+        g = g.to(device=d.device, dtype=self.torch_dtype).contiguous().reshape(-1)
+        dim = self.geom.dim
+        if g.numel() != d.numel() * dim:
+            raise InvalidArgument(f"embedding: gradient shape {g.numel()} misaligned with "
+                                  f"{d.numel()} ids x dim {dim}")
+        n = d.numel()
+        uq = torch.empty(max(n, 1), dtype=torch.int64, device=d.device)
+        rows = torch.empty((max(n, 1), dim), dtype=self.torch_dtype, device=d.device)
+        nu = C.c_uint64()
+        _lib.call("fsx_table_sgd_update", self.h, _ptr(d), n, _ptr(g), _ptr(uq), _ptr(rows),
+                  C.byref(nu), _stream())
+        return UpdateResult(_np_u64(uq[:nu.value]), rows[:nu.value])
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            _lib.lib().fsx_table_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def _wrap_device(ptr: int, n: int, dtype: torch.dtype, device: int) -> torch.Tensor:
+    """A torch view of libfsx-owned device memory (no copy, no ownership)."""
+
+    class _CAI:
+        def __init__(self):
+            typestr = {torch.float32: "<f4", torch.float64: "<f8", torch.int64: "<i8",
+                       torch.int32: "<i4", torch.uint8: "|u1"}[dtype]
+            self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr,
+                                             "data": (ptr, False), "version": 2}
+
+    with torch.cuda.device(device):
+        return torch.as_tensor(_CAI(), device=torch.device("cuda", device))
