@@ -1,0 +1,894 @@
+// Host side of the embedding engines: SynchronizedEmbedding (blocking
+// baseline, embedding.cpp:235-297) and PrioritizedEmbedding (collision-first
+// protocol, embedding.cpp:301-607) over the device kernels in
+// engine_kernels.cuh, plus the copy-engine all-to-all transport.
+//
+// Streams per rank:
+//   C  the caller's compute stream: merge (forward) and gradient split/pack
+//      (backward) — the only embedding work the model waits on;
+//   H  high priority side lane: the collision chain (collision gradients ->
+//      owner update -> E_co rows back to the next iteration's requesters);
+//   L  low priority side lane: deferred exclusive updates, routing and dedup
+//      of iteration i+1, collision detection, exclusive prefetch, masks.
+// Cross-stream order is expressed with CUDA events; cross-rank order with
+// stream memory operations on flag words in the peers' receive windows
+// (cuStreamWriteValue32 after each copy-engine copy, cuStreamWaitValue32 on
+// the receiving lane) — no SM ever spins and no kernel touches a peer.
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include "capi_util.cuh"
+#include "engine_kernels.cuh"
+
+namespace fsx {
+
+enum Channel : int { CH_IDS, CH_ROWS, CH_GRADS, CH_EX, CH_MASK, CH_COG, CH_EXG, CH_COR, NCH };
+
+namespace {
+
+__global__ void k_prefix(const uint64_t* cnt, int p, int stride, uint64_t* off) {
+  if (threadIdx.x == 0) {
+    uint64_t s = 0;
+    for (int d = 0; d < p; ++d) {
+      off[d] = s;
+      s += cnt[d * stride];
+    }
+    off[p] = s;
+  }
+}
+
+// out[0] = sum of even entries, out[1] = sum of odd entries of t[0..2p)
+__global__ void k_sum_pairs(const uint64_t* t, int p, uint64_t* out) {
+  if (threadIdx.x == 0) {
+    uint64_t a = 0, b = 0;
+    for (int d = 0; d < p; ++d) {
+      a += t[2 * d];
+      b += t[2 * d + 1];
+    }
+    out[0] = a;
+    out[1] = b;
+  }
+}
+
+__global__ void k_count_flags(const uint8_t* f, const uint64_t* d_n, unsigned long long* out) {
+  const uint64_t n = *d_n;
+  unsigned long long c = 0;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    c += f[i] ? 1 : 0;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31u) == 0 && c) atomicAdd(out, c);
+}
+
+// IterationStats.blocking_bytes (embedding.cpp:498-593) in the reference's
+// accounting (8-byte values): collision grads sent + received, E_co
+// messages sent + received.
+__global__ void k_blocking_bytes(int p, uint64_t rb8, const uint64_t* split_tot,
+                                 const uint64_t* occ_tot, const uint64_t* pack_tot, CSlots cor_recv,
+                                 int have_grads, int have_eco, uint64_t* out) {
+  if (threadIdx.x != 0) return;
+  uint64_t b = 0;
+  if (have_grads)
+    for (int d = 0; d < p; ++d) b += rb8 * (split_tot[2 * d + 1] + occ_tot[2 * d + 1]);
+  if (have_eco)
+    for (int d = 0; d < p; ++d)
+      b += 8 + pack_tot[2 * d + 1] * (8 + rb8) + 8 + slot_n(cor_recv.p[d]) * (8 + rb8);
+  *out = b;
+}
+
+}  // namespace
+
+// ---- per-batch state -----------------------------------------------------------
+struct ReqBatch {  // requester view of one iteration's ids
+  uint64_t n = 0;
+  DevBuf<uint64_t> ids, keys, uq_g;
+  DevBuf<uint32_t> send_pos, uq_off, split_rank;
+  DevBuf<uint8_t> send_dst, flag;
+  DevBuf<uint64_t> tot;        // [0..16) send counts, [16..33) send_off
+  DevBuf<uint64_t> split_tot;  // [32]
+  DevBuf<const char*> rowptr;
+  SortedIds srt;               // over composite (owner, local) keys
+  ScanScratch scan;
+  std::vector<uint64_t> h_send, h_split;
+  bool has_flags = false;
+  int ex_par = -1, cor_par = -1;  // channel parities holding E_ex / E_co of this batch
+  void reserve(uint64_t cap) {
+    if (ids.n >= cap && ids.p) return;
+    ids.alloc(cap); keys.alloc(cap); uq_g.alloc(cap); send_pos.alloc(cap); uq_off.alloc(kMaxRanks + 1);
+    split_rank.alloc(cap); send_dst.alloc(cap); flag.alloc(cap); tot.alloc(48); split_tot.alloc(32);
+    rowptr.alloc(cap);
+    srt.reserve(cap);
+  }
+  const uint64_t* send_off() const { return tot.p + 16; }
+};
+
+struct OwnBatch {  // owner view: occurrences received for this shard
+  DevBuf<uint64_t> ids;
+  DevBuf<uint8_t> occ_src, co;
+  DevBuf<uint32_t> occ_idx, occ_rank, bits;
+  DevBuf<uint64_t> cnt;  // k_recv_prefix layout: [0]=M, [2+s]=n_s, [2+16+s]=off_s
+  DevBuf<uint64_t> misc; // [0] co count, [8..40) pack totals (2p), [40..72) occ totals, [72..88) mask totals
+  DevBuf<PackEntry> ex_list, co_list;
+  SortedIds srt;
+  ScanScratch scan;
+  std::vector<uint64_t> h_recv, h_pack, h_mask;
+  bool has_co = false;
+  uint64_t m_cap = 0;
+  void reserve(uint64_t cap) {
+    if (m_cap >= cap && ids.p) return;
+    m_cap = cap;
+    ids.alloc(cap); occ_src.alloc(cap); co.alloc(cap); occ_idx.alloc(cap); occ_rank.alloc(cap);
+    bits.alloc(cap); cnt.alloc(2 + 2 * kMaxRanks + 8); misc.alloc(96); ex_list.alloc(cap);
+    co_list.alloc(cap);
+    srt.reserve(cap);
+  }
+  uint64_t* pack_tot() { return misc.p + 8; }
+  uint64_t* occ_tot() { return misc.p + 40; }
+  uint64_t* mask_tot() { return misc.p + 72; }
+};
+
+struct PeerView {
+  char* base = nullptr;       // peer's receive window (mapped)
+  uint32_t* flags = nullptr;  // peer's flag words (mapped)
+  bool ipc = false;
+};
+
+struct Engine {
+  Ctx* ctx = nullptr;
+  Table* t = nullptr;
+  fsx_engine_config cfg{};
+  int p = 1, me = 0;
+  uint64_t cap = 0;       // ids per rank per iteration
+  uint32_t rb = 0;        // row bytes
+  // receive window (IPC-exportable): per channel [2 parities][p slots][slot]
+  char* win = nullptr;
+  size_t win_bytes = 0;
+  size_t ch_off[NCH] = {};
+  size_t ch_slot[NCH] = {};
+  uint32_t* flags = nullptr;  // [NCH][kMaxRanks], inside win
+  size_t flags_off = 0;
+  DevBuf<char> stage;         // send staging, same layout as the channel region of win
+  PeerView peer[kMaxRanks];
+  uint32_t seq[NCH] = {};
+  cudaStream_t lo = nullptr, hi = nullptr;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_next = 0;
+  // exposed-wait timing on the compute stream
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> waits;
+  std::vector<cudaEvent_t> timing_pool;
+  size_t timing_next = 0;
+  // protocol state
+  ReqBatch rq[3];
+  OwnBatch ow[3];
+  int iter = 0;
+  bool forward_done = false;
+  bool has_pending = false;
+  int exg_par = -1;
+  cudaEvent_t ev_ex_ready = nullptr, ev_co_ready = nullptr, ev_mask = nullptr, ev_split = nullptr;
+  // stats slab (pinned): [iter][3]
+  uint64_t* h_stats = nullptr;
+  DevBuf<uint64_t> d_stats;  // ring of 3 x 4
+  size_t stats_cap = 0;
+  int stats_n = 0;
+  ScanScratch scan;
+
+  ReqBatch& R(int i) { return rq[((i % 3) + 3) % 3]; }
+  OwnBatch& O(int i) { return ow[((i % 3) + 3) % 3]; }
+
+  char* recv_slot(int ch, int par, int src) const {
+    return win + ch_off[ch] + (static_cast<size_t>(par) * p + src) * ch_slot[ch];
+  }
+  char* stage_slot(int ch, int par, int dst) const {
+    // self slot of the staging area is unused: self messages go straight to
+    // this rank's own receive slot
+    if (dst == me) return recv_slot(ch, par, dst);
+    return stage.p + ch_off[ch] + (static_cast<size_t>(par) * p + dst) * ch_slot[ch];
+  }
+  Slots send_slots(int ch, int par) const {
+    Slots s{};
+    for (int d = 0; d < p; ++d) s.p[d] = stage_slot(ch, par, d);
+    return s;
+  }
+  CSlots recv_slots(int ch, int par) const {
+    CSlots s{};
+    for (int d = 0; d < p; ++d) s.p[d] = recv_slot(ch, par, d);
+    return s;
+  }
+  int next_par(int ch) { return static_cast<int>(++seq[ch] & 1u); }
+
+  cudaEvent_t record(cudaStream_t s) {
+    if (ev_next == ev_pool.size()) {
+      cudaEvent_t e;
+      FSX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ev_pool.push_back(e);
+    }
+    cudaEvent_t e = ev_pool[ev_next];
+    ev_next = (ev_next + 1) % 64;
+    if (ev_pool.size() < 64 && ev_next == 0) ev_next = ev_pool.size();
+    FSX_CUDA(cudaEventRecord(e, s));
+    return e;
+  }
+  void wait(cudaStream_t s, cudaEvent_t e) {
+    if (e) FSX_CUDA(cudaStreamWaitEvent(s, e, 0));
+  }
+  cudaEvent_t timing_event() {
+    if (timing_next == timing_pool.size()) {
+      cudaEvent_t e;
+      FSX_CUDA(cudaEventCreate(&e));
+      timing_pool.push_back(e);
+    }
+    return timing_pool[timing_next++];
+  }
+  // compute stream waits on embedding traffic; the pair measures the stall
+  void exposed_wait(cudaStream_t c, std::initializer_list<cudaEvent_t> evs) {
+    cudaEvent_t a = timing_event(), b = timing_event();
+    FSX_CUDA(cudaEventRecord(a, c));
+    for (cudaEvent_t e : evs) wait(c, e);
+    FSX_CUDA(cudaEventRecord(b, c));
+    waits.emplace_back(a, b);
+  }
+
+  std::vector<uint64_t> fetch(const uint64_t* d, int n, cudaStream_t s) {
+    std::vector<uint64_t> h(n);
+    FSX_CUDA(cudaMemcpyAsync(h.data(), d, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, s));
+    FSX_CUDA(cudaStreamSynchronize(s));
+    return h;
+  }
+
+  // copy-engine all-to-all of channel `ch` (parity `par`): bytes[d] to rank d.
+  // Self messages are already in place. Returns after enqueueing; `s` then
+  // waits for every peer's message to this rank.
+  void a2a(int ch, int par, const std::vector<uint64_t>& bytes, cudaStream_t s) {
+    if (p == 1) return;
+    const uint32_t v = seq[ch];
+    for (int k = 1; k < p; ++k) {
+      const int d = (me + k) % p;  // stagger destinations across the NVSwitch
+      const PeerView& pv = peer[d];
+      if (!pv.base) raise(FSX_ERR_COLLECTIVE, "all_to_all: peer " + std::to_string(d) + " not connected");
+      char* dst = pv.base + ch_off[ch] + (static_cast<size_t>(par) * p + me) * ch_slot[ch];
+      if (bytes[d]) FSX_CUDA(cudaMemcpyAsync(dst, stage_slot(ch, par, d), bytes[d], cudaMemcpyDefault, s));
+      FSX_CU(cuStreamWriteValue32(reinterpret_cast<CUstream>(s),
+                                  reinterpret_cast<CUdeviceptr>(pv.flags + ch * kMaxRanks + me), v,
+                                  CU_STREAM_WRITE_VALUE_DEFAULT));
+    }
+    for (int k = 1; k < p; ++k) {
+      const int src = (me + p - k) % p;
+      FSX_CU(cuStreamWaitValue32(reinterpret_cast<CUstream>(s),
+                                 reinterpret_cast<CUdeviceptr>(flags + ch * kMaxRanks + src), v,
+                                 CU_STREAM_WAIT_VALUE_GEQ));
+    }
+  }
+
+  int nc2() const { return p <= 4 ? 8 : 16; }  // counters for 2p classes
+
+  // ---- requester: route a batch (embedding.cpp:185-212) ----------------------
+  int route(ReqBatch& r, const uint64_t* d_ids, uint64_t n, cudaStream_t s) {
+    if (n > cap) raise(FSX_ERR_INVALID_ARGUMENT, "embedding: batch of " + std::to_string(n) +
+                                                    " ids exceeds engine capacity " + std::to_string(cap));
+    r.reserve(cap);
+    r.n = n;
+    r.has_flags = false;
+    if (n) FSX_CUDA(cudaMemcpyAsync(r.ids.p, d_ids, n * 8, cudaMemcpyDeviceToDevice, s));
+    const int par = next_par(CH_IDS);
+    Slots send = send_slots(CH_IDS, par);
+    FSX_CUDA(cudaMemsetAsync(r.tot.p, 0, 48 * 8, s));
+    if (p <= 8) {
+      RouteOp<8> op{r.ids.p, t->g.total_rows, p, r.tot.p, send, r.send_pos.p, r.send_dst.p, cap, ctx->d_err};
+      run_scan(ctx, op, n, nullptr, r.scan, r.tot.p, s);
+    } else {
+      RouteOp<16> op{r.ids.p, t->g.total_rows, p, r.tot.p, send, r.send_pos.p, r.send_dst.p, cap, ctx->d_err};
+      run_scan(ctx, op, n, nullptr, r.scan, r.tot.p, s);
+    }
+    FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, r.tot.p, 1, cap, ctx->d_err);
+    FSX_LAUNCH(ctx, k_prefix, 1, 32, 0, s, r.tot.p, p, 1, r.tot.p + 16);
+    // per-owner sorted unique lists (unique_per_shard, embedding.cpp:205-208)
+    const int lbits = bits_for(t->g.total_rows / static_cast<uint64_t>(p) + 1);
+    if (n) {
+      FSX_LAUNCH(ctx, k_requester_keys, grid_for(ctx, n, 256, 8), 256, 0, s, r.ids.p, n, p, lbits, r.keys.p);
+      FSX_CUDA(cudaMemcpyAsync(r.srt.d_n(), &r.n, 8, cudaMemcpyHostToDevice, s));
+      ShardGeom g{~0ull, 0, 1, 1, 0};
+      r.srt.run(ctx, r.keys.p, n, g, false, false, lbits + bits_for(static_cast<uint64_t>(p - 1)), s);
+    } else {
+      FSX_CUDA(cudaMemsetAsync(r.srt.d_counts.p, 0, 32, s));
+    }
+    FSX_LAUNCH(ctx, k_requester_uq, grid_for(ctx, n, 256, 4), 256, 0, s, r.srt.uniq.p, r.srt.d_u(), p,
+               lbits, r.uq_g.p, r.uq_off.p);
+    if (p > 1) {
+      r.h_send = fetch(r.tot.p, p, s);
+      std::vector<uint64_t> bytes(p);
+      for (int d = 0; d < p; ++d) bytes[d] = kHdr + 8 * r.h_send[d];
+      a2a(CH_IDS, par, bytes, s);
+    }
+    return par;
+  }
+
+  // ---- owner: receive + dedup (embedding.cpp:214-229) -------------------------
+  void receive(OwnBatch& o, int ids_par, cudaStream_t s) {
+    o.reserve(static_cast<uint64_t>(p) * cap);
+    o.has_co = false;
+    CSlots slots = recv_slots(CH_IDS, ids_par);
+    FSX_LAUNCH(ctx, k_recv_prefix, 1, 32, 0, s, slots, p, cap, o.cnt.p, ctx->d_err);
+    FSX_CUDA(cudaMemcpyAsync(o.srt.d_n(), o.cnt.p, 8, cudaMemcpyDeviceToDevice, s));
+    FSX_LAUNCH(ctx, k_flatten_recv, grid_for(ctx, static_cast<uint64_t>(p) * cap, 256, 8), 256, 0, s,
+               slots, p, cap, o.cnt.p, t->g, o.ids.p, o.occ_src.p, o.occ_idx.p, ctx->d_err);
+    o.srt.run(ctx, o.ids.p, o.m_cap, t->g, true, false, t->key_bits(), s);
+    FSX_CUDA(cudaMemsetAsync(o.bits.p, 0, o.m_cap * 4, s));
+    FSX_LAUNCH(ctx, k_src_bits, grid_for(ctx, o.m_cap, 256, 8), 256, 0, s, o.srt.inverse.p,
+               o.occ_src.p, o.srt.d_n(), o.bits.p);
+    if (p > 1) o.h_recv = fetch(o.cnt.p + 2, p, s);
+  }
+
+  // full-row deterministic update of an owner batch from a grads channel
+  void update(OwnBatch& o, int ch, int par, const uint8_t* select, uint8_t want, bool by_rank,
+              cudaStream_t s) {
+    RowSegments rs{o.srt.uniq.p, o.srt.seg_start.p, o.srt.perm, o.srt.d_u(), select, want};
+    const uint64_t m = o.m_cap;
+    if (t->dtype == FSX_F32) {
+      GradRows<float> gr{recv_slot(ch, par, 0) + kHdr, ch_slot[ch], o.occ_src.p,
+                         by_rank ? o.occ_rank.p : o.occ_idx.p, rb};
+      sgd_update_rows<float>(ctx, *t, rs, m, m, gr, cfg.reduce_chunk, sgd[s == hi ? 1 : 0], nullptr, s);
+    } else {
+      GradRows<double> gr{recv_slot(ch, par, 0) + kHdr, ch_slot[ch], o.occ_src.p,
+                          by_rank ? o.occ_rank.p : o.occ_idx.p, rb};
+      sgd_update_rows<double>(ctx, *t, rs, m, m, gr, cfg.reduce_chunk, sgd[s == hi ? 1 : 0], nullptr, s);
+    }
+  }
+  SgdScratch sgd[2];
+
+  // ---- sync building blocks ---------------------------------------------------------
+  // owner lookup per occurrence -> ROWS -> requester scatter (embedding.cpp:244-264)
+  void serve_blocking(ReqBatch& r, OwnBatch& o, void* d_out, cudaStream_t s) {
+    const int par = next_par(CH_ROWS);
+    Slots send = send_slots(CH_ROWS, par);
+    OwnerLookupMap lm{static_cast<const char*>(t->values), o.ids.p, o.occ_src.p, o.occ_idx.p, send, rb, p};
+    launch_copy_rows(ctx, lm, o.m_cap, o.srt.d_n(), rb, s);
+    FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, o.cnt.p + 2, 1, cap, ctx->d_err);
+    if (p > 1) {
+      std::vector<uint64_t> bytes(p);
+      for (int d = 0; d < p; ++d) bytes[d] = kHdr + rb * o.h_recv[d];
+      a2a(CH_ROWS, par, bytes, s);
+    }
+    RequesterScatterMap sm{recv_slots(CH_ROWS, par), r.send_pos.p, r.send_dst.p, r.send_off(),
+                           static_cast<char*>(d_out), rb};
+    launch_copy_rows(ctx, sm, r.n, nullptr, rb, s);
+  }
+
+  // requester grads -> GRADS -> owner full update (embedding.cpp:276-295)
+  void update_blocking(ReqBatch& r, OwnBatch& o, const void* d_grads, cudaStream_t s) {
+    const int par = next_par(CH_GRADS);
+    Slots send = send_slots(CH_GRADS, par);
+    GradPackMap gm{static_cast<const char*>(d_grads), r.send_pos.p, r.send_dst.p, r.send_off(),
+                   r.srt.inverse.p, nullptr, nullptr, send, send, rb};
+    launch_copy_rows(ctx, gm, r.n, nullptr, rb, s);
+    FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, r.tot.p, 1, cap, ctx->d_err);
+    if (p > 1) {
+      std::vector<uint64_t> bytes(p);
+      for (int d = 0; d < p; ++d) bytes[d] = kHdr + rb * r.h_send[d];
+      a2a(CH_GRADS, par, bytes, s);
+    }
+    update(o, CH_GRADS, par, nullptr, 0, false, s);
+  }
+
+  // ---- prioritized building blocks ----------------------------------------------------
+  // collision of (cur, next) owner batches + pack lists + EX prefetch of next
+  // (embedding.cpp:360-390)
+  void collide_and_prefetch(OwnBatch& oc, OwnBatch& on, ReqBatch& rn, cudaStream_t s) {
+    FSX_CUDA(cudaMemsetAsync(on.co.p, 0, on.m_cap, s));
+    FSX_CUDA(cudaMemsetAsync(oc.misc.p, 0, 8, s));
+    FSX_LAUNCH(ctx, k_intersect_flags, grid_for(ctx, oc.m_cap, 256, 8), 256, 0, s, oc.srt.uniq_g.p,
+               oc.srt.d_u(), on.srt.uniq_g.p, on.srt.d_u(), oc.co.p, on.co.p);
+    FSX_LAUNCH(ctx, k_count_flags, grid_for(ctx, oc.m_cap, 256, 4), 256, 0, s, oc.co.p, oc.srt.d_u(),
+               reinterpret_cast<unsigned long long*>(oc.misc.p));
+    oc.has_co = true;
+    on.has_co = false;
+    // pack lists over next's unique rows: ex -> E_ex now, co -> E_co later
+    FSX_CUDA(cudaMemsetAsync(on.pack_tot(), 0, 32 * 8, s));
+    if (nc2() == 8) {
+      OwnerPackOp<8> op{on.bits.p, on.co.p, p, on.pack_tot(), on.ex_list.p, on.co_list.p};
+      run_scan(ctx, op, on.m_cap, on.srt.d_u(), on.scan, on.pack_tot(), s);
+    } else {
+      OwnerPackOp<16> op{on.bits.p, on.co.p, p, on.pack_tot(), on.ex_list.p, on.co_list.p};
+      run_scan(ctx, op, on.m_cap, on.srt.d_u(), on.scan, on.pack_tot(), s);
+    }
+    const int par = next_par(CH_EX);
+    Slots send = send_slots(CH_EX, par);
+    FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, on.pack_tot(), 2, cap, ctx->d_err);
+    IdRowPackMap pm{static_cast<const char*>(t->values), on.srt.uniq.p, on.srt.uniq_g.p, on.ex_list.p,
+                    send, on.pack_tot(), 0, rb};
+    FSX_LAUNCH(ctx, k_sum_pairs, 1, 32, 0, s, on.pack_tot(), p, on.misc.p + 2);
+    launch_copy_rows(ctx, pm, on.m_cap * static_cast<uint64_t>(p), on.misc.p + 2, rb, s);
+    if (p > 1) {
+      on.h_pack = fetch(on.pack_tot(), 2 * p, s);
+      std::vector<uint64_t> bytes(p);
+      for (int d = 0; d < p; ++d) bytes[d] = idrows_rows_off(on.h_pack[2 * d]) + rb * on.h_pack[2 * d];
+      a2a(CH_EX, par, bytes, s);
+    }
+    rn.ex_par = par;
+  }
+  // MASK messages for the current batch + requester flags + split plan
+  // (embedding.cpp:392-408, 524-536)
+  void masks_and_split(OwnBatch& oc, ReqBatch& rc, bool with_co, cudaStream_t s) {
+    const int par = next_par(CH_MASK);
+    Slots send = send_slots(CH_MASK, par);
+    FSX_CUDA(cudaMemsetAsync(oc.mask_tot(), 0, 16 * 8, s));
+    if (p <= 8) {
+      MaskOp<8> op{oc.bits.p, with_co ? oc.co.p : nullptr, send};
+      run_scan(ctx, op, oc.m_cap, oc.srt.d_u(), oc.scan, oc.mask_tot(), s);
+    } else {
+      MaskOp<16> op{oc.bits.p, with_co ? oc.co.p : nullptr, send};
+      run_scan(ctx, op, oc.m_cap, oc.srt.d_u(), oc.scan, oc.mask_tot(), s);
+    }
+    FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, oc.mask_tot(), 1, cap, ctx->d_err);
+    if (p > 1) {
+      oc.h_mask = fetch(oc.mask_tot(), p, s);
+      std::vector<uint64_t> bytes(p);
+      for (int d = 0; d < p; ++d) bytes[d] = kHdr + oc.h_mask[d];
+      a2a(CH_MASK, par, bytes, s);
+    }
+    FSX_LAUNCH(ctx, k_requester_flags, grid_for(ctx, rc.n, 256, 4), 256, 0, s, recv_slots(CH_MASK, par),
+               rc.uq_off.p, p, rc.srt.d_u(), rc.flag.p, ctx->d_err);
+    rc.has_flags = true;
+    // split plan (ranks of each occurrence in its (owner, flag) message)
+    FSX_CUDA(cudaMemsetAsync(rc.split_tot.p, 0, 32 * 8, s));
+    if (nc2() == 8) {
+      SplitOp<8> op{rc.send_pos.p, rc.send_dst.p, rc.srt.inverse.p, rc.flag.p, rc.split_rank.p};
+      run_scan(ctx, op, rc.n, nullptr, rc.scan, rc.split_tot.p, s);
+    } else {
+      SplitOp<16> op{rc.send_pos.p, rc.send_dst.p, rc.srt.inverse.p, rc.flag.p, rc.split_rank.p};
+      run_scan(ctx, op, rc.n, nullptr, rc.scan, rc.split_tot.p, s);
+    }
+    // owner side: per-occurrence rank within (source, flag)
+    FSX_CUDA(cudaMemsetAsync(oc.occ_tot(), 0, 32 * 8, s));
+    if (nc2() == 8) {
+      OccRankOp<8> op{oc.occ_src.p, oc.srt.inverse.p, with_co ? oc.co.p : nullptr, oc.occ_rank.p};
+      run_scan(ctx, op, oc.m_cap, oc.srt.d_n(), oc.scan, oc.occ_tot(), s);
+    } else {
+      OccRankOp<16> op{oc.occ_src.p, oc.srt.inverse.p, with_co ? oc.co.p : nullptr, oc.occ_rank.p};
+      run_scan(ctx, op, oc.m_cap, oc.srt.d_n(), oc.scan, oc.occ_tot(), s);
+    }
+    if (p > 1) rc.h_split = fetch(rc.split_tot.p, 2 * p, s);
+  }
+
+  // requester: split grads into CO_G / EX_G messages (embedding.cpp:526-536)
+  void split_grads(ReqBatch& r, const void* d_grads, int cog_par, int exg_par, cudaStream_t s) {
+    Slots co = send_slots(CH_COG, cog_par), ex = send_slots(CH_EXG, exg_par);
+    GradPackMap gm{static_cast<const char*>(d_grads), r.send_pos.p, r.send_dst.p, r.send_off(),
+                   r.srt.inverse.p, r.flag.p, r.split_rank.p, co, ex, rb};
+    launch_copy_rows(ctx, gm, r.n, nullptr, rb, s);
+    FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, co, p, r.split_tot.p + 1, 2, cap, ctx->d_err);
+    FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, ex, p, r.split_tot.p, 2, cap, ctx->d_err);
+  }
+
+  // owner: E_co rows of the next batch (embedding.cpp:560-590)
+  int send_eco(OwnBatch& on, cudaStream_t s) {
+    const int par = next_par(CH_COR);
+    Slots send = send_slots(CH_COR, par);
+    FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, on.pack_tot() + 1, 2, cap, ctx->d_err);
+    IdRowPackMap pm{static_cast<const char*>(t->values), on.srt.uniq.p, on.srt.uniq_g.p, on.co_list.p,
+                    send, on.pack_tot(), 1, rb};
+    launch_copy_rows(ctx, pm, on.m_cap * static_cast<uint64_t>(p), on.misc.p + 3, rb, s);
+    if (p > 1) {
+      std::vector<uint64_t> bytes(p);
+      for (int d = 0; d < p; ++d) bytes[d] = idrows_rows_off(on.h_pack[2 * d + 1]) + rb * on.h_pack[2 * d + 1];
+      a2a(CH_COR, par, bytes, s);
+    }
+    return par;
+  }
+
+  // requester: merge E_ex / E_co into batch-major rows (embedding.cpp:453-484)
+  void merge(ReqBatch& r, void* d_out, cudaStream_t s) {
+    CSlots ex = recv_slots(CH_EX, r.ex_par);
+    CSlots co{};
+    if (r.cor_par >= 0) co = recv_slots(CH_COR, r.cor_par);
+    FSX_LAUNCH(ctx, k_resolve_rows, grid_for(ctx, r.n, 256, 8), 256, 0, s, ex, co, r.uq_g.p, r.uq_off.p,
+               p, r.srt.d_u(), rb, r.rowptr.p, ctx->d_err);
+    MergeMap mm{r.rowptr.p, r.srt.inverse.p, static_cast<char*>(d_out), rb};
+    launch_copy_rows(ctx, mm, r.n, nullptr, rb, s);
+  }
+
+
+  // ---- protocol --------------------------------------------------------------------
+  cudaStream_t cur_c = nullptr;
+  cudaEvent_t ev_merged = nullptr;   // C: after the last merge / bootstrap serve
+  cudaEvent_t ev_next_ready = nullptr;  // L: owner batch i+1 built + pack lists
+  int pending_iter = -1;             // owner batch whose exclusive grads are deferred
+  cudaEvent_t ev_pending_split = nullptr;
+
+  void sync_forward(const uint64_t* ids, uint64_t n, void* out, cudaStream_t c) {
+    ReqBatch& r = R(0);
+    OwnBatch& o = O(0);
+    const int par = route(r, ids, n, c);
+    receive(o, par, c);
+    serve_blocking(r, o, out, c);
+    forward_done = true;
+  }
+
+  void sync_backward(const void* grads, cudaStream_t c) {
+    if (!forward_done) raise(FSX_ERR_PROTOCOL, "embedding: backward before forward");
+    update_blocking(R(0), O(0), grads, c);
+    forward_done = false;
+    ++iter;
+  }
+
+  void prio_forward(const uint64_t* ids_cur, uint64_t n_cur, const uint64_t* ids_next,
+                    uint64_t n_next, void* out, cudaStream_t c) {
+    if (forward_done) raise(FSX_ERR_PROTOCOL, "embedding: forward called twice in one iteration");
+    const int i = iter;
+    ReqBatch& rc = R(i);
+    OwnBatch& oc = O(i);
+    const bool bootstrap = i == 0;
+    cudaEvent_t ev_cur = nullptr;
+    if (bootstrap) {
+      const int par = route(rc, ids_cur, n_cur, c);
+      receive(oc, par, c);
+      rc.cor_par = -1;
+      ev_cur = record(c);
+    } else {
+      if (rc.n != n_cur)
+        raise(FSX_ERR_PROTOCOL, "embedding: current batch does not match the prefetched ids");
+      apply_deferred();
+    }
+    // ---- side lane L: prepare iteration i+1 (embedding.cpp:355-420) ----
+    wait(lo, ev_cur);
+    wait(lo, ev_merged);  // slots of the parity reused below were read by the last merge
+    if (ids_next) {
+      ReqBatch& rn = R(i + 1);
+      OwnBatch& on = O(i + 1);
+      const int par = route(rn, ids_next, n_next, lo);
+      receive(on, par, lo);
+      rn.cor_par = -1;
+      collide_and_prefetch(oc, on, rn, lo);
+      ev_next_ready = record(lo);
+      rn_ex_ready = ev_next_ready;
+      if (!bootstrap) masks_and_split(oc, rc, true, lo);
+    } else {
+      oc.has_co = false;
+      ev_next_ready = nullptr;
+      if (!bootstrap) masks_and_split(oc, rc, false, lo);
+    }
+    ev_mask = bootstrap ? nullptr : record(lo);
+    stats_forward(i, ids_next != nullptr);
+    // ---- compute stream C: serve iteration i ----
+    if (bootstrap) {
+      serve_blocking(rc, oc, out, c);
+    } else {
+      exposed_wait(c, {cur_ex_ready, cur_co_ready});
+      merge(rc, out, c);
+    }
+    ev_merged = record(c);
+    cur_ex_ready = rn_ex_ready;
+    forward_done = true;
+    has_next = ids_next != nullptr;
+  }
+  cudaEvent_t cur_ex_ready = nullptr, cur_co_ready = nullptr, rn_ex_ready = nullptr;
+  bool has_next = false;
+
+  // deferred exclusive gradients of the previous iteration (embedding.cpp:314-339)
+  void apply_deferred() {
+    if (!has_pending) return;
+    OwnBatch& op = O(pending_iter);
+    ReqBatch& rp = R(pending_iter);
+    wait(lo, ev_pending_split);
+    if (p > 1) {
+      std::vector<uint64_t> bytes(p);
+      for (int d = 0; d < p; ++d) bytes[d] = kHdr + rb * rp.h_split[2 * d];
+      a2a(CH_EXG, exg_par, bytes, lo);
+    }
+    update(op, CH_EXG, exg_par, op.has_co ? op.co.p : nullptr, 0, true, lo);
+    has_pending = false;
+  }
+
+  void prio_backward(const void* grads, cudaStream_t c) {
+    if (!forward_done) raise(FSX_ERR_PROTOCOL, "embedding: backward before forward");
+    const int i = iter;
+    ReqBatch& rc = R(i);
+    OwnBatch& oc = O(i);
+    cudaEvent_t ev_chain_start = nullptr;
+    bool have_grads = false;
+    if (i == 0) {
+      update_blocking(rc, oc, grads, c);  // bootstrap: one synchronized update
+      ev_chain_start = record(c);
+      has_pending = false;
+    } else {
+      exposed_wait(c, {ev_mask});
+      const int cog = next_par(CH_COG);
+      exg_par = next_par(CH_EXG);
+      split_grads(rc, grads, cog, exg_par, c);
+      ev_pending_split = record(c);
+      pending_iter = i;
+      has_pending = true;
+      ev_chain_start = ev_pending_split;
+      if (oc.has_co) {
+        // collision chain, high priority (embedding.cpp:539-557)
+        wait(hi, ev_pending_split);
+        if (p > 1) {
+          std::vector<uint64_t> bytes(p);
+          for (int d = 0; d < p; ++d) bytes[d] = kHdr + rb * rc.h_split[2 * d + 1];
+          a2a(CH_COG, cog, bytes, hi);
+        }
+        update(oc, CH_COG, cog, oc.co.p, 1, true, hi);
+        have_grads = true;
+      }
+    }
+    if (has_next) {
+      // E_co^{i+1}: fresh collision rows to the next iteration's requesters
+      OwnBatch& on = O(i + 1);
+      ReqBatch& rn = R(i + 1);
+      wait(hi, ev_chain_start);
+      wait(hi, ev_next_ready);
+      rn.cor_par = send_eco(on, hi);
+      cur_co_ready = record(hi);
+      stats_backward(i, have_grads, true, rc, oc, on, rn.cor_par, hi);
+    } else {
+      cur_co_ready = nullptr;
+      stats_backward(i, have_grads, false, rc, oc, oc, -1, i == 0 ? c : hi);
+    }
+    forward_done = false;
+    ++iter;
+  }
+
+  void finalize(cudaStream_t c) {
+    apply_deferred();
+    wait(c, record(lo));
+    wait(c, record(hi));
+  }
+
+  // ---- stats (IterationStats, embedding.hpp:119-124) ----------------------------
+  void stats_reserve(int n) {
+    if (static_cast<size_t>(n) <= stats_cap) return;
+    size_t nc = std::max<size_t>(1024, stats_cap * 2);
+    while (nc < static_cast<size_t>(n)) nc *= 2;
+    uint64_t* h = nullptr;
+    FSX_CUDA(cudaDeviceSynchronize());
+    FSX_CUDA(cudaMallocHost(&h, nc * 3 * 8));
+    std::memset(h, 0, nc * 3 * 8);
+    if (h_stats) {
+      std::memcpy(h, h_stats, stats_cap * 3 * 8);
+      cudaFreeHost(h_stats);
+    }
+    h_stats = h;
+    stats_cap = nc;
+  }
+  void stats_forward(int i, bool with_next) {
+    stats_reserve(i + 1);
+    stats_n = i + 1;
+    uint64_t* dst = h_stats + 3 * static_cast<size_t>(i);
+    dst[0] = dst[1] = dst[2] = 0;
+    if (with_next) {
+      FSX_CUDA(cudaMemcpyAsync(dst, O(i).misc.p, 8, cudaMemcpyDeviceToHost, lo));
+      FSX_CUDA(cudaMemcpyAsync(dst + 1, O(i + 1).srt.d_u(), 8, cudaMemcpyDeviceToHost, lo));
+    }
+  }
+  void stats_backward(int i, bool have_grads, bool have_eco, ReqBatch& rc, OwnBatch& oc,
+                      OwnBatch& on, int cor_par, cudaStream_t s) {
+    if (!have_grads && !have_eco) return;
+    uint64_t* d = d_stats.p + 4 * (i % 3);
+    CSlots cor{};
+    if (cor_par >= 0) cor = recv_slots(CH_COR, cor_par);
+    FSX_LAUNCH(ctx, k_blocking_bytes, 1, 32, 0, s, p, 8ull * t->g.dim, rc.split_tot.p, oc.occ_tot(),
+               on.pack_tot(), cor, have_grads ? 1 : 0, have_eco ? 1 : 0, d);
+    FSX_CUDA(cudaMemcpyAsync(h_stats + 3 * static_cast<size_t>(i) + 2, d, 8, cudaMemcpyDeviceToHost, s));
+  }
+
+  ~Engine() {
+    cudaDeviceSynchronize();
+    for (int d = 0; d < kMaxRanks; ++d)
+      if (peer[d].ipc && peer[d].base) cudaIpcCloseMemHandle(peer[d].base);
+    for (auto e : ev_pool) cudaEventDestroy(e);
+    for (auto e : timing_pool) cudaEventDestroy(e);
+    if (lo) cudaStreamDestroy(lo);
+    if (hi) cudaStreamDestroy(hi);
+    if (win) cudaFree(win);
+    if (h_stats) cudaFreeHost(h_stats);
+  }
+};
+
+}  // namespace fsx
+
+using namespace fsx;
+
+struct fsx_engine : Engine {};
+
+namespace {
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+struct ExportBlob {
+  uint64_t magic;
+  int32_t p, me, mode, pad;
+  uint64_t win_bytes, flags_off;
+  uint64_t ch_off[NCH], ch_slot[NCH];
+  cudaIpcMemHandle_t handle;
+};
+constexpr uint64_t kBlobMagic = 0x46535857494e3031ull;  // "FSXWIN01"
+}  // namespace
+
+extern "C" {
+
+int fsx_engine_create(fsx_ctx* ctx, fsx_table* table, const fsx_engine_config* cfg, fsx_engine** out) {
+  FSX_API_BEGIN
+  DeviceGuard dg(ctx->device);
+  if (!cfg || (cfg->mode != FSX_MODE_SYNC && cfg->mode != FSX_MODE_PRIO))
+    raise(FSX_ERR_INVALID_ARGUMENT, "fsx: bad engine mode");
+  if (cfg->transport != FSX_TRANSPORT_CE)
+    raise(FSX_ERR_CONFIG, "fsx: only the copy-engine transport is built into this engine");
+  if (table->g.p != ctx->world || table->g.shard != ctx->rank)
+    raise(FSX_ERR_INVALID_ARGUMENT, "fsx: table shard does not match the context rank/world");
+  if (ctx->world > kMaxRanks) raise(FSX_ERR_INVALID_ARGUMENT, "fsx: at most 16 ranks");
+  auto e = std::make_unique<fsx_engine>();
+  e->ctx = ctx;
+  e->t = table;
+  e->cfg = *cfg;
+  e->p = ctx->world;
+  e->me = ctx->rank;
+  e->cap = std::max<uint64_t>(cfg->max_occurrences, 1);
+  e->rb = table->row_bytes();
+  const bool prio = cfg->mode == FSX_MODE_PRIO;
+  const uint64_t cap = e->cap, rb = e->rb;
+  auto round256 = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
+  uint64_t slot[NCH] = {};
+  slot[CH_IDS] = kHdr + cap * 8;
+  slot[CH_ROWS] = kHdr + cap * rb;
+  slot[CH_GRADS] = kHdr + cap * rb;
+  if (prio) {
+    slot[CH_EX] = idrows_rows_off(cap) + cap * rb;
+    slot[CH_MASK] = kHdr + align16(cap);
+    slot[CH_COG] = kHdr + cap * rb;
+    slot[CH_EXG] = kHdr + cap * rb;
+    slot[CH_COR] = idrows_rows_off(cap) + cap * rb;
+  }
+  size_t off = 0;
+  for (int ch = 0; ch < NCH; ++ch) {
+    e->ch_slot[ch] = round256(slot[ch]);
+    e->ch_off[ch] = off;
+    off += 2 * static_cast<size_t>(e->p) * e->ch_slot[ch];
+  }
+  e->flags_off = off;
+  e->win_bytes = off + round256(NCH * kMaxRanks * sizeof(uint32_t));
+  FSX_CUDA(cudaMalloc(&e->win, e->win_bytes));
+  e->flags = reinterpret_cast<uint32_t*>(e->win + e->flags_off);
+  FSX_CUDA(cudaMemset(e->flags, 0, NCH * kMaxRanks * sizeof(uint32_t)));
+  if (e->p > 1) e->stage.alloc(off);
+  int lo_prio = 0, hi_prio = 0;
+  FSX_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+  FSX_CUDA(cudaStreamCreateWithPriority(&e->lo, cudaStreamNonBlocking, lo_prio));
+  FSX_CUDA(cudaStreamCreateWithPriority(&e->hi, cudaStreamNonBlocking, hi_prio));
+  e->d_stats.alloc(16);
+  for (int k = 0; k < 3; ++k) {
+    e->rq[k].reserve(cap);
+    e->ow[k].reserve(static_cast<uint64_t>(e->p) * cap);
+  }
+  FSX_CUDA(cudaDeviceSynchronize());
+  *out = e.release();
+  FSX_API_END
+}
+
+int fsx_engine_destroy(fsx_engine* e) {
+  FSX_API_BEGIN
+  if (!e) return FSX_OK;
+  DeviceGuard dg(e->ctx->device);
+  delete e;
+  FSX_API_END
+}
+
+int fsx_engine_connect_local(fsx_engine* e, int peer, fsx_engine* other) {
+  FSX_API_BEGIN
+  if (peer < 0 || peer >= e->p || other->p != e->p || other->me != peer || other->win_bytes != e->win_bytes)
+    raise(FSX_ERR_COLLECTIVE, "fsx: peer engine layout mismatch");
+  DeviceGuard dg(e->ctx->device);
+  if (other->ctx->device != e->ctx->device) {
+    cudaError_t rc = cudaDeviceEnablePeerAccess(other->ctx->device, 0);
+    if (rc != cudaSuccess && rc != cudaErrorPeerAccessAlreadyEnabled) FSX_CUDA(rc);
+    cudaGetLastError();
+  }
+  e->peer[peer].base = other->win;
+  e->peer[peer].flags = other->flags;
+  e->peer[peer].ipc = false;
+  FSX_API_END
+}
+
+int fsx_engine_export(fsx_engine* e, void* blob, uint64_t* len) {
+  FSX_API_BEGIN
+  DeviceGuard dg(e->ctx->device);
+  ExportBlob b{};
+  b.magic = kBlobMagic;
+  b.p = e->p;
+  b.me = e->me;
+  b.mode = e->cfg.mode;
+  b.win_bytes = e->win_bytes;
+  b.flags_off = e->flags_off;
+  for (int ch = 0; ch < NCH; ++ch) {
+    b.ch_off[ch] = e->ch_off[ch];
+    b.ch_slot[ch] = e->ch_slot[ch];
+  }
+  FSX_CUDA(cudaIpcGetMemHandle(&b.handle, e->win));
+  std::memcpy(blob, &b, sizeof b);
+  *len = sizeof b;
+  FSX_API_END
+}
+
+int fsx_engine_connect_ipc(fsx_engine* e, int peer, const void* blob, uint64_t len) {
+  FSX_API_BEGIN
+  DeviceGuard dg(e->ctx->device);
+  ExportBlob b{};
+  if (len != sizeof b) raise(FSX_ERR_COLLECTIVE, "fsx: bad peer blob");
+  std::memcpy(&b, blob, sizeof b);
+  if (b.magic != kBlobMagic || b.p != e->p || b.me != peer || b.win_bytes != e->win_bytes ||
+      b.flags_off != e->flags_off)
+    raise(FSX_ERR_COLLECTIVE, "fsx: peer " + std::to_string(peer) + " window layout mismatch");
+  void* base = nullptr;
+  FSX_CUDA(cudaIpcOpenMemHandle(&base, b.handle, cudaIpcMemLazyEnablePeerAccess));
+  e->peer[peer].base = static_cast<char*>(base);
+  e->peer[peer].flags = reinterpret_cast<uint32_t*>(static_cast<char*>(base) + b.flags_off);
+  e->peer[peer].ipc = true;
+  FSX_API_END
+}
+
+int fsx_nccl_unique_id(void*) {
+  capi_set_error("fsx: NCCL baseline transport not built");
+  return FSX_ERR_CONFIG;
+}
+int fsx_engine_connect_nccl(fsx_engine*, const void*) {
+  capi_set_error("fsx: NCCL baseline transport not built");
+  return FSX_ERR_CONFIG;
+}
+
+int fsx_engine_forward(fsx_engine* e, const uint64_t* d_ids_cur, uint64_t n_cur,
+                       const uint64_t* d_ids_next, uint64_t n_next, void* d_out, void* stream) {
+  FSX_API_BEGIN
+  DeviceGuard dg(e->ctx->device);
+  e->cur_c = S(stream);
+  e->waits.clear();
+  e->timing_next = 0;
+  if (e->cfg.mode == FSX_MODE_SYNC)
+    e->sync_forward(d_ids_cur, n_cur, d_out, S(stream));
+  else
+    e->prio_forward(d_ids_cur, n_cur, d_ids_next, n_next, d_out, S(stream));
+  FSX_API_END
+}
+
+int fsx_engine_backward(fsx_engine* e, const void* d_grads, void* stream) {
+  FSX_API_BEGIN
+  DeviceGuard dg(e->ctx->device);
+  e->cur_c = S(stream);
+  if (e->cfg.mode == FSX_MODE_SYNC)
+    e->sync_backward(d_grads, S(stream));
+  else
+    e->prio_backward(d_grads, S(stream));
+  FSX_API_END
+}
+
+int fsx_engine_finalize(fsx_engine* e, void* stream) {
+  FSX_API_BEGIN
+  DeviceGuard dg(e->ctx->device);
+  if (e->cfg.mode == FSX_MODE_PRIO) e->finalize(S(stream));
+  FSX_API_END
+}
+
+int fsx_engine_stats(fsx_engine* e, int iter, uint64_t* out3) {
+  FSX_API_BEGIN
+  DeviceGuard dg(e->ctx->device);
+  if (iter < 0 || iter >= e->stats_n) raise(FSX_ERR_OUT_OF_RANGE, "fsx: no stats for iteration " + std::to_string(iter));
+  FSX_CUDA(cudaDeviceSynchronize());
+  std::memcpy(out3, e->h_stats + 3 * static_cast<size_t>(iter), 24);
+  FSX_API_END
+}
+
+int fsx_engine_exposed_ms(fsx_engine* e, double* ms) {
+  FSX_API_BEGIN
+  DeviceGuard dg(e->ctx->device);
+  double total = 0;
+  for (auto& w : e->waits) {
+    FSX_CUDA(cudaEventSynchronize(w.second));
+    float x = 0;
+    FSX_CUDA(cudaEventElapsedTime(&x, w.first, w.second));
+    total += x;
+  }
+  *ms = total;
+  FSX_API_END
+}
+
+uint64_t fsx_engine_slot_bytes(const fsx_engine* e) { return e ? e->ch_slot[CH_GRADS] - kHdr : 0; }
+
+}  // extern "C"

@@ -1,0 +1,426 @@
+// Device side of the embedding engines (SynchronizedEmbedding /
+// PrioritizedEmbedding, embedding.cpp:235-607).
+//
+// Wire format of every message slot (one per (channel, peer)):
+//   [u64 n][u64 reserved][payload]
+// payload = n u64 ids                       (IDS)
+//         | n rows                          (ROWS, GRADS, CO_G, EX_G)
+//         | n u64 ids, pad16, n rows        (EX, CO_R; rows at 16+align16(8n))
+//         | n u8 flags                      (MASK)
+// The reference's [u64 count][ids][rows] (embedding.cpp:29-55) with the ids
+// 16-byte aligned so rows move as 128-bit vectors.
+#pragma once
+
+#include "table.cuh"
+
+namespace fsx {
+
+constexpr int kMaxRanks = 16;
+constexpr uint64_t kHdr = 16;
+
+__host__ __device__ __forceinline__ uint64_t align16(uint64_t x) { return (x + 15) & ~uint64_t(15); }
+__host__ __device__ __forceinline__ uint64_t idrows_rows_off(uint64_t n) { return kHdr + align16(8 * n); }
+
+// per-peer slot base addresses of one channel as seen by this rank
+struct Slots {
+  char* p[kMaxRanks];
+};
+struct CSlots {
+  const char* p[kMaxRanks];
+};
+
+__device__ __forceinline__ uint64_t slot_n(const char* s) { return *reinterpret_cast<const uint64_t*>(s); }
+
+// ---- headers ---------------------------------------------------------------
+// n of destination d = counts[d * stride] (device); one thread per slot.
+static __global__ void k_write_headers(Slots dst, int p, const uint64_t* counts, int stride,
+                                uint64_t cap, DevErr* err) {
+  const int d = threadIdx.x;
+  if (d < p) {
+    const uint64_t n = counts[d * stride];
+    if (n > cap) report(err, kErrCapacity, n, cap);
+    reinterpret_cast<uint64_t*>(dst.p[d])[0] = n;
+    reinterpret_cast<uint64_t*>(dst.p[d])[1] = 0;
+  }
+}
+
+// ---- requester: route (embedding.cpp:194-212) -------------------------------
+// stable partition by owner straight into the IDS send slots
+template <int NC_>
+struct RouteOp {
+  static constexpr int NC = NC_;
+  const uint64_t* ids;
+  uint64_t total_rows;
+  int p;
+  const uint64_t* totals;   // per-owner counts (scan phase 2)
+  Slots send;               // IDS send slots
+  uint32_t* send_pos;       // grouped k -> position j
+  uint8_t* send_dst;        // grouped k -> owner
+  uint64_t cap;
+  DevErr* err;
+  __device__ void count(uint64_t i, uint32_t (&c)[NC]) const {
+    const uint64_t id = ids[i];
+    const int o = static_cast<int>(id % static_cast<uint64_t>(p));
+#pragma unroll
+    for (int q = 0; q < NC; ++q) c[q] = (q == o && id < total_rows) ? 1u : 0u;
+  }
+  __device__ void emit(uint64_t i, const uint32_t (&ex)[NC], const uint32_t (&c)[NC]) const {
+    const uint64_t id = ids[i];
+    if (id >= total_rows) {
+      report(err, kErrRowRange, id, total_rows);
+      return;
+    }
+    const int o = static_cast<int>(id % static_cast<uint64_t>(p));
+    uint64_t base = 0;
+    for (int q = 0; q < o; ++q) base += totals[q];
+    uint32_t r = 0;
+#pragma unroll
+    for (int q = 0; q < NC; ++q)
+      if (q == o) r = ex[q];
+    if (r >= cap) {
+      report(err, kErrCapacity, static_cast<unsigned long long>(r) + 1, cap);
+      return;
+    }
+    reinterpret_cast<uint64_t*>(send.p[o] + kHdr)[r] = id;
+    send_pos[base + r] = static_cast<uint32_t>(i);
+    send_dst[base + r] = static_cast<uint8_t>(o);
+  }
+};
+
+// requester composite key (owner, local index) so per-owner unique lists come
+// out as contiguous sorted runs (== the owner's recv_unique_per_src order)
+static __global__ void k_requester_keys(const uint64_t* __restrict__ ids, uint64_t n, int p, int lbits,
+                                 uint64_t* __restrict__ keys) {
+  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < n;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t id = ids[j];
+    keys[j] = (static_cast<uint64_t>(id % static_cast<uint64_t>(p)) << lbits) |
+              (id / static_cast<uint64_t>(p));
+  }
+}
+
+// unique composite keys -> global ids and per-owner offsets uq_off[p+1]
+static __global__ void k_requester_uq(const uint64_t* __restrict__ uq_key, const uint64_t* d_u, int p,
+                               int lbits, uint64_t* __restrict__ uq_g, uint32_t* __restrict__ uq_off) {
+  const uint64_t U = *d_u;
+  const uint64_t mask = (lbits >= 64) ? ~0ull : ((1ull << lbits) - 1);
+  for (uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; u < U;
+       u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t k = uq_key[u];
+    const int d = static_cast<int>(k >> lbits);
+    uq_g[u] = (k & mask) * static_cast<uint64_t>(p) + static_cast<uint64_t>(d);
+    const int prev = u == 0 ? -1 : static_cast<int>(uq_key[u - 1] >> lbits);
+    for (int q = prev + 1; q <= d; ++q) uq_off[q] = static_cast<uint32_t>(u);
+    if (u + 1 == U)
+      for (int q = d + 1; q <= p; ++q) uq_off[q] = static_cast<uint32_t>(U);
+  }
+  if (U == 0 && blockIdx.x == 0 && threadIdx.x <= static_cast<unsigned>(p)) uq_off[threadIdx.x] = 0;
+}
+
+// ---- owner: flatten received ids (embedding.cpp:214-229) ----------------------
+// cnt[0] = M, cnt[2+s] = n_s, off[s] prefix (cnt[2+p+s])
+static __global__ void k_recv_prefix(CSlots slots, int p, uint64_t cap, uint64_t* cnt, DevErr* err) {
+  if (threadIdx.x == 0) {
+    uint64_t off = 0;
+    for (int s = 0; s < p; ++s) {
+      const uint64_t n = slot_n(slots.p[s]);
+      if (n > cap) report(err, kErrCapacity, n, cap);
+      cnt[2 + s] = n;
+      cnt[2 + kMaxRanks + s] = off;
+      off += n <= cap ? n : cap;
+    }
+    cnt[0] = off;
+  }
+}
+
+static __global__ void k_flatten_recv(CSlots slots, int p, uint64_t cap, const uint64_t* cnt, ShardGeom g,
+                               uint64_t* __restrict__ ids, uint8_t* __restrict__ occ_src,
+                               uint32_t* __restrict__ occ_idx, DevErr* err) {
+  const uint64_t total = static_cast<uint64_t>(p) * cap;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const int s = static_cast<int>(i / cap);
+    const uint64_t idx = i - static_cast<uint64_t>(s) * cap;
+    if (idx >= cnt[2 + s]) continue;
+    const uint64_t id = reinterpret_cast<const uint64_t*>(slots.p[s] + kHdr)[idx];
+    if (!g.owns(id)) report(err, kErrRecvNotOwned, id, g.shard);
+    const uint64_t j = cnt[2 + kMaxRanks + s] + idx;
+    ids[j] = id;
+    occ_src[j] = static_cast<uint8_t>(s);
+    occ_idx[j] = static_cast<uint32_t>(idx);
+  }
+}
+
+// src bitmask per unique row: bit s set iff source s requested it
+static __global__ void k_src_bits(const uint32_t* __restrict__ inverse, const uint8_t* __restrict__ occ_src,
+                           const uint64_t* d_m, uint32_t* __restrict__ bits) {
+  const uint64_t m = *d_m;
+  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < m;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    atomicOr(&bits[inverse[j]], 1u << occ_src[j]);
+}
+
+// ---- owner: per-source pack lists -------------------------------------------
+// Over the unique rows of the NEXT batch: counters 2s (bit s, exclusive) and
+// 2s+1 (bit s, collision). Emits entry lists: ex_list / co_list, ordered by
+// source then rank (rank = position inside that source's message).
+struct PackEntry {
+  uint32_t u;
+  uint32_t rank;
+  uint32_t src;
+  uint32_t pad;
+};
+
+template <int NC_>
+struct OwnerPackOp {
+  static constexpr int NC = NC_;  // 2 * kMax(p)
+  const uint32_t* bits;
+  const uint8_t* co;          // co flag per unique row of the batch
+  int p;
+  const uint64_t* totals;     // [NC] from phase 2
+  PackEntry* ex_list;
+  PackEntry* co_list;
+  __device__ void count(uint64_t u, uint32_t (&c)[NC]) const {
+    const uint32_t b = bits[u];
+    const uint32_t f = co[u] ? 1u : 0u;
+#pragma unroll
+    for (int q = 0; q < NC / 2; ++q) {
+      const uint32_t has = (b >> q) & 1u;
+      c[2 * q] = has & (1u - f);
+      c[2 * q + 1] = has & f;
+    }
+  }
+  __device__ void emit(uint64_t u, const uint32_t (&ex)[NC], const uint32_t (&c)[NC]) const {
+    const uint32_t b = bits[u];
+    const uint32_t f = co[u] ? 1u : 0u;
+    uint64_t base_ex = 0, base_co = 0;
+#pragma unroll
+    for (int q = 0; q < NC / 2; ++q) {
+      if ((b >> q) & 1u) {
+        PackEntry e{static_cast<uint32_t>(u), ex[2 * q + f], static_cast<uint32_t>(q), 0};
+        if (f) co_list[base_co + e.rank] = e;
+        else ex_list[base_ex + e.rank] = e;
+      }
+      base_ex += totals[2 * q];
+      base_co += totals[2 * q + 1];
+    }
+  }
+};
+
+// MASK messages of the CURRENT batch: for each unique row and each source
+// that asked for it, the row's collision flag at the row's rank in that
+// source's (sorted) unique list. Counter s = bit s.
+template <int NC_>
+struct MaskOp {
+  static constexpr int NC = NC_;
+  const uint32_t* bits;
+  const uint8_t* co;
+  Slots send;  // MASK send slots
+  __device__ void count(uint64_t u, uint32_t (&c)[NC]) const {
+    const uint32_t b = bits[u];
+#pragma unroll
+    for (int q = 0; q < NC; ++q) c[q] = (b >> q) & 1u;
+  }
+  __device__ void emit(uint64_t u, const uint32_t (&ex)[NC], const uint32_t (&c)[NC]) const {
+    const uint32_t b = bits[u];
+    const uint8_t f = co ? co[u] : 0;
+#pragma unroll
+    for (int q = 0; q < NC; ++q)
+      if ((b >> q) & 1u) reinterpret_cast<uint8_t*>(send.p[q] + kHdr)[ex[q]] = f;
+  }
+};
+
+// per-occurrence rank inside its (source, flag) class, flat recv order:
+// counters 2s (exclusive) / 2s+1 (collision)
+template <int NC_>
+struct OccRankOp {
+  static constexpr int NC = NC_;
+  const uint8_t* occ_src;
+  const uint32_t* inverse;
+  const uint8_t* co;          // nullable -> all exclusive
+  uint32_t* occ_rank;
+  __device__ void count(uint64_t j, uint32_t (&c)[NC]) const {
+    const int s = occ_src[j];
+    const uint32_t f = co ? (co[inverse[j]] ? 1u : 0u) : 0u;
+#pragma unroll
+    for (int q = 0; q < NC; ++q) c[q] = (q == 2 * s + static_cast<int>(f)) ? 1u : 0u;
+  }
+  __device__ void emit(uint64_t j, const uint32_t (&ex)[NC], const uint32_t (&c)[NC]) const {
+    const int s = occ_src[j];
+    const uint32_t f = co ? (co[inverse[j]] ? 1u : 0u) : 0u;
+    uint32_t r = 0;
+#pragma unroll
+    for (int q = 0; q < NC; ++q)
+      if (q == 2 * s + static_cast<int>(f)) r = ex[q];
+    occ_rank[j] = r;
+  }
+};
+
+// ---- requester: collision flags from the MASK messages ------------------------
+static __global__ void k_requester_flags(CSlots mask, const uint32_t* __restrict__ uq_off, int p,
+                                  const uint64_t* d_u, uint8_t* __restrict__ flag, DevErr* err) {
+  const uint64_t U = *d_u;
+  for (uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; u < U;
+       u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    int d = 0;
+    while (d + 1 < p && uq_off[d + 1] <= u) ++d;
+    const uint64_t q = u - uq_off[d];
+    const uint64_t n = slot_n(mask.p[d]);
+    if (n != uq_off[d + 1] - uq_off[d]) {
+      report(err, kErrMaskOverlap, n, uq_off[d + 1] - uq_off[d]);
+      flag[u] = 0;
+      continue;
+    }
+    flag[u] = reinterpret_cast<const uint8_t*>(mask.p[d] + kHdr)[q];
+  }
+}
+
+// split counters over the grouped send order: 2d + flag
+template <int NC_>
+struct SplitOp {
+  static constexpr int NC = NC_;
+  const uint32_t* send_pos;
+  const uint8_t* send_dst;
+  const uint32_t* occ_slot;  // position j -> requester unique slot
+  const uint8_t* flag;       // per unique slot (nullable -> all exclusive)
+  uint32_t* split_rank;      // grouped k -> rank in its (dst, flag) message
+  __device__ uint32_t f(uint64_t k) const {
+    return flag ? (flag[occ_slot[send_pos[k]]] ? 1u : 0u) : 0u;
+  }
+  __device__ void count(uint64_t k, uint32_t (&c)[NC]) const {
+    const int d = send_dst[k];
+    const uint32_t fl = f(k);
+#pragma unroll
+    for (int q = 0; q < NC; ++q) c[q] = (q == 2 * d + static_cast<int>(fl)) ? 1u : 0u;
+  }
+  __device__ void emit(uint64_t k, const uint32_t (&ex)[NC], const uint32_t (&c)[NC]) const {
+    const int d = send_dst[k];
+    const uint32_t fl = f(k);
+    uint32_t r = 0;
+#pragma unroll
+    for (int q = 0; q < NC; ++q)
+      if (q == 2 * d + static_cast<int>(fl)) r = ex[q];
+    split_rank[k] = r;
+  }
+};
+
+// ---- row movers (all go through k_copy_rows) ----------------------------------
+// sync forward, owner side: per received occurrence, its row into the ROWS
+// send slot of its source at its index (embedding.cpp:245-248)
+struct OwnerLookupMap {
+  const char* table;
+  const uint64_t* ids;
+  const uint8_t* occ_src;
+  const uint32_t* occ_idx;
+  Slots send;
+  uint32_t row_bytes;
+  int p;
+  __device__ const char* src(uint64_t j) const {
+    return table + (ids[j] / static_cast<uint64_t>(p)) * row_bytes;
+  }
+  __device__ char* dst(uint64_t j) const {
+    return send.p[occ_src[j]] + kHdr + static_cast<uint64_t>(occ_idx[j]) * row_bytes;
+  }
+};
+
+// sync forward, requester side: reply row k of owner d -> out[send_pos[k]]
+// (embedding.cpp:252-264)
+struct RequesterScatterMap {
+  CSlots recv;
+  const uint32_t* send_pos;
+  const uint8_t* send_dst;
+  const uint64_t* send_off;  // per owner start in the grouped order (device)
+  char* out;
+  uint32_t row_bytes;
+  __device__ const char* src(uint64_t k) const {
+    const int d = send_dst[k];
+    return recv.p[d] + kHdr + (k - send_off[d]) * row_bytes;
+  }
+  __device__ char* dst(uint64_t k) const { return out + static_cast<uint64_t>(send_pos[k]) * row_bytes; }
+};
+
+// backward, requester side: grads of grouped k into GRADS / CO_G / EX_G send
+// slots (embedding.cpp:276-286, 526-536). split_rank == nullptr: sync pack.
+struct GradPackMap {
+  const char* grads;
+  const uint32_t* send_pos;
+  const uint8_t* send_dst;
+  const uint64_t* send_off;
+  const uint32_t* occ_slot;
+  const uint8_t* flag;        // nullable: everything to `ex`
+  const uint32_t* split_rank; // nullable: rank = k - send_off[d]
+  Slots co, ex;
+  uint32_t row_bytes;
+  __device__ const char* src(uint64_t k) const {
+    return grads + static_cast<uint64_t>(send_pos[k]) * row_bytes;
+  }
+  __device__ char* dst(uint64_t k) const {
+    const int d = send_dst[k];
+    const bool f = flag && flag[occ_slot[send_pos[k]]];
+    const uint64_t r = split_rank ? split_rank[k] : k - send_off[d];
+    return (f ? co.p[d] : ex.p[d]) + kHdr + r * row_bytes;
+  }
+};
+
+// owner pack of [ids][rows] messages (EX prefetch, E_co) from the entry lists
+struct IdRowPackMap {
+  const char* table;
+  const uint64_t* uniq_local;
+  const uint64_t* uniq_g;
+  const PackEntry* list;
+  Slots send;
+  const uint64_t* totals;  // per-source counts: totals[2*s + which]
+  int which;
+  uint32_t row_bytes;
+  __device__ const char* src(uint64_t i) const {
+    const PackEntry e = list[i];
+    // the id rides in the same pass
+    reinterpret_cast<uint64_t*>(send.p[e.src] + kHdr)[e.rank] = uniq_g[e.u];
+    return table + uniq_local[e.u] * row_bytes;
+  }
+  __device__ char* dst(uint64_t i) const {
+    const PackEntry e = list[i];
+    const uint64_t n = totals[2 * e.src + which];
+    return send.p[e.src] + idrows_rows_off(n) + static_cast<uint64_t>(e.rank) * row_bytes;
+  }
+};
+
+// requester: locate every unique slot's row in the EX or CO_R message of its
+// owner (embedding.cpp:465-482: lower_bound per id)
+static __global__ void k_resolve_rows(CSlots ex, CSlots co, const uint64_t* __restrict__ uq_g,
+                               const uint32_t* __restrict__ uq_off, int p, const uint64_t* d_u,
+                               uint32_t row_bytes, const char** __restrict__ rowptr, DevErr* err) {
+  const uint64_t U = *d_u;
+  for (uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; u < U;
+       u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    int d = 0;
+    while (d + 1 < p && uq_off[d + 1] <= u) ++d;
+    const uint64_t id = uq_g[u];
+    const char* hit = nullptr;
+    for (int which = 0; which < 2 && !hit; ++which) {
+      const char* s = which == 0 ? ex.p[d] : co.p[d];
+      if (!s) continue;
+      const uint64_t n = slot_n(s);
+      const uint64_t* ids = reinterpret_cast<const uint64_t*>(s + kHdr);
+      uint64_t lo = 0, hi = n;
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (ids[mid] < id) lo = mid + 1; else hi = mid;
+      }
+      if (lo < n && ids[lo] == id) hit = s + idrows_rows_off(n) + lo * row_bytes;
+    }
+    if (!hit) report(err, kErrMissingRow, id, 0);
+    rowptr[u] = hit;
+  }
+}
+
+struct MergeMap {
+  const char* const* rowptr;
+  const uint32_t* occ_slot;
+  char* out;
+  uint32_t row_bytes;
+  __device__ const char* src(uint64_t j) const { return rowptr[occ_slot[j]]; }
+  __device__ char* dst(uint64_t j) const { return out + j * row_bytes; }
+};
+
+}  // namespace fsx

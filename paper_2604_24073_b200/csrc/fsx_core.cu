@@ -80,8 +80,6 @@ __global__ void k_intersect_flags(const uint64_t* __restrict__ a, const uint64_t
 
 using namespace fsx;
 
-struct fsx_ctx : Ctx {};
-struct fsx_table : Table {};
 
 namespace {
 

@@ -65,7 +65,7 @@ __device__ __forceinline__ void block_exclusive_scan(uint32_t (&v)[NC], uint32_t
 }
 
 template <class Op>
-__global__ void __launch_bounds__(kScanThreads) k_tile_reduce(Op op, uint64_t n_cap,
+static __global__ void __launch_bounds__(kScanThreads) k_tile_reduce(Op op, uint64_t n_cap,
                                                               const uint64_t* d_n,
                                                               uint32_t* tile_sums) {
   constexpr int NC = Op::NC;
@@ -131,7 +131,7 @@ __device__ __forceinline__ uint32_t block1024_exclusive(uint32_t& v) {
 
 // One CTA: in-place exclusive scan of n u32 (each thread a contiguous chunk).
 // Returns nothing; used for radix tile-offset tables.
-__global__ void __launch_bounds__(1024) k_scan_u32(uint32_t* data, uint64_t n) {
+static __global__ void __launch_bounds__(1024) k_scan_u32(uint32_t* data, uint64_t n) {
   const uint64_t per = (n + blockDim.x - 1) / blockDim.x;
   const uint64_t lo = threadIdx.x * per;
   const uint64_t hi = lo + per < n ? lo + per : n;
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(1024) k_scan_u32(uint32_t* data, uint64_t n) {
 // One CTA: exclusive scan over `tiles` rows of NC counters (in place), grand
 // totals to `totals` (device) as u64.
 template <int NC>
-__global__ void __launch_bounds__(1024) k_scan_tiles(uint32_t* tile_sums, unsigned tiles,
+static __global__ void __launch_bounds__(1024) k_scan_tiles(uint32_t* tile_sums, unsigned tiles,
                                                      uint64_t* totals) {
   const unsigned per = (tiles + blockDim.x - 1) / blockDim.x;
   const unsigned lo = threadIdx.x * per;
@@ -167,7 +167,7 @@ __global__ void __launch_bounds__(1024) k_scan_tiles(uint32_t* tile_sums, unsign
 }
 
 template <class Op>
-__global__ void __launch_bounds__(kScanThreads) k_tile_emit(Op op, uint64_t n_cap,
+static __global__ void __launch_bounds__(kScanThreads) k_tile_emit(Op op, uint64_t n_cap,
                                                             const uint64_t* d_n,
                                                             const uint32_t* tile_prefix) {
   constexpr int NC = Op::NC;

@@ -61,3 +61,7 @@ void sgd_update_rows(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_ca
 }
 
 }  // namespace fsx
+
+// opaque C-ABI handles (include/fsx.h) are the internal objects
+struct fsx_ctx : fsx::Ctx {};
+struct fsx_table : fsx::Table {};

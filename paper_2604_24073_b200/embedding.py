@@ -270,3 +270,143 @@ def _wrap_device(ptr: int, n: int, dtype: torch.dtype, device: int) -> torch.Ten
 
     with torch.cuda.device(device):
         return torch.as_tensor(_CAI(), device=torch.device("cuda", device))
+
+
+# ---- engines (embedding.hpp:126-189) -------------------------------------------
+@dataclass
+class IterationStats:
+    """embedding.hpp:119-124 (blocking_bytes in the reference's 8-byte-value
+    accounting, whatever the table dtype)."""
+    collision_rows: int = 0
+    unique_next_rows: int = 0
+    blocking_bytes: int = 0
+
+    @property
+    def collision_fraction(self) -> float:
+        return self.collision_rows / self.unique_next_rows if self.unique_next_rows else 0.0
+
+
+class _Engine:
+    _mode = _lib.FSX_MODE_SYNC
+
+    def __init__(self, shard: ShardView, comm=None, max_occurrences: int = 1 << 16,
+                 reduce_chunk: int = 0):
+        from .comm import DeviceFabric
+        self.shard = shard
+        if comm is None:
+            comm = DeviceFabric(1, [shard.ctx.device]).communicator(0)
+        self.comm = comm
+        if comm.world_size() != shard.geom.num_shards or comm.rank() != shard.shard_id:
+            raise InvalidArgument("embedding: shard geometry does not match the communicator")
+        cfg = _lib.EngineConfig(self._mode, _lib.FSX_TRANSPORT_CE, max_occurrences, reduce_chunk)
+        h = C.c_void_p()
+        _lib.call("fsx_engine_create", shard.ctx.h, shard.h, C.byref(cfg), C.byref(h))
+        self.h = h
+        self.max_occurrences = max_occurrences
+        self._n_cur = None
+        comm.connect(h)
+
+    def _ids(self, ids) -> torch.Tensor:
+        return _dev_u64(ids, self.shard.ctx.torch_device)
+
+    def exposed_ms(self) -> float:
+        v = C.c_double()
+        _lib.call("fsx_engine_exposed_ms", self.h, C.byref(v))
+        return v.value
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            _lib.lib().fsx_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class SynchronizedEmbedding(_Engine):
+    """Blocking baseline (embedding.cpp:235-297)."""
+    _mode = _lib.FSX_MODE_SYNC
+
+    def forward(self, ids, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        d = self._ids(ids)
+        n = d.numel()
+        if out is None:
+            out = torch.empty((n, self.shard.geom.dim), dtype=self.shard.torch_dtype, device=d.device)
+        _lib.call("fsx_engine_forward", self.h, _ptr(d), n, None, 0, _ptr(out), _stream(stream))
+        self._keep = d
+        self._n_cur = n
+        return out
+
+    def backward(self, grads: torch.Tensor, stream=None) -> None:
+        if self._n_cur is None:
+            raise ProtocolError("embedding: backward before forward")
+        g = grads.to(dtype=self.shard.torch_dtype).contiguous()
+        if g.numel() != self._n_cur * self.shard.geom.dim:
+            raise InvalidArgument("embedding: gradient count does not match forward occurrences")
+        _lib.call("fsx_engine_backward", self.h, _ptr(g), _stream(stream))
+        self._keep_g = g
+        self._n_cur = None
+
+
+class PrioritizedEmbedding(_Engine):
+    """Collision-first protocol (embedding.cpp:301-607)."""
+    _mode = _lib.FSX_MODE_PRIO
+
+    def __init__(self, *a, **kw):
+        super().__init__(*a, **kw)
+        self._iters = 0
+        self._keep = []
+
+    def forward(self, ids_cur, ids_next=None, out: torch.Tensor | None = None,
+                stream=None) -> torch.Tensor:
+        c = self._ids(ids_cur)
+        nx = None if ids_next is None else self._ids(ids_next)
+        n = c.numel()
+        if out is None:
+            out = torch.empty((n, self.shard.geom.dim), dtype=self.shard.torch_dtype, device=c.device)
+        _lib.call("fsx_engine_forward", self.h, _ptr(c), n, _ptr(nx),
+                  0 if nx is None else nx.numel(), _ptr(out), _stream(stream))
+        self._keep = [c, nx, out]
+        self._n_cur = n
+        self._iters += 1
+        return out
+
+    def backward(self, grads: torch.Tensor, stream=None) -> None:
+        if self._n_cur is None:
+            raise ProtocolError("embedding: backward before forward")
+        g = grads.to(dtype=self.shard.torch_dtype).contiguous()
+        if g.numel() != self._n_cur * self.shard.geom.dim:
+            raise InvalidArgument("embedding: gradient count does not match forward occurrences")
+        _lib.call("fsx_engine_backward", self.h, _ptr(g), _stream(stream))
+        self._keep.append(g)
+        self._n_cur = None
+
+    def finalize(self, stream=None) -> None:
+        _lib.call("fsx_engine_finalize", self.h, _stream(stream))
+
+    def stats(self) -> list[IterationStats]:
+        out = []
+        buf = (C.c_uint64 * 3)()
+        for i in range(self._iters):
+            _lib.call("fsx_engine_stats", self.h, i, buf)
+            out.append(IterationStats(buf[0], buf[1], buf[2]))
+        return out
+
+
+def gather_full_table(shards: list[ShardView]) -> np.ndarray:
+    """gather_full_table (embedding.cpp:611-631) from every rank's shard:
+    the full table in global row-major order (f64)."""
+    geom = shards[0].geom
+    full = np.zeros((geom.total_rows, geom.dim), np.float64)
+    for s in shards:
+        full[s.shard_id::geom.num_shards] = s.values()
+    return full
+
+
+def checkpoint_bytes(geom: TableGeometry, full_table: np.ndarray) -> bytes:
+    """embedding.cpp:633-640: u64 rows, u64 dim, u64 shards, row-major f64."""
+    hdr = np.array([geom.total_rows, geom.dim, geom.num_shards], np.uint64).tobytes()
+    return hdr + np.ascontiguousarray(full_table, np.float64).tobytes()
