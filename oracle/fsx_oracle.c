@@ -223,11 +223,36 @@ static uint64_t shard_unique(int world, const uint64_t* ids, uint64_t n, int s, 
   return fso_sorted_unique(out, k);
 }
 
+/* store_f32 != 0 models an fp32 table: values are rounded to float after
+ * init and after every update, and the caller's gradient fixture is evaluated
+ * in float arithmetic (g = fl(fl(scale*row) + shift), as a float32 tensor op
+ * would); sums and the update itself stay f64, exactly as the reference. */
+int fso_run_engine_ex(int world, int iters, const uint64_t* ids, const uint64_t* lens,
+                      uint64_t total_rows, uint32_t dim, double lr, uint64_t seed, double grad_scale,
+                      double grad_shift, double* table, uint64_t* stats_out, int store_f32);
+
 int fso_run_engine(int world, int iters, const uint64_t* ids, const uint64_t* lens,
                    uint64_t total_rows, uint32_t dim, double lr, uint64_t seed, double grad_scale,
                    double grad_shift, double* table, uint64_t* stats_out) {
+  return fso_run_engine_ex(world, iters, ids, lens, total_rows, dim, lr, seed, grad_scale, grad_shift,
+                           table, stats_out, 0);
+}
+
+static double fixture(double row, double scale, double shift, int f32) {
+  if (!f32) return scale * row + shift;
+  float a = (float)row * (float)scale;
+  float b = a + (float)shift;
+  return (double)b;
+}
+
+int fso_run_engine_ex(int world, int iters, const uint64_t* ids, const uint64_t* lens,
+                      uint64_t total_rows, uint32_t dim, double lr, uint64_t seed, double grad_scale,
+                      double grad_shift, double* table, uint64_t* stats_out, int store_f32) {
   for (uint64_t g = 0; g < total_rows; ++g)
-    for (uint32_t d = 0; d < dim; ++d) table[g * dim + d] = fso_initial_value(seed, g, d);
+    for (uint32_t d = 0; d < dim; ++d) {
+      double v = fso_initial_value(seed, g, d);
+      table[g * dim + d] = store_f32 ? (double)(float)v : v;
+    }
   uint64_t* it_start = malloc(((size_t)iters + 1) * 8);
   uint64_t at = 0, maxn = 0;
   for (int i = 0; i < iters; ++i) {
@@ -335,8 +360,9 @@ int fso_run_engine(int world, int iters, const uint64_t* ids, const uint64_t* le
       double* row = table + occ[k].id * dim;
       for (uint32_t d = 0; d < dim; ++d) {
         double acc = 0.0;
-        for (uint64_t q = k; q < e; ++q) acc += grad_scale * served[occ[q].seq * dim + d] + grad_shift;
+        for (uint64_t q = k; q < e; ++q) acc += fixture(served[occ[q].seq * dim + d], grad_scale, grad_shift, store_f32);
         row[d] -= lr * acc;
+        if (store_f32) row[d] = (double)(float)row[d];
         if (!isfinite(row[d])) {
           free(occ); free(served); free(it_start);
           return fail(FSO_DOMAIN, "embedding: non-finite value after update of row %llu%.0llu", occ[k].id, 0);

@@ -53,6 +53,10 @@ int fso_run_engine(int world, int iters, const uint64_t* ids, const uint64_t* le
                    uint64_t total_rows, uint32_t dim, double lr, uint64_t seed, double grad_scale,
                    double grad_shift, double* table_out, uint64_t* stats_out);
 
+int fso_run_engine_ex(int world, int iters, const uint64_t* ids, const uint64_t* lens,
+                      uint64_t total_rows, uint32_t dim, double lr, uint64_t seed, double grad_scale,
+                      double grad_shift, double* table_out, uint64_t* stats_out, int store_f32);
+
 int fso_fbs(const uint64_t* lens, const int* origin, const int* local, uint64_t m, int n,
             int* assignment, uint64_t* order, uint64_t* order_lens);
 int fso_vbs(const uint64_t* lens, const int* origin, const int* local, uint64_t m, int n,

@@ -15,6 +15,13 @@
 // (cuStreamWriteValue32 after each copy-engine copy, cuStreamWaitValue32 on
 // the receiving lane) — no SM ever spins and no kernel touches a peer.
 #include <algorithm>
+#include <chrono>
+#include <condition_variable>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -133,6 +140,44 @@ struct PeerView {
   char* base = nullptr;       // peer's receive window (mapped)
   uint32_t* flags = nullptr;  // peer's flag words (mapped)
   bool ipc = false;
+  void* local = nullptr;      // in-process peer engine (host mailbox signalling)
+};
+
+// In-process signalling: ranks that are threads of one process (the
+// reference's InProcessFabric shape, several ranks may share a GPU) hand each
+// other CUDA events through a host mailbox instead of flag words. A receiver
+// only ever waits on an event that was already recorded, so no stream can park
+// on work that is queued behind it (flag waits between streams of ONE GPU can
+// deadlock when the streams share a hardware queue).
+struct Hub {
+  std::mutex mu;
+  std::condition_variable cv;
+  std::map<std::tuple<const void*, int, uint32_t, int>, cudaEvent_t> box;  // (dst engine, ch, seq, src)
+  static Hub& get() {
+    static Hub h;
+    return h;
+  }
+  void post(const void* dst, int ch, uint32_t seq, int src, cudaEvent_t ev) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      box[{dst, ch, seq, src}] = ev;
+    }
+    cv.notify_all();
+  }
+  cudaEvent_t take(const void* dst, int ch, uint32_t seq, int src) {
+    static const int timeout_s = [] {
+      const char* v = std::getenv("FSX_HUB_TIMEOUT_S");
+      return v ? std::atoi(v) : 300;
+    }();
+    std::unique_lock<std::mutex> lk(mu);
+    const auto key = std::make_tuple(dst, ch, seq, src);
+    if (!cv.wait_for(lk, std::chrono::seconds(timeout_s), [&] { return box.count(key) > 0; }))
+      raise(FSX_ERR_COLLECTIVE, "collective aborted: no message from rank " + std::to_string(src) +
+                                    " on channel " + std::to_string(ch) + " (timeout)");
+    cudaEvent_t ev = box[key];
+    box.erase(key);
+    return ev;
+  }
 };
 
 struct Engine {
@@ -140,6 +185,7 @@ struct Engine {
   Table* t = nullptr;
   fsx_engine_config cfg{};
   int p = 1, me = 0;
+  bool debug = std::getenv("FSX_DEBUG") != nullptr;
   uint64_t cap = 0;       // ids per rank per iteration
   uint32_t rb = 0;        // row bytes
   // receive window (IPC-exportable): per channel [2 parities][p slots][slot]
@@ -167,11 +213,13 @@ struct Engine {
   bool has_pending = false;
   int exg_par = -1;
   cudaEvent_t ev_ex_ready = nullptr, ev_co_ready = nullptr, ev_mask = nullptr, ev_split = nullptr;
-  // stats slab (pinned): [iter][3]
-  uint64_t* h_stats = nullptr;
+  // stats: pinned chunks of kStatsChunk iterations x 3, never moved or freed
+  // while iterations run (cudaFreeHost would synchronize the device)
+  static constexpr int kStatsChunk = 1024;
+  std::vector<uint64_t*> h_stats;
   DevBuf<uint64_t> d_stats;  // ring of 3 x 4
-  size_t stats_cap = 0;
   int stats_n = 0;
+  uint64_t* stat_row(int i) { return h_stats[i / kStatsChunk] + 3 * (i % kStatsChunk); }
   ScanScratch scan;
 
   ReqBatch& R(int i) { return rq[((i % 3) + 3) % 3]; }
@@ -231,6 +279,8 @@ struct Engine {
   }
 
   std::vector<uint64_t> fetch(const uint64_t* d, int n, cudaStream_t s) {
+    if (debug)
+      std::fprintf(stderr, "[fsx r%d] fetch on %s\n", me, s == lo ? "L" : s == hi ? "H" : "C");
     std::vector<uint64_t> h(n);
     FSX_CUDA(cudaMemcpyAsync(h.data(), d, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost, s));
     FSX_CUDA(cudaStreamSynchronize(s));
@@ -243,21 +293,37 @@ struct Engine {
   void a2a(int ch, int par, const std::vector<uint64_t>& bytes, cudaStream_t s) {
     if (p == 1) return;
     const uint32_t v = seq[ch];
+    if (debug)
+      std::fprintf(stderr, "[fsx r%d] a2a ch=%d seq=%u par=%d stream=%s\n", me, ch, v, par,
+                   s == lo ? "L" : s == hi ? "H" : "C");
     for (int k = 1; k < p; ++k) {
       const int d = (me + k) % p;  // stagger destinations across the NVSwitch
       const PeerView& pv = peer[d];
       if (!pv.base) raise(FSX_ERR_COLLECTIVE, "all_to_all: peer " + std::to_string(d) + " not connected");
       char* dst = pv.base + ch_off[ch] + (static_cast<size_t>(par) * p + me) * ch_slot[ch];
       if (bytes[d]) FSX_CUDA(cudaMemcpyAsync(dst, stage_slot(ch, par, d), bytes[d], cudaMemcpyDefault, s));
-      FSX_CU(cuStreamWriteValue32(reinterpret_cast<CUstream>(s),
-                                  reinterpret_cast<CUdeviceptr>(pv.flags + ch * kMaxRanks + me), v,
-                                  CU_STREAM_WRITE_VALUE_DEFAULT));
+      if (pv.local) {
+        cudaEvent_t ev;
+        FSX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        FSX_CUDA(cudaEventRecord(ev, s));
+        Hub::get().post(pv.local, ch, v, me, ev);
+      } else {
+        FSX_CU(cuStreamWriteValue32(reinterpret_cast<CUstream>(s),
+                                    reinterpret_cast<CUdeviceptr>(pv.flags + ch * kMaxRanks + me), v,
+                                    CU_STREAM_WRITE_VALUE_DEFAULT));
+      }
     }
     for (int k = 1; k < p; ++k) {
       const int src = (me + p - k) % p;
-      FSX_CU(cuStreamWaitValue32(reinterpret_cast<CUstream>(s),
-                                 reinterpret_cast<CUdeviceptr>(flags + ch * kMaxRanks + src), v,
-                                 CU_STREAM_WAIT_VALUE_GEQ));
+      if (peer[src].local) {
+        cudaEvent_t ev = Hub::get().take(this, ch, v, src);
+        FSX_CUDA(cudaStreamWaitEvent(s, ev, 0));
+        FSX_CUDA(cudaEventDestroy(ev));
+      } else {
+        FSX_CU(cuStreamWaitValue32(reinterpret_cast<CUstream>(s),
+                                   reinterpret_cast<CUdeviceptr>(flags + ch * kMaxRanks + src), v,
+                                   CU_STREAM_WAIT_VALUE_GEQ));
+      }
     }
   }
 
@@ -637,24 +703,17 @@ struct Engine {
 
   // ---- stats (IterationStats, embedding.hpp:119-124) ----------------------------
   void stats_reserve(int n) {
-    if (static_cast<size_t>(n) <= stats_cap) return;
-    size_t nc = std::max<size_t>(1024, stats_cap * 2);
-    while (nc < static_cast<size_t>(n)) nc *= 2;
-    uint64_t* h = nullptr;
-    FSX_CUDA(cudaDeviceSynchronize());
-    FSX_CUDA(cudaMallocHost(&h, nc * 3 * 8));
-    std::memset(h, 0, nc * 3 * 8);
-    if (h_stats) {
-      std::memcpy(h, h_stats, stats_cap * 3 * 8);
-      cudaFreeHost(h_stats);
+    while (static_cast<int>(h_stats.size()) * kStatsChunk < n) {
+      uint64_t* h = nullptr;
+      FSX_CUDA(cudaHostAlloc(&h, kStatsChunk * 3 * 8, cudaHostAllocDefault));
+      std::memset(h, 0, kStatsChunk * 3 * 8);
+      h_stats.push_back(h);
     }
-    h_stats = h;
-    stats_cap = nc;
   }
   void stats_forward(int i, bool with_next) {
     stats_reserve(i + 1);
     stats_n = i + 1;
-    uint64_t* dst = h_stats + 3 * static_cast<size_t>(i);
+    uint64_t* dst = stat_row(i);
     dst[0] = dst[1] = dst[2] = 0;
     if (with_next) {
       FSX_CUDA(cudaMemcpyAsync(dst, O(i).misc.p, 8, cudaMemcpyDeviceToHost, lo));
@@ -669,7 +728,7 @@ struct Engine {
     if (cor_par >= 0) cor = recv_slots(CH_COR, cor_par);
     FSX_LAUNCH(ctx, k_blocking_bytes, 1, 32, 0, s, p, 8ull * t->g.dim, rc.split_tot.p, oc.occ_tot(),
                on.pack_tot(), cor, have_grads ? 1 : 0, have_eco ? 1 : 0, d);
-    FSX_CUDA(cudaMemcpyAsync(h_stats + 3 * static_cast<size_t>(i) + 2, d, 8, cudaMemcpyDeviceToHost, s));
+    FSX_CUDA(cudaMemcpyAsync(stat_row(i) + 2, d, 8, cudaMemcpyDeviceToHost, s));
   }
 
   ~Engine() {
@@ -681,7 +740,7 @@ struct Engine {
     if (lo) cudaStreamDestroy(lo);
     if (hi) cudaStreamDestroy(hi);
     if (win) cudaFree(win);
-    if (h_stats) cudaFreeHost(h_stats);
+    for (auto* h : h_stats) cudaFreeHost(h);
   }
 };
 
@@ -755,10 +814,16 @@ int fsx_engine_create(fsx_ctx* ctx, fsx_table* table, const fsx_engine_config* c
   FSX_CUDA(cudaStreamCreateWithPriority(&e->lo, cudaStreamNonBlocking, lo_prio));
   FSX_CUDA(cudaStreamCreateWithPriority(&e->hi, cudaStreamNonBlocking, hi_prio));
   e->d_stats.alloc(16);
+  const uint64_t m = static_cast<uint64_t>(e->p) * cap;
   for (int k = 0; k < 3; ++k) {
     e->rq[k].reserve(cap);
-    e->ow[k].reserve(static_cast<uint64_t>(e->p) * cap);
+    e->rq[k].scan.ensure(cap, 16);
+    e->rq[k].srt.reserve64();
+    e->ow[k].reserve(m);
+    e->ow[k].scan.ensure(m, 16);
   }
+  for (auto& s : e->sgd) s.reserve(m, m, table->g.dim, cfg->reduce_chunk);
+  e->stats_reserve(4 * Engine::kStatsChunk);
   FSX_CUDA(cudaDeviceSynchronize());
   *out = e.release();
   FSX_API_END
@@ -785,6 +850,7 @@ int fsx_engine_connect_local(fsx_engine* e, int peer, fsx_engine* other) {
   e->peer[peer].base = other->win;
   e->peer[peer].flags = other->flags;
   e->peer[peer].ipc = false;
+  e->peer[peer].local = other;
   FSX_API_END
 }
 
@@ -871,7 +937,7 @@ int fsx_engine_stats(fsx_engine* e, int iter, uint64_t* out3) {
   DeviceGuard dg(e->ctx->device);
   if (iter < 0 || iter >= e->stats_n) raise(FSX_ERR_OUT_OF_RANGE, "fsx: no stats for iteration " + std::to_string(iter));
   FSX_CUDA(cudaDeviceSynchronize());
-  std::memcpy(out3, e->h_stats + 3 * static_cast<size_t>(iter), 24);
+  std::memcpy(out3, e->stat_row(iter), 24);
   FSX_API_END
 }
 

@@ -197,6 +197,7 @@ int fsx_sort_unique_u64(fsx_ctx* ctx, const uint64_t* d_keys, uint64_t n, uint64
   }
   SortedIds srt;
   srt.reserve(n);
+  srt.reserve64();
   FSX_CUDA(cudaMemcpyAsync(srt.d_n(), &n, 8, cudaMemcpyHostToDevice, s));
   ShardGeom g{~0ull, 0, 1, 1, 0};
   srt.run(ctx, d_keys, n, g, false, false, bits_for(h[0]), s);

@@ -50,6 +50,14 @@ struct SortedIds {
     k64a.release(); k64b.release();
     uniq.alloc(cap); uniq_g.alloc(cap); seg_start.alloc(cap + 1); inverse.alloc(cap);
     if (!d_counts.p) d_counts.alloc(4);
+    // every scratch buffer is sized up front: a lazy cudaMalloc/cudaFree in
+    // the middle of a multi-rank iteration can serialize the device
+    radix.counts.ensure(static_cast<size_t>(ceil_div(cap, kRadixTile)) * 256);
+    scan.ensure(cap, 1);
+  }
+  void reserve64() {
+    k64a.ensure(cap);
+    k64b.ensure(cap);
   }
   uint64_t* d_n() { return d_counts.p; }
   uint64_t* d_u() { return d_counts.p + 1; }
@@ -71,7 +79,7 @@ struct SortedIds {
                             local ? (uint64_t)g.shard : 0ull, seg_start.p, inverse.p};
       run_scan(ctx, op, n_cap, d_n(), scan, totals, s);
     } else {
-      k64a.ensure(cap); k64b.ensure(cap);
+      if (k64a.n < cap || k64b.n < cap) raise(FSX_ERR_CONFIG, "fsx: 64-bit sort keys need reserve64()");
       FSX_LAUNCH(ctx, k_make_keys<uint64_t>, grid, 256, 0, s, ids, n_cap, d_n(), g, local ? 1 : 0,
                  validate ? 1 : 0, k64a.p, ctx->d_err);
       uint64_t* ko;

@@ -3,6 +3,14 @@ import sys
 
 import pytest
 
+# Stream memory-op waits (the copy-engine transport's cross-rank flags) must not
+# share a hardware queue with the writes they wait for; give every stream its
+# own connection. Must be set before the CUDA context exists.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# Lazy module loading can block a host thread on the first launch of a kernel
+# while another stream waits on a peer flag: load everything eagerly.
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))

@@ -83,18 +83,29 @@ def test_sync_single_rank_dense(drv, oracle):
 
 @pytest.mark.parametrize("world", [1, 2, 4])
 def test_fp32_zipf_within_tolerance(drv, oracle, world):
-    """config-1-like Zipf traffic on fp32 tables, chunked deterministic reduce."""
+    """config-1-like Zipf traffic on fp32 tables.
+    * reduce_chunk=0 (reference accumulation order): bit-exact with the oracle
+      run on an fp32 table (store_f32: values rounded to float on store, the
+      gradient fixture evaluated in float as the torch op does) — the kernels
+      add no error beyond the storage rounding itself;
+    * reduce_chunk=64 (parallel hot rows): both engine modes agree bit for bit
+      and stay within 1e-6 normwise (max|a-b| / max|b|) of the f64 reference.
+      (A per-element floored 1e-6 vs f64 is not a property of fp32 storage:
+      the init rounding alone is ~4e-9 absolute, 4e-6 of the 1e-3 floor.)"""
     from paper_2604_24073_b200 import workload
     from paper_2604_24073_b200.embedding import TableGeometry
     rows, dim, iters = 50_000, 64, 4
     batches = [[workload.zipf_batch(100 + r, 3000, rows, offset=3000 * i) for r in range(world)]
                for i in range(iters)]
-    want, _ = oracle.run_engine(world, batches, rows, dim, 0.05, 3)
     geom = TableGeometry(rows, dim, world)
+    exact, _ = drv.run_engine(True, batches, geom, 0.05, 3, dtype="f32", reduce_chunk=0)
+    want32, _ = oracle.run_engine(world, batches, rows, dim, 0.05, 3, store_f32=True)
+    assert np.array_equal(_bits(exact), _bits(want32))
     got_p, _ = drv.run_engine(True, batches, geom, 0.05, 3, dtype="f32", reduce_chunk=64)
     got_s, _ = drv.run_engine(False, batches, geom, 0.05, 3, dtype="f32", reduce_chunk=64)
-    assert np.array_equal(_bits(got_p), _bits(got_s))  # both modes share one reduce order
-    assert frel(got_p, want) < 1e-6
+    assert np.array_equal(_bits(got_p), _bits(got_s))
+    want, _ = oracle.run_engine(world, batches, rows, dim, 0.05, 3)
+    assert float(np.max(np.abs(got_p - want)) / np.max(np.abs(want))) < 1e-6
 
 
 def test_f64_chunked_reduce_close(drv, oracle):
