@@ -178,6 +178,27 @@ int fsx_engine_stats(fsx_engine* e, int iter, uint64_t* out3);
  * on embedding traffic (event pairs around each wait), synchronizes */
 int fsx_engine_exposed_ms(fsx_engine* e, double* ms);
 
+/* Live per-phase device timing (CUDA event pairs on the stream each phase
+ * runs on). Off by default; when on, every phase launch is bracketed. */
+#define FSX_PHASE_MERGE 0     /* C: resolve + batch-major merge (K6)            */
+#define FSX_PHASE_SPLIT 1     /* C: gradient split / pack (K7)                  */
+#define FSX_PHASE_CO_UPDATE 2 /* H: collision-row SGD (K8)                       */
+#define FSX_PHASE_EX_UPDATE 3 /* L: deferred exclusive-row SGD (K8)             */
+#define FSX_PHASE_PREFETCH 4  /* L: exclusive prefetch pack (K5)                */
+#define FSX_PHASE_ECO 5       /* H: E_co pack (K9)                              */
+#define FSX_PHASE_ROUTE 6     /* requester route + per-owner dedup (K1 K2 K4)   */
+#define FSX_PHASE_DEDUP 7     /* owner flatten + sort/unique + src bits (K1 K2) */
+#define FSX_PHASE_COLLIDE 8   /* collision flags + pack plans (K3)              */
+#define FSX_PHASE_MASKS 9     /* masks + split / occurrence ranks (K10)         */
+#define FSX_PHASE_SERVE 10    /* C: blocking per-occurrence lookup + scatter    */
+#define FSX_PHASE_UPDATE 11   /* C: blocking full update                        */
+#define FSX_PHASE_A2A 12      /* copy-engine transfers (any lane)               */
+#define FSX_NUM_PHASES 13
+int fsx_engine_set_profiling(fsx_engine* e, int on);
+/* total ms and number of spans of `phase` since the last call for that
+ * phase (synchronizes; resets the phase) */
+int fsx_engine_phase_ms(fsx_engine* e, int phase, double* total_ms, uint64_t* spans);
+
 /* ---- load balancer (partition.cpp, sim.hpp) -------------------------------- */
 
 /* K12: CostModel::compute_time_for_lengths (sim.hpp:24-35) for each of

@@ -19,6 +19,8 @@ CSRC = os.path.join(HERE, "csrc")
 FSX_F32, FSX_F64 = 0, 1
 FSX_MODE_SYNC, FSX_MODE_PRIO = 0, 1
 FSX_TRANSPORT_CE, FSX_TRANSPORT_NCCL = 0, 1
+PHASES = ["merge", "split", "co_update", "ex_update", "prefetch", "eco", "route", "dedup",
+          "collide", "masks", "serve", "update", "a2a"]
 
 _lock = threading.Lock()
 _lib = None
@@ -67,6 +69,8 @@ _SIGS = {
     "fsx_engine_finalize": ([vp, vp], i32),
     "fsx_engine_stats": ([vp, i32, P(u64)], i32),
     "fsx_engine_exposed_ms": ([vp, P(dbl)], i32),
+    "fsx_engine_set_profiling": ([vp, i32], i32),
+    "fsx_engine_phase_ms": ([vp, i32, P(dbl), P(u64)], i32),
     "fsx_cost_estimate": ([vp, vp, vp, i32, dbl, dbl, dbl, vp, vp], i32),
     "fsx_fbs_partition": ([vp, vp, vp, vp, u64, i32, vp, vp, vp], i32),
     "fsx_vbs_partition": ([vp, vp, vp, vp, u64, i32, dbl, vp, vp, vp, vp, vp], i32),

@@ -205,6 +205,38 @@ struct Engine {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> waits;
   std::vector<cudaEvent_t> timing_pool;
   size_t timing_next = 0;
+  // live phase timing (fsx_engine_set_profiling)
+  bool prof = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spans[FSX_NUM_PHASES];
+  std::vector<cudaEvent_t> prof_pool;
+  size_t prof_next = 0;
+  cudaEvent_t prof_event() {
+    if (prof_next == prof_pool.size()) {
+      cudaEvent_t e;
+      FSX_CUDA(cudaEventCreate(&e));
+      prof_pool.push_back(e);
+    }
+    return prof_pool[prof_next++];
+  }
+  struct Span {
+    Engine* e;
+    int phase;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr;
+    Span(Engine* eng, int ph, cudaStream_t st) : e(eng), phase(ph), s(st) {
+      if (e->prof) {
+        a = e->prof_event();
+        FSX_CUDA(cudaEventRecord(a, s));
+      }
+    }
+    ~Span() {
+      if (a) {
+        cudaEvent_t b = e->prof_event();
+        cudaEventRecord(b, s);
+        e->spans[phase].emplace_back(a, b);
+      }
+    }
+  };
   // protocol state
   ReqBatch rq[3];
   OwnBatch ow[3];
@@ -296,6 +328,7 @@ struct Engine {
     if (debug)
       std::fprintf(stderr, "[fsx r%d] a2a ch=%d seq=%u par=%d stream=%s\n", me, ch, v, par,
                    s == lo ? "L" : s == hi ? "H" : "C");
+    Span sp(this, FSX_PHASE_A2A, s);
     for (int k = 1; k < p; ++k) {
       const int d = (me + k) % p;  // stagger destinations across the NVSwitch
       const PeerView& pv = peer[d];
@@ -331,6 +364,7 @@ struct Engine {
 
   // ---- requester: route a batch (embedding.cpp:185-212) ----------------------
   int route(ReqBatch& r, const uint64_t* d_ids, uint64_t n, cudaStream_t s) {
+    Span sp(this, FSX_PHASE_ROUTE, s);
     if (n > cap) raise(FSX_ERR_INVALID_ARGUMENT, "embedding: batch of " + std::to_string(n) +
                                                     " ids exceeds engine capacity " + std::to_string(cap));
     r.reserve(cap);
@@ -372,6 +406,7 @@ struct Engine {
 
   // ---- owner: receive + dedup (embedding.cpp:214-229) -------------------------
   void receive(OwnBatch& o, int ids_par, cudaStream_t s) {
+    Span sp(this, FSX_PHASE_DEDUP, s);
     o.reserve(static_cast<uint64_t>(p) * cap);
     o.has_co = false;
     CSlots slots = recv_slots(CH_IDS, ids_par);
@@ -388,7 +423,8 @@ struct Engine {
 
   // full-row deterministic update of an owner batch from a grads channel
   void update(OwnBatch& o, int ch, int par, const uint8_t* select, uint8_t want, bool by_rank,
-              cudaStream_t s) {
+              cudaStream_t s, int phase = FSX_PHASE_UPDATE) {
+    Span sp(this, phase, s);
     RowSegments rs{o.srt.uniq.p, o.srt.seg_start.p, o.srt.perm, o.srt.d_u(), select, want};
     const uint64_t m = o.m_cap;
     if (t->dtype == FSX_F32) {
@@ -406,6 +442,7 @@ struct Engine {
   // ---- sync building blocks ---------------------------------------------------------
   // owner lookup per occurrence -> ROWS -> requester scatter (embedding.cpp:244-264)
   void serve_blocking(ReqBatch& r, OwnBatch& o, void* d_out, cudaStream_t s) {
+    Span sp(this, FSX_PHASE_SERVE, s);
     const int par = next_par(CH_ROWS);
     Slots send = send_slots(CH_ROWS, par);
     OwnerLookupMap lm{static_cast<const char*>(t->values), o.ids.p, o.occ_src.p, o.occ_idx.p, send, rb, p};
@@ -423,6 +460,7 @@ struct Engine {
 
   // requester grads -> GRADS -> owner full update (embedding.cpp:276-295)
   void update_blocking(ReqBatch& r, OwnBatch& o, const void* d_grads, cudaStream_t s) {
+    Span sp(this, FSX_PHASE_UPDATE, s);
     const int par = next_par(CH_GRADS);
     Slots send = send_slots(CH_GRADS, par);
     GradPackMap gm{static_cast<const char*>(d_grads), r.send_pos.p, r.send_dst.p, r.send_off(),
@@ -441,6 +479,7 @@ struct Engine {
   // collision of (cur, next) owner batches + pack lists + EX prefetch of next
   // (embedding.cpp:360-390)
   void collide_and_prefetch(OwnBatch& oc, OwnBatch& on, ReqBatch& rn, cudaStream_t s) {
+    Span sp(this, FSX_PHASE_COLLIDE, s);
     FSX_CUDA(cudaMemsetAsync(on.co.p, 0, on.m_cap, s));
     FSX_CUDA(cudaMemsetAsync(oc.misc.p, 0, 8, s));
     FSX_LAUNCH(ctx, k_intersect_flags, grid_for(ctx, oc.m_cap, 256, 8), 256, 0, s, oc.srt.uniq_g.p,
@@ -464,7 +503,10 @@ struct Engine {
     IdRowPackMap pm{static_cast<const char*>(t->values), on.srt.uniq.p, on.srt.uniq_g.p, on.ex_list.p,
                     send, on.pack_tot(), 0, rb};
     FSX_LAUNCH(ctx, k_sum_pairs, 1, 32, 0, s, on.pack_tot(), p, on.misc.p + 2);
-    launch_copy_rows(ctx, pm, on.m_cap * static_cast<uint64_t>(p), on.misc.p + 2, rb, s);
+    {
+      Span sp2(this, FSX_PHASE_PREFETCH, s);
+      launch_copy_rows(ctx, pm, on.m_cap * static_cast<uint64_t>(p), on.misc.p + 2, rb, s);
+    }
     if (p > 1) {
       on.h_pack = fetch(on.pack_tot(), 2 * p, s);
       std::vector<uint64_t> bytes(p);
@@ -476,6 +518,7 @@ struct Engine {
   // MASK messages for the current batch + requester flags + split plan
   // (embedding.cpp:392-408, 524-536)
   void masks_and_split(OwnBatch& oc, ReqBatch& rc, bool with_co, cudaStream_t s) {
+    Span sp(this, FSX_PHASE_MASKS, s);
     const int par = next_par(CH_MASK);
     Slots send = send_slots(CH_MASK, par);
     FSX_CUDA(cudaMemsetAsync(oc.mask_tot(), 0, 16 * 8, s));
@@ -519,6 +562,7 @@ struct Engine {
 
   // requester: split grads into CO_G / EX_G messages (embedding.cpp:526-536)
   void split_grads(ReqBatch& r, const void* d_grads, int cog_par, int exg_par, cudaStream_t s) {
+    Span sp(this, FSX_PHASE_SPLIT, s);
     Slots co = send_slots(CH_COG, cog_par), ex = send_slots(CH_EXG, exg_par);
     GradPackMap gm{static_cast<const char*>(d_grads), r.send_pos.p, r.send_dst.p, r.send_off(),
                    r.srt.inverse.p, r.flag.p, r.split_rank.p, co, ex, rb};
@@ -529,6 +573,7 @@ struct Engine {
 
   // owner: E_co rows of the next batch (embedding.cpp:560-590)
   int send_eco(OwnBatch& on, cudaStream_t s) {
+    Span sp(this, FSX_PHASE_ECO, s);
     const int par = next_par(CH_COR);
     Slots send = send_slots(CH_COR, par);
     FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, on.pack_tot() + 1, 2, cap, ctx->d_err);
@@ -545,6 +590,7 @@ struct Engine {
 
   // requester: merge E_ex / E_co into batch-major rows (embedding.cpp:453-484)
   void merge(ReqBatch& r, void* d_out, cudaStream_t s) {
+    Span sp(this, FSX_PHASE_MERGE, s);
     CSlots ex = recv_slots(CH_EX, r.ex_par);
     CSlots co{};
     if (r.cor_par >= 0) co = recv_slots(CH_COR, r.cor_par);
@@ -597,6 +643,9 @@ struct Engine {
       apply_deferred();
     }
     // ---- side lane L: prepare iteration i+1 (embedding.cpp:355-420) ----
+    // everything the caller enqueued on C so far (e.g. the H2D of ids_next)
+    // happens-before the side lane reads it
+    wait(lo, record(c));
     wait(lo, ev_cur);
     wait(lo, ev_merged);  // slots of the parity reused below were read by the last merge
     if (ids_next) {
@@ -642,7 +691,7 @@ struct Engine {
       for (int d = 0; d < p; ++d) bytes[d] = kHdr + rb * rp.h_split[2 * d];
       a2a(CH_EXG, exg_par, bytes, lo);
     }
-    update(op, CH_EXG, exg_par, op.has_co ? op.co.p : nullptr, 0, true, lo);
+    update(op, CH_EXG, exg_par, op.has_co ? op.co.p : nullptr, 0, true, lo, FSX_PHASE_EX_UPDATE);
     has_pending = false;
   }
 
@@ -674,7 +723,7 @@ struct Engine {
           for (int d = 0; d < p; ++d) bytes[d] = kHdr + rb * rc.h_split[2 * d + 1];
           a2a(CH_COG, cog, bytes, hi);
         }
-        update(oc, CH_COG, cog, oc.co.p, 1, true, hi);
+        update(oc, CH_COG, cog, oc.co.p, 1, true, hi, FSX_PHASE_CO_UPDATE);
         have_grads = true;
       }
     }
@@ -737,6 +786,7 @@ struct Engine {
       if (peer[d].ipc && peer[d].base) cudaIpcCloseMemHandle(peer[d].base);
     for (auto e : ev_pool) cudaEventDestroy(e);
     for (auto e : timing_pool) cudaEventDestroy(e);
+    for (auto e : prof_pool) cudaEventDestroy(e);
     if (lo) cudaStreamDestroy(lo);
     if (hi) cudaStreamDestroy(hi);
     if (win) cudaFree(win);
@@ -952,6 +1002,32 @@ int fsx_engine_exposed_ms(fsx_engine* e, double* ms) {
     total += x;
   }
   *ms = total;
+  FSX_API_END
+}
+
+int fsx_engine_set_profiling(fsx_engine* e, int on) {
+  FSX_API_BEGIN
+  e->prof = on != 0;
+  FSX_API_END
+}
+
+int fsx_engine_phase_ms(fsx_engine* e, int phase, double* total_ms, uint64_t* count) {
+  FSX_API_BEGIN
+  DeviceGuard dg(e->ctx->device);
+  if (phase < 0 || phase >= FSX_NUM_PHASES) raise(FSX_ERR_OUT_OF_RANGE, "fsx: bad phase");
+  double t = 0;
+  for (auto& sp : e->spans[phase]) {
+    FSX_CUDA(cudaEventSynchronize(sp.second));
+    float x = 0;
+    FSX_CUDA(cudaEventElapsedTime(&x, sp.first, sp.second));
+    t += x;
+  }
+  *total_ms = t;
+  *count = e->spans[phase].size();
+  e->spans[phase].clear();
+  bool any = false;
+  for (auto& v : e->spans) any = any || !v.empty();
+  if (!any) e->prof_next = 0;  // recycle the event pool once every phase was read
   FSX_API_END
 }
 

@@ -283,7 +283,7 @@ struct RowSegments {
 // Work list: every selected row contributes ceil(len / chunk) items (1 when
 // chunk == 0); multi-chunk rows are also listed for the combine pass.
 struct SgdPlanOp {
-  static constexpr int NC = 2;
+  static constexpr int NC = 3;
   RowSegments rs;
   uint32_t chunk;
   uint2* work;          // (row, chunk index)
@@ -295,16 +295,18 @@ struct SgdPlanOp {
     if (chunk == 0 || len <= chunk) return 1;
     return (len + chunk - 1) / chunk;
   }
-  __device__ void count(uint64_t u, uint32_t (&c)[2]) const {
+  // c0: work items, c1: multi-chunk rows, c2: partial slots (multi rows only)
+  __device__ void count(uint64_t u, uint32_t (&c)[3]) const {
     const uint32_t k = nchunks(u);
     c[0] = k;
     c[1] = k > 1 ? 1u : 0u;
+    c[2] = k > 1 ? k : 0u;
   }
-  __device__ void emit(uint64_t u, const uint32_t (&ex)[2], const uint32_t (&c)[2]) const {
+  __device__ void emit(uint64_t u, const uint32_t (&ex)[3], const uint32_t (&c)[3]) const {
     for (uint32_t q = 0; q < c[0]; ++q) work[ex[0] + q] = make_uint2(static_cast<uint32_t>(u), q);
     if (c[1]) {
       multi[ex[1]] = static_cast<uint32_t>(u);
-      part_base[u] = ex[0];
+      part_base[u] = ex[2];
     }
   }
 };
@@ -391,7 +393,7 @@ __global__ void __launch_bounds__(256) k_sgd_chunks(SgdArgs<T> a) {
         if (single) {
           sgd_apply(a, u, d, acc[c]);
         } else {
-          a.partials[w * dim + d] = acc[c];
+          a.partials[(static_cast<uint64_t>(a.part_base[u]) + item.y) * dim + d] = acc[c];
         }
       }
     }

@@ -10,7 +10,7 @@ struct SgdScratch {
   DevBuf<uint2> work;
   DevBuf<uint32_t> multi, part_base;
   DevBuf<double> partials;
-  DevBuf<uint64_t> d_tot;  // [0] work items, [1] multi rows
+  DevBuf<uint64_t> d_tot;  // [0] work items, [1] multi rows, [2] partial slots
   ScanScratch scan;
   uint64_t cap_rows = 0, cap_work = 0;
   uint32_t dim = 0;
@@ -21,9 +21,11 @@ struct SgdScratch {
       cap_work = w > cap_work ? w : cap_work;
       dim = d;
       work.alloc(cap_work); multi.alloc(cap_rows); part_base.alloc(cap_rows);
-      partials.alloc(chunk ? cap_work * d : 1);
+      // a row with k > 1 chunks has > (k-1)*chunk occurrences: slots <= 2*occ/chunk
+      partials.alloc(chunk ? (2 * occ / chunk + 1) * d : 1);
     }
-    if (!d_tot.p) d_tot.alloc(2);
+    if (!d_tot.p) d_tot.alloc(4);
+    scan.ensure(rows, 3);
   }
 };
 

@@ -309,6 +309,18 @@ class _Engine:
     def _ids(self, ids) -> torch.Tensor:
         return _dev_u64(ids, self.shard.ctx.torch_device)
 
+    def set_profiling(self, on: bool = True) -> None:
+        _lib.call("fsx_engine_set_profiling", self.h, int(on))
+
+    def phase_ms(self) -> dict:
+        """{phase: (total ms, spans)} since the last call (synchronizes)."""
+        out = {}
+        for k, name in enumerate(_lib.PHASES):
+            t, n = C.c_double(), C.c_uint64()
+            _lib.call("fsx_engine_phase_ms", self.h, k, C.byref(t), C.byref(n))
+            out[name] = (t.value, n.value)
+        return out
+
     def exposed_ms(self) -> float:
         v = C.c_double()
         _lib.call("fsx_engine_exposed_ms", self.h, C.byref(v))
