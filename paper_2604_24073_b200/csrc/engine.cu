@@ -31,7 +31,7 @@
 
 namespace fsx {
 
-enum Channel : int { CH_IDS, CH_ROWS, CH_GRADS, CH_EX, CH_MASK, CH_COG, CH_EXG, CH_COR, NCH };
+enum Channel : int { CH_IDS, CH_ROWS, CH_GRADS, CH_EX, CH_MASK, CH_COG, CH_EXG, CH_COR, CH_IDX, NCH };
 
 namespace {
 
@@ -90,23 +90,19 @@ __global__ void k_blocking_bytes(int p, uint64_t rb8, const uint64_t* split_tot,
 // ---- per-batch state -----------------------------------------------------------
 struct ReqBatch {  // requester view of one iteration's ids
   uint64_t n = 0;
-  DevBuf<uint64_t> ids, keys, uq_g;
-  DevBuf<uint32_t> send_pos, uq_off, split_rank;
-  DevBuf<uint8_t> send_dst, flag;
+  DevBuf<uint64_t> ids;
+  DevBuf<uint32_t> send_pos, split_rank;
+  DevBuf<uint8_t> send_dst, flag;  // flag: collision flag per grouped occurrence
   DevBuf<uint64_t> tot;        // [0..16) send counts, [16..33) send_off
   DevBuf<uint64_t> split_tot;  // [32]
-  DevBuf<const char*> rowptr;
-  SortedIds srt;               // over composite (owner, local) keys
   ScanScratch scan;
   std::vector<uint64_t> h_send, h_split;
   bool has_flags = false;
-  int ex_par = -1, cor_par = -1;  // channel parities holding E_ex / E_co of this batch
+  int ex_par = -1, cor_par = -1, idx_par = -1;  // channel parities of E_ex / E_co / IDX
   void reserve(uint64_t cap) {
     if (ids.n >= cap && ids.p) return;
-    ids.alloc(cap); keys.alloc(cap); uq_g.alloc(cap); send_pos.alloc(cap); uq_off.alloc(kMaxRanks + 1);
-    split_rank.alloc(cap); send_dst.alloc(cap); flag.alloc(cap); tot.alloc(48); split_tot.alloc(32);
-    rowptr.alloc(cap);
-    srt.reserve(cap);
+    ids.alloc(cap); send_pos.alloc(cap); split_rank.alloc(cap); send_dst.alloc(cap); flag.alloc(cap);
+    tot.alloc(48); split_tot.alloc(32);
   }
   const uint64_t* send_off() const { return tot.p + 16; }
 };
@@ -118,6 +114,7 @@ struct OwnBatch {  // owner view: occurrences received for this shard
   DevBuf<uint64_t> cnt;  // k_recv_prefix layout: [0]=M, [2+s]=n_s, [2+16+s]=off_s
   DevBuf<uint64_t> misc; // [0] co count, [8..40) pack totals (2p), [40..72) occ totals, [72..88) mask totals
   DevBuf<PackEntry> ex_list, co_list;
+  DevBuf<uint32_t> rank_us;  // [unique row][kMaxRanks] position in each source's message
   SortedIds srt;
   ScanScratch scan;
   std::vector<uint64_t> h_recv, h_pack, h_mask;
@@ -129,6 +126,7 @@ struct OwnBatch {  // owner view: occurrences received for this shard
     ids.alloc(cap); occ_src.alloc(cap); co.alloc(cap); occ_idx.alloc(cap); occ_rank.alloc(cap);
     bits.alloc(cap); cnt.alloc(2 + 2 * kMaxRanks + 8); misc.alloc(96); ex_list.alloc(cap);
     co_list.alloc(cap);
+    rank_us.alloc(cap * kMaxRanks);
     srt.reserve(cap);
   }
   uint64_t* pack_tot() { return misc.p + 8; }
@@ -198,7 +196,7 @@ struct Engine {
   DevBuf<char> stage;         // send staging, same layout as the channel region of win
   PeerView peer[kMaxRanks];
   uint32_t seq[NCH] = {};
-  cudaStream_t lo = nullptr, hi = nullptr;
+  cudaStream_t lo = nullptr, hi = nullptr, ux = nullptr;  // ux: deferred exclusive updates
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_next = 0;
   // exposed-wait timing on the compute stream
@@ -383,18 +381,6 @@ struct Engine {
     }
     FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, r.tot.p, 1, cap, ctx->d_err);
     FSX_LAUNCH(ctx, k_prefix, 1, 32, 0, s, r.tot.p, p, 1, r.tot.p + 16);
-    // per-owner sorted unique lists (unique_per_shard, embedding.cpp:205-208)
-    const int lbits = bits_for(t->g.total_rows / static_cast<uint64_t>(p) + 1);
-    if (n) {
-      FSX_LAUNCH(ctx, k_requester_keys, grid_for(ctx, n, 256, 8), 256, 0, s, r.ids.p, n, p, lbits, r.keys.p);
-      FSX_CUDA(cudaMemcpyAsync(r.srt.d_n(), &r.n, 8, cudaMemcpyHostToDevice, s));
-      ShardGeom g{~0ull, 0, 1, 1, 0};
-      r.srt.run(ctx, r.keys.p, n, g, false, false, lbits + bits_for(static_cast<uint64_t>(p - 1)), s);
-    } else {
-      FSX_CUDA(cudaMemsetAsync(r.srt.d_counts.p, 0, 32, s));
-    }
-    FSX_LAUNCH(ctx, k_requester_uq, grid_for(ctx, n, 256, 4), 256, 0, s, r.srt.uniq.p, r.srt.d_u(), p,
-               lbits, r.uq_g.p, r.uq_off.p);
     if (p > 1) {
       r.h_send = fetch(r.tot.p, p, s);
       std::vector<uint64_t> bytes(p);
@@ -430,14 +416,15 @@ struct Engine {
     if (t->dtype == FSX_F32) {
       GradRows<float> gr{recv_slot(ch, par, 0) + kHdr, ch_slot[ch], o.occ_src.p,
                          by_rank ? o.occ_rank.p : o.occ_idx.p, rb};
-      sgd_update_rows<float>(ctx, *t, rs, m, m, gr, cfg.reduce_chunk, sgd[s == hi ? 1 : 0], nullptr, s);
+      sgd_update_rows<float>(ctx, *t, rs, m, m, gr, cfg.reduce_chunk, sgd_for(s), nullptr, s);
     } else {
       GradRows<double> gr{recv_slot(ch, par, 0) + kHdr, ch_slot[ch], o.occ_src.p,
                           by_rank ? o.occ_rank.p : o.occ_idx.p, rb};
-      sgd_update_rows<double>(ctx, *t, rs, m, m, gr, cfg.reduce_chunk, sgd[s == hi ? 1 : 0], nullptr, s);
+      sgd_update_rows<double>(ctx, *t, rs, m, m, gr, cfg.reduce_chunk, sgd_for(s), nullptr, s);
     }
   }
-  SgdScratch sgd[2];
+  SgdScratch sgd[3];  // one per lane that updates: ux, hi, compute
+  SgdScratch& sgd_for(cudaStream_t s) { return sgd[s == ux ? 0 : s == hi ? 1 : 2]; }
 
   // ---- sync building blocks ---------------------------------------------------------
   // owner lookup per occurrence -> ROWS -> requester scatter (embedding.cpp:244-264)
@@ -464,7 +451,7 @@ struct Engine {
     const int par = next_par(CH_GRADS);
     Slots send = send_slots(CH_GRADS, par);
     GradPackMap gm{static_cast<const char*>(d_grads), r.send_pos.p, r.send_dst.p, r.send_off(),
-                   r.srt.inverse.p, nullptr, nullptr, send, send, rb};
+                   nullptr, nullptr, send, send, rb};
     launch_copy_rows(ctx, gm, r.n, nullptr, rb, s);
     FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, r.tot.p, 1, cap, ctx->d_err);
     if (p > 1) {
@@ -491,10 +478,10 @@ struct Engine {
     // pack lists over next's unique rows: ex -> E_ex now, co -> E_co later
     FSX_CUDA(cudaMemsetAsync(on.pack_tot(), 0, 32 * 8, s));
     if (nc2() == 8) {
-      OwnerPackOp<8> op{on.bits.p, on.co.p, p, on.pack_tot(), on.ex_list.p, on.co_list.p};
+      OwnerPackOp<8> op{on.bits.p, on.co.p, p, on.pack_tot(), on.ex_list.p, on.co_list.p, on.rank_us.p};
       run_scan(ctx, op, on.m_cap, on.srt.d_u(), on.scan, on.pack_tot(), s);
     } else {
-      OwnerPackOp<16> op{on.bits.p, on.co.p, p, on.pack_tot(), on.ex_list.p, on.co_list.p};
+      OwnerPackOp<16> op{on.bits.p, on.co.p, p, on.pack_tot(), on.ex_list.p, on.co_list.p, on.rank_us.p};
       run_scan(ctx, op, on.m_cap, on.srt.d_u(), on.scan, on.pack_tot(), s);
     }
     const int par = next_par(CH_EX);
@@ -503,6 +490,7 @@ struct Engine {
     IdRowPackMap pm{static_cast<const char*>(t->values), on.srt.uniq.p, on.srt.uniq_g.p, on.ex_list.p,
                     send, on.pack_tot(), 0, rb};
     FSX_LAUNCH(ctx, k_sum_pairs, 1, 32, 0, s, on.pack_tot(), p, on.misc.p + 2);
+    wait(s, ev_ex_applied);  // rows of the previous exclusive set may be prefetched now
     {
       Span sp2(this, FSX_PHASE_PREFETCH, s);
       launch_copy_rows(ctx, pm, on.m_cap * static_cast<uint64_t>(p), on.misc.p + 2, rb, s);
@@ -514,38 +502,47 @@ struct Engine {
       a2a(CH_EX, par, bytes, s);
     }
     rn.ex_par = par;
+    // IDX: per-occurrence row positions for the next merge
+    const int ipar = next_par(CH_IDX);
+    Slots isend = send_slots(CH_IDX, ipar);
+    FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, isend, p, on.cnt.p + 2, 1, cap, ctx->d_err);
+    FSX_LAUNCH(ctx, k_idx_pack, grid_for(ctx, on.m_cap, 256, 8), 256, 0, s, on.srt.inverse.p, on.occ_src.p,
+               on.occ_idx.p, on.srt.d_n(), on.rank_us.p, on.co.p, isend);
+    if (p > 1) {
+      std::vector<uint64_t> bytes(p);
+      for (int d = 0; d < p; ++d) bytes[d] = kHdr + 4 * on.h_recv[d];
+      a2a(CH_IDX, ipar, bytes, s);
+    }
+    rn.idx_par = ipar;
   }
   // MASK messages for the current batch + requester flags + split plan
   // (embedding.cpp:392-408, 524-536)
   void masks_and_split(OwnBatch& oc, ReqBatch& rc, bool with_co, cudaStream_t s) {
     Span sp(this, FSX_PHASE_MASKS, s);
-    const int par = next_par(CH_MASK);
-    Slots send = send_slots(CH_MASK, par);
-    FSX_CUDA(cudaMemsetAsync(oc.mask_tot(), 0, 16 * 8, s));
-    if (p <= 8) {
-      MaskOp<8> op{oc.bits.p, with_co ? oc.co.p : nullptr, send};
-      run_scan(ctx, op, oc.m_cap, oc.srt.d_u(), oc.scan, oc.mask_tot(), s);
-    } else {
-      MaskOp<16> op{oc.bits.p, with_co ? oc.co.p : nullptr, send};
-      run_scan(ctx, op, oc.m_cap, oc.srt.d_u(), oc.scan, oc.mask_tot(), s);
+    if (with_co) {
+      const int par = next_par(CH_MASK);
+      Slots send = send_slots(CH_MASK, par);
+      FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, oc.cnt.p + 2, 1, cap, ctx->d_err);
+      FSX_LAUNCH(ctx, k_mask_pack, grid_for(ctx, oc.m_cap, 256, 8), 256, 0, s, oc.srt.inverse.p,
+                 oc.occ_src.p, oc.occ_idx.p, oc.srt.d_n(), oc.co.p, send);
+      if (p > 1) {
+        std::vector<uint64_t> bytes(p);
+        for (int d = 0; d < p; ++d) bytes[d] = kHdr + oc.h_recv[d];
+        a2a(CH_MASK, par, bytes, s);
+      }
+      if (rc.n)
+        FSX_LAUNCH(ctx, k_req_flags, grid_for(ctx, rc.n, 256, 8), 256, 0, s, recv_slots(CH_MASK, par),
+                   rc.send_dst.p, rc.send_off(), rc.n, rc.flag.p, ctx->d_err);
     }
-    FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, oc.mask_tot(), 1, cap, ctx->d_err);
-    if (p > 1) {
-      oc.h_mask = fetch(oc.mask_tot(), p, s);
-      std::vector<uint64_t> bytes(p);
-      for (int d = 0; d < p; ++d) bytes[d] = kHdr + oc.h_mask[d];
-      a2a(CH_MASK, par, bytes, s);
-    }
-    FSX_LAUNCH(ctx, k_requester_flags, grid_for(ctx, rc.n, 256, 4), 256, 0, s, recv_slots(CH_MASK, par),
-               rc.uq_off.p, p, rc.srt.d_u(), rc.flag.p, ctx->d_err);
-    rc.has_flags = true;
+    rc.has_flags = with_co;
+    const uint8_t* flag = with_co ? rc.flag.p : nullptr;
     // split plan (ranks of each occurrence in its (owner, flag) message)
     FSX_CUDA(cudaMemsetAsync(rc.split_tot.p, 0, 32 * 8, s));
     if (nc2() == 8) {
-      SplitOp<8> op{rc.send_pos.p, rc.send_dst.p, rc.srt.inverse.p, rc.flag.p, rc.split_rank.p};
+      SplitOp<8> op{rc.send_dst.p, flag, rc.split_rank.p};
       run_scan(ctx, op, rc.n, nullptr, rc.scan, rc.split_tot.p, s);
     } else {
-      SplitOp<16> op{rc.send_pos.p, rc.send_dst.p, rc.srt.inverse.p, rc.flag.p, rc.split_rank.p};
+      SplitOp<16> op{rc.send_dst.p, flag, rc.split_rank.p};
       run_scan(ctx, op, rc.n, nullptr, rc.scan, rc.split_tot.p, s);
     }
     // owner side: per-occurrence rank within (source, flag)
@@ -565,7 +562,7 @@ struct Engine {
     Span sp(this, FSX_PHASE_SPLIT, s);
     Slots co = send_slots(CH_COG, cog_par), ex = send_slots(CH_EXG, exg_par);
     GradPackMap gm{static_cast<const char*>(d_grads), r.send_pos.p, r.send_dst.p, r.send_off(),
-                   r.srt.inverse.p, r.flag.p, r.split_rank.p, co, ex, rb};
+                   r.has_flags ? r.flag.p : nullptr, r.split_rank.p, co, ex, rb};
     launch_copy_rows(ctx, gm, r.n, nullptr, rb, s);
     FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, co, p, r.split_tot.p + 1, 2, cap, ctx->d_err);
     FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, ex, p, r.split_tot.p, 2, cap, ctx->d_err);
@@ -591,15 +588,14 @@ struct Engine {
   // requester: merge E_ex / E_co into batch-major rows (embedding.cpp:453-484)
   void merge(ReqBatch& r, void* d_out, cudaStream_t s) {
     Span sp(this, FSX_PHASE_MERGE, s);
-    CSlots ex = recv_slots(CH_EX, r.ex_par);
     CSlots co{};
     if (r.cor_par >= 0) co = recv_slots(CH_COR, r.cor_par);
-    FSX_LAUNCH(ctx, k_resolve_rows, grid_for(ctx, r.n, 256, 8), 256, 0, s, ex, co, r.uq_g.p, r.uq_off.p,
-               p, r.srt.d_u(), rb, r.rowptr.p, ctx->d_err);
-    MergeMap mm{r.rowptr.p, r.srt.inverse.p, static_cast<char*>(d_out), rb};
+    else co = recv_slots(CH_EX, r.ex_par);  // no collision rows were sent
+    MergeMap mm{recv_slots(CH_IDX, r.idx_par), recv_slots(CH_EX, r.ex_par), co, nullptr,
+                r.send_pos.p, r.send_dst.p, r.send_off(), r.ids.p, static_cast<char*>(d_out), rb,
+                ctx->d_err};
     launch_copy_rows(ctx, mm, r.n, nullptr, rb, s);
   }
-
 
   // ---- protocol --------------------------------------------------------------------
   cudaStream_t cur_c = nullptr;
@@ -680,18 +676,23 @@ struct Engine {
   cudaEvent_t cur_ex_ready = nullptr, cur_co_ready = nullptr, rn_ex_ready = nullptr;
   bool has_next = false;
 
-  // deferred exclusive gradients of the previous iteration (embedding.cpp:314-339)
+  // deferred exclusive gradients of the previous iteration (embedding.cpp:314-339),
+  // on their own lane: they only have to land before the next exclusive
+  // prefetch reads rows, so routing / dedup / collision overlap with them
+  cudaEvent_t ev_ex_applied = nullptr;
   void apply_deferred() {
+    ev_ex_applied = nullptr;
     if (!has_pending) return;
     OwnBatch& op = O(pending_iter);
     ReqBatch& rp = R(pending_iter);
-    wait(lo, ev_pending_split);
+    wait(ux, ev_pending_split);
     if (p > 1) {
       std::vector<uint64_t> bytes(p);
       for (int d = 0; d < p; ++d) bytes[d] = kHdr + rb * rp.h_split[2 * d];
-      a2a(CH_EXG, exg_par, bytes, lo);
+      a2a(CH_EXG, exg_par, bytes, ux);
     }
-    update(op, CH_EXG, exg_par, op.has_co ? op.co.p : nullptr, 0, true, lo, FSX_PHASE_EX_UPDATE);
+    update(op, CH_EXG, exg_par, op.has_co ? op.co.p : nullptr, 0, true, ux, FSX_PHASE_EX_UPDATE);
+    ev_ex_applied = record(ux);
     has_pending = false;
   }
 
@@ -748,6 +749,7 @@ struct Engine {
     apply_deferred();
     wait(c, record(lo));
     wait(c, record(hi));
+    wait(c, record(ux));
   }
 
   // ---- stats (IterationStats, embedding.hpp:119-124) ----------------------------
@@ -789,6 +791,7 @@ struct Engine {
     for (auto e : prof_pool) cudaEventDestroy(e);
     if (lo) cudaStreamDestroy(lo);
     if (hi) cudaStreamDestroy(hi);
+    if (ux) cudaStreamDestroy(ux);
     if (win) cudaFree(win);
     for (auto* h : h_stats) cudaFreeHost(h);
   }
@@ -843,6 +846,7 @@ int fsx_engine_create(fsx_ctx* ctx, fsx_table* table, const fsx_engine_config* c
   if (prio) {
     slot[CH_EX] = idrows_rows_off(cap) + cap * rb;
     slot[CH_MASK] = kHdr + align16(cap);
+    slot[CH_IDX] = kHdr + align16(4 * cap);
     slot[CH_COG] = kHdr + cap * rb;
     slot[CH_EXG] = kHdr + cap * rb;
     slot[CH_COR] = idrows_rows_off(cap) + cap * rb;
@@ -863,12 +867,12 @@ int fsx_engine_create(fsx_ctx* ctx, fsx_table* table, const fsx_engine_config* c
   FSX_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
   FSX_CUDA(cudaStreamCreateWithPriority(&e->lo, cudaStreamNonBlocking, lo_prio));
   FSX_CUDA(cudaStreamCreateWithPriority(&e->hi, cudaStreamNonBlocking, hi_prio));
+  FSX_CUDA(cudaStreamCreateWithPriority(&e->ux, cudaStreamNonBlocking, lo_prio));
   e->d_stats.alloc(16);
   const uint64_t m = static_cast<uint64_t>(e->p) * cap;
   for (int k = 0; k < 3; ++k) {
     e->rq[k].reserve(cap);
     e->rq[k].scan.ensure(cap, 16);
-    e->rq[k].srt.reserve64();
     e->ow[k].reserve(m);
     e->ow[k].scan.ensure(m, 16);
   }

@@ -87,36 +87,6 @@ struct RouteOp {
   }
 };
 
-// requester composite key (owner, local index) so per-owner unique lists come
-// out as contiguous sorted runs (== the owner's recv_unique_per_src order)
-static __global__ void k_requester_keys(const uint64_t* __restrict__ ids, uint64_t n, int p, int lbits,
-                                 uint64_t* __restrict__ keys) {
-  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < n;
-       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t id = ids[j];
-    keys[j] = (static_cast<uint64_t>(id % static_cast<uint64_t>(p)) << lbits) |
-              (id / static_cast<uint64_t>(p));
-  }
-}
-
-// unique composite keys -> global ids and per-owner offsets uq_off[p+1]
-static __global__ void k_requester_uq(const uint64_t* __restrict__ uq_key, const uint64_t* d_u, int p,
-                               int lbits, uint64_t* __restrict__ uq_g, uint32_t* __restrict__ uq_off) {
-  const uint64_t U = *d_u;
-  const uint64_t mask = (lbits >= 64) ? ~0ull : ((1ull << lbits) - 1);
-  for (uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; u < U;
-       u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t k = uq_key[u];
-    const int d = static_cast<int>(k >> lbits);
-    uq_g[u] = (k & mask) * static_cast<uint64_t>(p) + static_cast<uint64_t>(d);
-    const int prev = u == 0 ? -1 : static_cast<int>(uq_key[u - 1] >> lbits);
-    for (int q = prev + 1; q <= d; ++q) uq_off[q] = static_cast<uint32_t>(u);
-    if (u + 1 == U)
-      for (int q = d + 1; q <= p; ++q) uq_off[q] = static_cast<uint32_t>(U);
-  }
-  if (U == 0 && blockIdx.x == 0 && threadIdx.x <= static_cast<unsigned>(p)) uq_off[threadIdx.x] = 0;
-}
-
 // ---- owner: flatten received ids (embedding.cpp:214-229) ----------------------
 // cnt[0] = M, cnt[2+s] = n_s, off[s] prefix (cnt[2+p+s])
 static __global__ void k_recv_prefix(CSlots slots, int p, uint64_t cap, uint64_t* cnt, DevErr* err) {
@@ -180,6 +150,7 @@ struct OwnerPackOp {
   const uint64_t* totals;     // [NC] from phase 2
   PackEntry* ex_list;
   PackEntry* co_list;
+  uint32_t* rank_us;          // [u][kMaxRanks]: position of row u in source s's message
   __device__ void count(uint64_t u, uint32_t (&c)[NC]) const {
     const uint32_t b = bits[u];
     const uint32_t f = co[u] ? 1u : 0u;
@@ -200,6 +171,7 @@ struct OwnerPackOp {
         PackEntry e{static_cast<uint32_t>(u), ex[2 * q + f], static_cast<uint32_t>(q), 0};
         if (f) co_list[base_co + e.rank] = e;
         else ex_list[base_ex + e.rank] = e;
+        rank_us[u * kMaxRanks + q] = e.rank;
       }
       base_ex += totals[2 * q];
       base_co += totals[2 * q + 1];
@@ -207,28 +179,38 @@ struct OwnerPackOp {
   }
 };
 
-// MASK messages of the CURRENT batch: for each unique row and each source
-// that asked for it, the row's collision flag at the row's rank in that
-// source's (sorted) unique list. Counter s = bit s.
-template <int NC_>
-struct MaskOp {
-  static constexpr int NC = NC_;
-  const uint32_t* bits;
-  const uint8_t* co;
-  Slots send;  // MASK send slots
-  __device__ void count(uint64_t u, uint32_t (&c)[NC]) const {
-    const uint32_t b = bits[u];
-#pragma unroll
-    for (int q = 0; q < NC; ++q) c[q] = (b >> q) & 1u;
+// Per-occurrence messages back to the requesters, in each source's own send
+// order (occurrence j of the owner batch = element occ_idx[j] of source
+// occ_src[j]'s id message):
+//  IDX  (next batch): where the occurrence's row sits in this owner's E_ex /
+//       E_co message to that source: rank | collision << 31. Replaces the
+//       reference's merge-time lower_bound by id (embedding.cpp:465-482).
+//  MASK (current batch): the occurrence's collision flag, i.e. mask_co_
+//       membership (embedding.cpp:392-401, 530) as one byte per occurrence.
+static __global__ void k_idx_pack(const uint32_t* __restrict__ inverse,
+                                  const uint8_t* __restrict__ occ_src,
+                                  const uint32_t* __restrict__ occ_idx, const uint64_t* d_m,
+                                  const uint32_t* __restrict__ rank_us,
+                                  const uint8_t* __restrict__ co, Slots send) {
+  const uint64_t m = *d_m;
+  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < m;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t u = inverse[j];
+    const int s = occ_src[j];
+    const uint32_t v = rank_us[static_cast<uint64_t>(u) * kMaxRanks + s] | (co[u] ? 0x80000000u : 0u);
+    reinterpret_cast<uint32_t*>(send.p[s] + kHdr)[occ_idx[j]] = v;
   }
-  __device__ void emit(uint64_t u, const uint32_t (&ex)[NC], const uint32_t (&c)[NC]) const {
-    const uint32_t b = bits[u];
-    const uint8_t f = co ? co[u] : 0;
-#pragma unroll
-    for (int q = 0; q < NC; ++q)
-      if ((b >> q) & 1u) reinterpret_cast<uint8_t*>(send.p[q] + kHdr)[ex[q]] = f;
-  }
-};
+}
+
+static __global__ void k_mask_pack(const uint32_t* __restrict__ inverse,
+                                   const uint8_t* __restrict__ occ_src,
+                                   const uint32_t* __restrict__ occ_idx, const uint64_t* d_m,
+                                   const uint8_t* __restrict__ co, Slots send) {
+  const uint64_t m = *d_m;
+  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < m;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    reinterpret_cast<uint8_t*>(send.p[occ_src[j]] + kHdr)[occ_idx[j]] = co && co[inverse[j]] ? 1 : 0;
+}
 
 // per-occurrence rank inside its (source, flag) class, flat recv order:
 // counters 2s (exclusive) / 2s+1 (collision)
@@ -256,22 +238,17 @@ struct OccRankOp {
   }
 };
 
-// ---- requester: collision flags from the MASK messages ------------------------
-static __global__ void k_requester_flags(CSlots mask, const uint32_t* __restrict__ uq_off, int p,
-                                  const uint64_t* d_u, uint8_t* __restrict__ flag, DevErr* err) {
-  const uint64_t U = *d_u;
-  for (uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; u < U;
-       u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    int d = 0;
-    while (d + 1 < p && uq_off[d + 1] <= u) ++d;
-    const uint64_t q = u - uq_off[d];
-    const uint64_t n = slot_n(mask.p[d]);
-    if (n != uq_off[d + 1] - uq_off[d]) {
-      report(err, kErrMaskOverlap, n, uq_off[d + 1] - uq_off[d]);
-      flag[u] = 0;
-      continue;
-    }
-    flag[u] = reinterpret_cast<const uint8_t*>(mask.p[d] + kHdr)[q];
+// ---- requester: collision flag of every sent occurrence (MASK messages) ----
+static __global__ void k_req_flags(CSlots mask, const uint8_t* __restrict__ send_dst,
+                                   const uint64_t* __restrict__ send_off, uint64_t n,
+                                   uint8_t* __restrict__ flag, DevErr* err) {
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const int d = send_dst[k];
+    const uint64_t q = k - send_off[d];
+    if (q == 0 && slot_n(mask.p[d]) != send_off[d + 1] - send_off[d])
+      report(err, kErrMaskOverlap, slot_n(mask.p[d]), send_off[d + 1] - send_off[d]);
+    flag[k] = reinterpret_cast<const uint8_t*>(mask.p[d] + kHdr)[q];
   }
 }
 
@@ -279,14 +256,10 @@ static __global__ void k_requester_flags(CSlots mask, const uint32_t* __restrict
 template <int NC_>
 struct SplitOp {
   static constexpr int NC = NC_;
-  const uint32_t* send_pos;
   const uint8_t* send_dst;
-  const uint32_t* occ_slot;  // position j -> requester unique slot
-  const uint8_t* flag;       // per unique slot (nullable -> all exclusive)
+  const uint8_t* flag;       // per grouped k (nullable -> all exclusive)
   uint32_t* split_rank;      // grouped k -> rank in its (dst, flag) message
-  __device__ uint32_t f(uint64_t k) const {
-    return flag ? (flag[occ_slot[send_pos[k]]] ? 1u : 0u) : 0u;
-  }
+  __device__ uint32_t f(uint64_t k) const { return flag ? (flag[k] ? 1u : 0u) : 0u; }
   __device__ void count(uint64_t k, uint32_t (&c)[NC]) const {
     const int d = send_dst[k];
     const uint32_t fl = f(k);
@@ -346,8 +319,7 @@ struct GradPackMap {
   const uint32_t* send_pos;
   const uint8_t* send_dst;
   const uint64_t* send_off;
-  const uint32_t* occ_slot;
-  const uint8_t* flag;        // nullable: everything to `ex`
+  const uint8_t* flag;        // per grouped k; nullable: everything to `ex`
   const uint32_t* split_rank; // nullable: rank = k - send_off[d]
   Slots co, ex;
   uint32_t row_bytes;
@@ -356,7 +328,7 @@ struct GradPackMap {
   }
   __device__ char* dst(uint64_t k) const {
     const int d = send_dst[k];
-    const bool f = flag && flag[occ_slot[send_pos[k]]];
+    const bool f = flag && flag[k];
     const uint64_t r = split_rank ? split_rank[k] : k - send_off[d];
     return (f ? co.p[d] : ex.p[d]) + kHdr + r * row_bytes;
   }
@@ -385,42 +357,34 @@ struct IdRowPackMap {
   }
 };
 
-// requester: locate every unique slot's row in the EX or CO_R message of its
-// owner (embedding.cpp:465-482: lower_bound per id)
-static __global__ void k_resolve_rows(CSlots ex, CSlots co, const uint64_t* __restrict__ uq_g,
-                               const uint32_t* __restrict__ uq_off, int p, const uint64_t* d_u,
-                               uint32_t row_bytes, const char** __restrict__ rowptr, DevErr* err) {
-  const uint64_t U = *d_u;
-  for (uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; u < U;
-       u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    int d = 0;
-    while (d + 1 < p && uq_off[d + 1] <= u) ++d;
-    const uint64_t id = uq_g[u];
-    const char* hit = nullptr;
-    for (int which = 0; which < 2 && !hit; ++which) {
-      const char* s = which == 0 ? ex.p[d] : co.p[d];
-      if (!s) continue;
-      const uint64_t n = slot_n(s);
-      const uint64_t* ids = reinterpret_cast<const uint64_t*>(s + kHdr);
-      uint64_t lo = 0, hi = n;
-      while (lo < hi) {
-        const uint64_t mid = (lo + hi) >> 1;
-        if (ids[mid] < id) lo = mid + 1; else hi = mid;
-      }
-      if (lo < n && ids[lo] == id) hit = s + idrows_rows_off(n) + lo * row_bytes;
-    }
-    if (!hit) report(err, kErrMissingRow, id, 0);
-    rowptr[u] = hit;
-  }
-}
-
+// requester merge (embedding.cpp:453-484): occurrence k of owner d takes row
+// IDX[d][q] of that owner's E_ex or E_co message; the id stored next to the
+// row must be the id asked for ("missing from both prefetched buffers").
 struct MergeMap {
-  const char* const* rowptr;
-  const uint32_t* occ_slot;
+  CSlots idx, ex, co;
+  const uint64_t* send_ids_dummy;
+  const uint32_t* send_pos;
+  const uint8_t* send_dst;
+  const uint64_t* send_off;
+  const uint64_t* ids;  // batch ids (position order)
   char* out;
   uint32_t row_bytes;
-  __device__ const char* src(uint64_t j) const { return rowptr[occ_slot[j]]; }
-  __device__ char* dst(uint64_t j) const { return out + j * row_bytes; }
+  DevErr* err;
+  __device__ const char* src(uint64_t k) const {
+    const int d = send_dst[k];
+    const uint64_t q = k - send_off[d];
+    const uint32_t v = reinterpret_cast<const uint32_t*>(idx.p[d] + kHdr)[q];
+    const char* s = (v & 0x80000000u) ? co.p[d] : ex.p[d];
+    const uint64_t r = v & 0x7fffffffu;
+    const uint64_t n = slot_n(s);
+    const uint64_t want = ids[send_pos[k]];
+    if (r >= n || reinterpret_cast<const uint64_t*>(s + kHdr)[r] != want) {
+      report(err, kErrMissingRow, want, 0);
+      return nullptr;
+    }
+    return s + idrows_rows_off(n) + r * row_bytes;
+  }
+  __device__ char* dst(uint64_t k) const { return out + static_cast<uint64_t>(send_pos[k]) * row_bytes; }
 };
 
 }  // namespace fsx

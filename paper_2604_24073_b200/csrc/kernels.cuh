@@ -329,23 +329,41 @@ struct SgdArgs {
   DevErr* err;
 };
 
-template <class T>
-__device__ __forceinline__ void sgd_apply(const SgdArgs<T>& a, uint32_t u, uint32_t d, double acc) {
+// vector of VE elements of T moved as one 4/8/16-byte access
+template <class T, int VE>
+struct alignas(sizeof(T) * VE) VecOf {
+  T v[VE];
+};
+
+template <class T, int VE>
+__device__ __forceinline__ void sgd_apply_vec(const SgdArgs<T>& a, uint32_t u, uint32_t col,
+                                              const double (&acc)[VE]) {
   const uint64_t l = a.rs.uniq_local[u];
   if (l >= a.g.local_rows) return;  // never write outside the shard
-  T* cell = a.table + l * a.g.dim + d;
-  const double v = __dsub_rn(static_cast<double>(*cell), __dmul_rn(a.lr, acc));
-  const T out = static_cast<T>(v);
-  *cell = out;
-  if (a.rows_out) a.rows_out[static_cast<uint64_t>(u) * a.g.dim + d] = out;
-  if (!isfinite(static_cast<double>(out)))
-    report(a.err, kErrNonFinite, l * static_cast<uint64_t>(a.g.p) + a.g.shard, 0);
+  VecOf<T, VE>* cell = reinterpret_cast<VecOf<T, VE>*>(a.table + l * a.g.dim + col);
+  VecOf<T, VE> r = *cell;
+  bool bad = false;
+#pragma unroll
+  for (int e = 0; e < VE; ++e) {
+    const double v = __dsub_rn(static_cast<double>(r.v[e]), __dmul_rn(a.lr, acc[e]));
+    r.v[e] = static_cast<T>(v);
+    bad |= !isfinite(static_cast<double>(r.v[e]));
+  }
+  *cell = r;
+  if (a.rows_out)
+    *reinterpret_cast<VecOf<T, VE>*>(a.rows_out + static_cast<uint64_t>(u) * a.g.dim + col) = r;
+  if (bad) report(a.err, kErrNonFinite, l * static_cast<uint64_t>(a.g.p) + a.g.shard, 0);
 }
 
-// One warp per work item; lanes stride the dimension; the occurrence loop is
-// unrolled 4-wide (independent loads first, then the in-order f64 adds).
-template <class T>
-__global__ void __launch_bounds__(256) k_sgd_chunks(SgdArgs<T> a) {
+// One warp per work item (a row, or one `chunk`-occurrence slice of a hot
+// row). Each lane owns NV vectors of VE consecutive elements (16-byte loads
+// when the row pitch allows), so one pass covers 32*VE*NV columns; the
+// occurrence loop is unrolled 4-wide with all loads issued before the
+// in-order f64 adds.
+template <class T, int VE, int NV>
+__global__ void __launch_bounds__(128, 6) k_sgd_chunks(SgdArgs<T> a) {
+  using V = VecOf<T, VE>;
+  constexpr int COLS = 32 * VE * NV;
   const uint64_t nwork = *a.d_work_n;
   const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
   const uint64_t wid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
@@ -358,64 +376,98 @@ __global__ void __launch_bounds__(256) k_sgd_chunks(SgdArgs<T> a) {
     const bool single = a.chunk == 0 || e - s <= a.chunk;
     const uint32_t kb = single ? s : s + item.y * a.chunk;
     const uint32_t ke = single ? e : min(e, kb + a.chunk);
-    for (uint32_t d0 = 0; d0 < dim; d0 += 32 * 4) {
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};
-      uint32_t k = kb;
-      for (; k + 4 <= ke; k += 4) {
-        const T* g[4];
+    for (uint32_t c0 = 0; c0 < dim; c0 += COLS) {
+      double acc[NV][VE];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) g[q] = a.gr.row(a.rs.perm[k + q]);
-        T v[4][4];
+      for (int v = 0; v < NV; ++v)
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+        for (int x = 0; x < VE; ++x) acc[v][x] = 0.0;
+      // lanes resolve up to 32 occurrences' gradient row addresses at once
+      // (perm -> source/rank -> row), then the warp walks them in order
+      for (uint32_t kb2 = kb; kb2 < ke; kb2 += 32) {
+        const uint32_t cnt = min(32u, ke - kb2);
+        const T* mine = lane < cnt ? a.gr.row(a.rs.perm[kb2 + lane]) : nullptr;
+        uint32_t q0 = 0;
+        for (; q0 + 2 <= cnt; q0 += 2) {
+          V g[2][NV];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const uint32_t d = d0 + c * 32 + lane;
-            v[q][c] = d < dim ? g[q][d] : T(0);
+          for (int q = 0; q < 2; ++q) {
+            const T* row = reinterpret_cast<const T*>(
+                __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(mine), q0 + q));
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+              const uint32_t col = c0 + (v * 32 + lane) * VE;
+              if (col < dim) g[q][v] = *reinterpret_cast<const V*>(row + col);
+            }
           }
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+          for (int q = 0; q < 2; ++q)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) acc[c] = __dadd_rn(acc[c], static_cast<double>(v[q][c]));
-      }
-      for (; k < ke; ++k) {
-        const T* g = a.gr.row(a.rs.perm[k]);
+            for (int v = 0; v < NV; ++v)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const uint32_t d = d0 + c * 32 + lane;
-          if (d < dim) acc[c] = __dadd_rn(acc[c], static_cast<double>(g[d]));
+              for (int x = 0; x < VE; ++x) acc[v][x] = __dadd_rn(acc[v][x], static_cast<double>(g[q][v].v[x]));
+        }
+        for (; q0 < cnt; ++q0) {
+          const T* row = reinterpret_cast<const T*>(
+              __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(mine), q0));
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+            const uint32_t col = c0 + (v * 32 + lane) * VE;
+            if (col < dim) {
+              const V g = *reinterpret_cast<const V*>(row + col);
+#pragma unroll
+              for (int x = 0; x < VE; ++x) acc[v][x] = __dadd_rn(acc[v][x], static_cast<double>(g.v[x]));
+            }
+          }
         }
       }
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const uint32_t d = d0 + c * 32 + lane;
-        if (d >= dim) continue;
+      for (int v = 0; v < NV; ++v) {
+        const uint32_t col = c0 + (v * 32 + lane) * VE;
+        if (col >= dim) continue;
         if (single) {
-          sgd_apply(a, u, d, acc[c]);
+          sgd_apply_vec<T, VE>(a, u, col, acc[v]);
         } else {
-          a.partials[(static_cast<uint64_t>(a.part_base[u]) + item.y) * dim + d] = acc[c];
+          double* p = a.partials + (static_cast<uint64_t>(a.part_base[u]) + item.y) * dim + col;
+#pragma unroll
+          for (int x = 0; x < VE; ++x) p[x] = acc[v][x];
         }
       }
     }
   }
 }
 
-template <class T>
-__global__ void __launch_bounds__(256) k_sgd_combine(SgdArgs<T> a) {
+// one CTA per multi-chunk row, each thread owning VE columns: the row's chunk
+// partials are summed in chunk order (8 loads in flight per thread)
+template <class T, int VE>
+__global__ void __launch_bounds__(128) k_sgd_combine(SgdArgs<T> a) {
   const uint64_t nm = *a.d_multi_n;
-  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-  const uint64_t wid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const unsigned lane = threadIdx.x & 31u;
   const uint32_t dim = a.g.dim;
-  for (uint64_t m = wid; m < nm; m += warps) {
+  for (uint64_t m = blockIdx.x; m < nm; m += gridDim.x) {
     const uint32_t u = a.multi[m];
     const uint32_t len = a.rs.seg_start[u + 1] - a.rs.seg_start[u];
     const uint32_t nch = (len + a.chunk - 1) / a.chunk;
-    const uint64_t b = a.part_base[u];
-    for (uint32_t d = lane; d < dim; d += 32) {
-      double acc = 0.0;
-      for (uint32_t q = 0; q < nch; ++q) acc = __dadd_rn(acc, a.partials[(b + q) * dim + d]);
-      sgd_apply(a, u, d, acc);
+    const double* base = a.partials + static_cast<uint64_t>(a.part_base[u]) * dim;
+    for (uint32_t col = threadIdx.x * VE; col < dim; col += blockDim.x * VE) {
+      double acc[VE];
+#pragma unroll
+      for (int x = 0; x < VE; ++x) acc[x] = 0.0;
+      uint32_t q = 0;
+      for (; q + 8 <= nch; q += 8) {
+        double t[8][VE];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+          for (int x = 0; x < VE; ++x) t[j][x] = base[static_cast<uint64_t>(q + j) * dim + col + x];
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+#pragma unroll
+          for (int x = 0; x < VE; ++x) acc[x] = __dadd_rn(acc[x], t[j][x]);
+      }
+      for (; q < nch; ++q)
+#pragma unroll
+        for (int x = 0; x < VE; ++x) acc[x] = __dadd_rn(acc[x], base[static_cast<uint64_t>(q) * dim + col + x]);
+      sgd_apply_vec<T, VE>(a, u, col, acc);
     }
   }
 }

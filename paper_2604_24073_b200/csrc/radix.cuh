@@ -4,7 +4,8 @@
 //   k_radix_hist    per-2048-key tile digit histogram; equal digits inside a
 //                   warp are aggregated with __match_any_sync so Zipf-hot keys
 //                   cost one shared atomic per warp, not one per key
-//   k_scan_u32      exclusive scan of the [digit][tile] count table (one CTA)
+//   k_radix_rows    exclusive scan of each digit's row of tile counts (one
+//                   warp per digit) and the digit totals
 //   k_radix_scatter stable rank inside the tile: each warp walks its
 //                   contiguous 256-key chunk in 32-key rounds; match_any gives
 //                   the equal-digit peers, popc(peers & lanemask_lt) the rank
@@ -49,20 +50,58 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const K* __restric
   counts[static_cast<uint64_t>(threadIdx.x) * tiles + blockIdx.x] = hist[threadIdx.x];
 }
 
+// one warp per digit: exclusive scan of counts[d][0..tiles) in place, total[d]
+static __global__ void __launch_bounds__(256) k_radix_rows(uint32_t* __restrict__ counts,
+                                                           unsigned tiles, uint32_t* __restrict__ total) {
+  const unsigned lane = threadIdx.x & 31u;
+  const unsigned d = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (d >= 256) return;
+  uint32_t* row = counts + static_cast<uint64_t>(d) * tiles;
+  uint32_t carry = 0;
+  for (unsigned t0 = 0; t0 < tiles; t0 += 32) {
+    const unsigned t = t0 + lane;
+    const uint32_t v = t < tiles ? row[t] : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= static_cast<unsigned>(o)) x += y;
+    }
+    if (t < tiles) row[t] = carry + x - v;
+    carry += __shfl_sync(0xffffffffu, x, 31);
+  }
+  if (lane == 0) total[d] = carry;
+}
+
 template <class K>
 __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(
     const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
     uint32_t* __restrict__ vout, uint64_t n_cap, const uint64_t* d_n, int shift,
-    const uint32_t* __restrict__ offsets, unsigned tiles) {
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ digit_total, unsigned tiles) {
   __shared__ uint32_t wcount[kRadixWarps][256];
   __shared__ uint32_t tile_off[256];
+  __shared__ uint32_t wsum[kRadixWarps];
   const uint64_t n = scan_n(n_cap, d_n);
   const uint64_t tile_base = static_cast<uint64_t>(blockIdx.x) * kRadixTile;
   if (tile_base >= n) return;
-  for (int w = 0; w < kRadixWarps; ++w) wcount[w][threadIdx.x] = 0;
-  tile_off[threadIdx.x] = offsets[static_cast<uint64_t>(threadIdx.x) * tiles + blockIdx.x];
-  __syncthreads();
   const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  for (int w = 0; w < kRadixWarps; ++w) wcount[w][threadIdx.x] = 0;
+  {
+    // digit base = exclusive scan of the digit totals (256 threads, 1 each)
+    const uint32_t tot = digit_total[threadIdx.x];
+    uint32_t x = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= static_cast<unsigned>(o)) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    uint32_t before = 0;
+    for (unsigned w = 0; w < warp; ++w) before += wsum[w];
+    tile_off[threadIdx.x] = before + x - tot + offsets[static_cast<uint64_t>(threadIdx.x) * tiles + blockIdx.x];
+  }
+  __syncthreads();
   const uint64_t base = tile_base + warp * kRadixWarpItems;
   K k[kRadixRounds];
   uint32_t v[kRadixRounds], rk[kRadixRounds];
@@ -122,7 +161,8 @@ void radix_sort_pairs(Ctx* ctx, K* k0, uint32_t* v0, K* k1, uint32_t* v1, uint64
   if (nbits < 1) nbits = 1;
   const int passes = (nbits + 7) / 8;
   const unsigned tiles = ceil_div(n_cap > 0 ? n_cap : 1, kRadixTile);
-  s.counts.ensure(static_cast<size_t>(tiles) * 256);
+  s.counts.ensure(static_cast<size_t>(tiles) * 256 + 256);
+  uint32_t* totals = s.counts.p + static_cast<size_t>(tiles) * 256;
   K* kin = k0;
   K* kout = k1;
   const uint32_t* vin = v_init;
@@ -137,9 +177,9 @@ void radix_sort_pairs(Ctx* ctx, K* k0, uint32_t* v0, K* k1, uint32_t* v1, uint64
     const int shift = 8 * p;
     FSX_LAUNCH(ctx, k_radix_hist<K>, tiles, kRadixThreads, 0, stream, kin, n_cap, d_n, shift,
                s.counts.p, tiles);
-    FSX_LAUNCH(ctx, k_scan_u32, 1, 1024, 0, stream, s.counts.p, static_cast<uint64_t>(tiles) * 256);
+    FSX_LAUNCH(ctx, k_radix_rows, 32, 256, 0, stream, s.counts.p, tiles, totals);
     FSX_LAUNCH(ctx, k_radix_scatter<K>, tiles, kRadixThreads, 0, stream, kin, vin, kout, vout,
-               n_cap, d_n, shift, s.counts.p, tiles);
+               n_cap, d_n, shift, s.counts.p, totals, tiles);
     // next pass reads what this one wrote
     K* kt = kin;
     kin = kout;

@@ -95,73 +95,49 @@ static __global__ void __launch_bounds__(kScanThreads) k_tile_reduce(Op op, uint
   }
 }
 
-// Block-wide (1024 threads) exclusive scan of one u32 per thread; returns
-// the block total.
-__device__ __forceinline__ uint32_t block1024_exclusive(uint32_t& v) {
-  __shared__ uint32_t wt[32];
-  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  uint32_t x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= static_cast<unsigned>(o)) x += y;
-  }
-  if (lane == 31) wt[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    uint32_t t = lane < (blockDim.x >> 5) ? wt[lane] : 0;
-    uint32_t s = t;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, s, o);
-      if (lane >= static_cast<unsigned>(o)) s += y;
-    }
-    wt[lane] = s - t;  // exclusive base of warp `lane`
-  }
-  __syncthreads();
-  uint32_t excl = wt[warp] + x - v;
-  __shared__ uint32_t total;
-  if (threadIdx.x == blockDim.x - 1) total = excl + v;
-  __syncthreads();
-  uint32_t tot = total;
-  v = excl;
-  __syncthreads();
-  return tot;
-}
-
-// One CTA: in-place exclusive scan of n u32 (each thread a contiguous chunk).
-// Returns nothing; used for radix tile-offset tables.
-static __global__ void __launch_bounds__(1024) k_scan_u32(uint32_t* data, uint64_t n) {
-  const uint64_t per = (n + blockDim.x - 1) / blockDim.x;
-  const uint64_t lo = threadIdx.x * per;
-  const uint64_t hi = lo + per < n ? lo + per : n;
-  uint32_t s = 0;
-  for (uint64_t t = lo; t < hi; ++t) s += data[t];
-  block1024_exclusive(s);
-  for (uint64_t t = lo; t < hi; ++t) {
-    uint32_t x = data[t];
-    data[t] = s;
-    s += x;
-  }
-}
-
-// One CTA: exclusive scan over `tiles` rows of NC counters (in place), grand
-// totals to `totals` (device) as u64.
+// One CTA of 1024 threads: exclusive scan over `tiles` rows of NC counters
+// (in place, all counters in one block pass), grand totals to `totals`.
 template <int NC>
 static __global__ void __launch_bounds__(1024) k_scan_tiles(uint32_t* tile_sums, unsigned tiles,
-                                                     uint64_t* totals) {
+                                                            uint64_t* totals) {
+  __shared__ uint32_t wt[32][NC];
   const unsigned per = (tiles + blockDim.x - 1) / blockDim.x;
   const unsigned lo = threadIdx.x * per;
   const unsigned hi = min(tiles, lo + per);
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint32_t s[NC], incl[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) s[c] = 0;
+  for (unsigned t = lo; t < hi; ++t)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) s[c] += tile_sums[static_cast<uint64_t>(t) * NC + c];
+#pragma unroll
   for (int c = 0; c < NC; ++c) {
-    uint32_t s = 0;
-    for (unsigned t = lo; t < hi; ++t) s += tile_sums[static_cast<uint64_t>(t) * NC + c];
-    const uint32_t tot = block1024_exclusive(s);
-    if (totals && threadIdx.x == 0) totals[c] = tot;
+    uint32_t x = s[c];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= static_cast<unsigned>(o)) x += y;
+    }
+    incl[c] = x;
+    if (lane == 31) wt[warp][c] = x;
+  }
+  __syncthreads();
+  const unsigned nw = blockDim.x >> 5;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    uint32_t before = 0, all = 0;
+    for (unsigned w = 0; w < nw; ++w) {
+      const uint32_t t = wt[w][c];
+      before += w < warp ? t : 0u;
+      all += t;
+    }
+    uint32_t run = before + incl[c] - s[c];
+    if (totals && threadIdx.x == 0) totals[c] = all;
     for (unsigned t = lo; t < hi; ++t) {
-      uint32_t x = tile_sums[static_cast<uint64_t>(t) * NC + c];
-      tile_sums[static_cast<uint64_t>(t) * NC + c] = s;
-      s += x;
+      const uint32_t x = tile_sums[static_cast<uint64_t>(t) * NC + c];
+      tile_sums[static_cast<uint64_t>(t) * NC + c] = run;
+      run += x;
     }
   }
 }
