@@ -1,0 +1,100 @@
+"""Multi-process engine parity (one process per GPU, CUDA-IPC receive windows,
+copy-engine transfers + stream-memory-op flags). Launched by
+tests/test_gpu_multiproc.py as
+
+    torchrun --nproc-per-node N tests/mp_engine_check.py [f64|f32]
+
+Each rank runs the reference's run_engine protocol (test_embedding.cpp:22-63)
+on its shard; rank 0 gathers the table and compares it with the oracle:
+bit-exact for f64, and sync == prio bitwise for f32."""
+import os
+import sys
+
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+from paper_2604_24073_b200 import embedding as E  # noqa: E402
+from paper_2604_24073_b200 import workload  # noqa: E402
+from paper_2604_24073_b200.comm import ProcessGroupFabric  # noqa: E402
+
+
+def run(prio, dtype, batches, geom, rank, world, dev, chunk):
+    fabric = ProcessGroupFabric(rank, world, dev)
+    ctx = E.Context(dev, rank, world)
+    shard = E.ShardView(geom, rank, 0.05, 3, dtype=dtype, ctx=ctx)
+    cap = max(len(b) for it in batches for b in it)
+    cls = E.PrioritizedEmbedding if prio else E.SynchronizedEmbedding
+    eng = cls(shard, fabric.communicator(), max_occurrences=cap, reduce_chunk=chunk)
+    s = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(s):
+        for i in range(len(batches)):
+            if prio:
+                nxt = batches[i + 1][rank] if i + 1 < len(batches) else None
+                rows = eng.forward(batches[i][rank], nxt, stream=s)
+            else:
+                rows = eng.forward(batches[i][rank], stream=s)
+            eng.backward(rows * 0.125 + 0.0625, stream=s)
+        if prio:
+            eng.finalize(stream=s)
+    s.synchronize()
+    ctx.sync()
+    stats = eng.stats() if prio else None
+    vals = torch.from_numpy(shard.values()).to(dev)
+    eng.close()
+    # gather the table (gather_full_table, embedding.cpp:611-631)
+    sizes = [geom.local_rows(r) for r in range(world)]
+    parts = [torch.zeros((sizes[r], geom.dim), dtype=torch.float64, device=dev) for r in range(world)]
+    dist.all_gather(parts, vals)
+    full = np.zeros((geom.total_rows, geom.dim), np.float64)
+    for r in range(world):
+        full[r::world] = parts[r].cpu().numpy()
+    return full, stats
+
+
+def main():
+    dtype = sys.argv[1] if len(sys.argv) > 1 else "f64"
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    dev = int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(dev)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    rows, dim, iters = 40_000, 32, 5
+    batches = [[workload.zipf_batch(50 + r, 4000, rows, offset=4000 * i) for r in range(world)]
+               for i in range(iters)]
+    geom = E.TableGeometry(rows, dim, world)
+    chunk = 0 if dtype == "f64" else 64
+    t_sync, _ = run(False, dtype, batches, geom, rank, world, dev, chunk)
+    t_prio, stats = run(True, dtype, batches, geom, rank, world, dev, chunk)
+    ok = True
+    if rank == 0:
+        from oracle import Oracle
+        O = Oracle()
+        want, want_stats = O.run_engine(world, batches, rows, dim, 0.05, 3, with_stats=True)
+        same = np.array_equal(t_sync.view(np.uint64), t_prio.view(np.uint64))
+        print(f"[mp] world={world} dtype={dtype} sync==prio bitwise: {same}")
+        ok &= same
+        if dtype == "f64":
+            exact = np.array_equal(t_prio.view(np.uint64), want.view(np.uint64))
+            got_stats = np.array([[s.collision_rows, s.unique_next_rows, s.blocking_bytes] for s in stats],
+                                 np.uint64)
+            st_ok = np.array_equal(got_stats, want_stats)
+            print(f"[mp] f64 bit-exact vs oracle: {exact}; stats equal: {st_ok}")
+            ok &= exact and st_ok
+        else:
+            nrm = float(np.max(np.abs(t_prio - want)) / np.max(np.abs(want)))
+            print(f"[mp] f32 normwise rel err vs f64 oracle: {nrm:.3e}")
+            ok &= nrm < 1e-6
+        print("MP_OK" if ok else "MP_FAIL", flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()
