@@ -218,6 +218,10 @@ def main():
     batches = batches_for(args, rank, world, iters)
     t_gen = time.time() - t_gen
     cap = int(max(b.size for b in batches) * 1.05) + 1024
+    if world > 1:  # every rank's engine must use the same capacity (same window layout)
+        t = torch.tensor([cap], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        cap = int(t.item())
     tables = args.tables_per_rank * world
     total_rows = tables * args.rows_per_table
     geom = E.TableGeometry(total_rows, args.dim, world)

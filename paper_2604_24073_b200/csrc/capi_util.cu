@@ -19,6 +19,27 @@ __global__ void k_max_u64(const uint64_t* __restrict__ k, uint64_t n, unsigned l
 }  // namespace
 
 void capi_set_error(const std::string& msg) { g_last_error = msg; }
+
+namespace drv {
+namespace {
+void* entry(const char* name) {
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  FSX_CUDA(cudaGetDriverEntryPoint(name, &fn, cudaEnableDefault, &q));
+  if (!fn || q != cudaDriverEntryPointSuccess)
+    raise(FSX_ERR_CUDA, std::string("cuda driver entry point not found: ") + name);
+  return fn;
+}
+}  // namespace
+WriteValue32 write_value32() {
+  static WriteValue32 f = reinterpret_cast<WriteValue32>(entry("cuStreamWriteValue32"));
+  return f;
+}
+WaitValue32 wait_value32() {
+  static WaitValue32 f = reinterpret_cast<WaitValue32>(entry("cuStreamWaitValue32"));
+  return f;
+}
+}  // namespace drv
 const char* capi_last_error() { return g_last_error.c_str(); }
 
 void capi_launch_max_u64(Ctx* ctx, const uint64_t* d_keys, uint64_t n, uint64_t* d_max,

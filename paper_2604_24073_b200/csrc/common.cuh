@@ -35,14 +35,22 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 }
 inline void cu_check(CUresult e, const char* what, const char* file, int line) {
   if (e != CUDA_SUCCESS) {
-    const char* s = nullptr;
-    cuGetErrorString(e, &s);
     char buf[512];
-    std::snprintf(buf, sizeof buf, "cuda driver: %s failed at %s:%d: %s", what, file, line,
-                  s ? s : "?");
+    std::snprintf(buf, sizeof buf, "cuda driver: %s failed at %s:%d: CUresult %d", what, file, line,
+                  static_cast<int>(e));
     throw Error(FSX_ERR_CUDA, buf);
   }
 }
+
+// Driver entry points used by the copy-engine transport, resolved through the
+// runtime (cudaGetDriverEntryPoint) so libfsx.so has no link-time dependency
+// on libcuda and loads on machines without a driver (build/CPU checks).
+namespace drv {
+using WriteValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WaitValue32 = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+WriteValue32 write_value32();
+WaitValue32 wait_value32();
+}  // namespace drv
 #define FSX_CUDA(x) ::fsx::cuda_check((x), #x, __FILE__, __LINE__)
 #define FSX_CU(x) ::fsx::cu_check((x), #x, __FILE__, __LINE__)
 

@@ -339,7 +339,7 @@ struct Engine {
         FSX_CUDA(cudaEventRecord(ev, s));
         Hub::get().post(pv.local, ch, v, me, ev);
       } else {
-        FSX_CU(cuStreamWriteValue32(reinterpret_cast<CUstream>(s),
+        FSX_CU(drv::write_value32()(reinterpret_cast<CUstream>(s),
                                     reinterpret_cast<CUdeviceptr>(pv.flags + ch * kMaxRanks + me), v,
                                     CU_STREAM_WRITE_VALUE_DEFAULT));
       }
@@ -351,7 +351,7 @@ struct Engine {
         FSX_CUDA(cudaStreamWaitEvent(s, ev, 0));
         FSX_CUDA(cudaEventDestroy(ev));
       } else {
-        FSX_CU(cuStreamWaitValue32(reinterpret_cast<CUstream>(s),
+        FSX_CU(drv::wait_value32()(reinterpret_cast<CUstream>(s),
                                    reinterpret_cast<CUdeviceptr>(flags + ch * kMaxRanks + src), v,
                                    CU_STREAM_WAIT_VALUE_GEQ));
       }
