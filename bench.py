@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="fsx", choices=["fsx", "reference"])
     ap.add_argument("--mode", default="prio", choices=["prio", "sync"])
+    ap.add_argument("--transport", default=None, choices=["ce", "nccl"],
+                    help="all-to-all transport (default: ce for prio, nccl for the sync baseline)")
     ap.add_argument("--tables-per-rank", type=int, default=8)
     ap.add_argument("--rows-per-table", type=int, default=10_000_000)
     ap.add_argument("--dim", type=int, default=256)
@@ -50,18 +52,23 @@ def parse():
     ap.add_argument("--seed", type=int, default=20261018)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-phases", type=int, default=1)
+    ap.add_argument("--cfg5", type=int, default=-1,
+                    help="also run config 5 (embedding + HSTU-style victim; blocking NCCL vs "
+                         "prioritized copy-engine); default: on when N > 1")
+    ap.add_argument("--victim-layers", type=int, default=1)
     return ap.parse_args()
 
 
 # ---- workload -----------------------------------------------------------------
-def batches_for(args, rank, world, iters):
+def batches_for(args, rank, world, iters, with_lens=False):
     from paper_2604_24073_b200 import workload
     tables = args.tables_per_rank * world
-    out = []
+    out, lens = [], []
     for i in range(iters):
-        _, ids = workload.cfg_tokens(args.seed, i, rank, args.samples, tables, args.rows_per_table)
+        ln, ids = workload.cfg_tokens(args.seed, i, rank, args.samples, tables, args.rows_per_table)
         out.append(ids)
-    return out
+        lens.append(ln)
+    return (out, lens) if with_lens else out
 
 
 def work_rows(batches, world=1):
@@ -116,6 +123,86 @@ class Clocks:
                           if len(r) > 5 + k and r[5 + k].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---- config 5: synthetic HSTU-style attention "victim" ---------------------------
+class Victim:
+    """The dense model between embedding forward and backward (config 5): one
+    attention layer over each sample's UIH sequence, so its cost grows like
+    c1*sum(L) + c2*sum(L^2) (sim.hpp:24-35). Samples are bucketed by length
+    (powers of two, padded within a bucket), QKV / output projections are
+    bf16 GEMMs and attention is torch SDPA (fused flash kernels); forward and
+    autograd backward run on the compute stream. Its input is the engine's
+    batch-major output and the gradient it hands back is the real gradient
+    of sum(outputs) with respect to those embedding rows."""
+
+    EDGES = [0, 64, 128, 256, 512, 1024, 2048, 4096, 8193]
+
+    @classmethod
+    def bucket_sizes(cls, lens_list):
+        """fixed samples-per-bucket over all iterations: constant shapes, so
+        attention kernels / plans are chosen once, during warm-up"""
+        sizes = []
+        for lo, hi in zip(cls.EDGES[:-1], cls.EDGES[1:]):
+            m = max(int(np.sum((np.asarray(l) >= max(lo, 1)) & (np.asarray(l) < hi))) for l in lens_list)
+            sizes.append(((m + 7) // 8) * 8 if m else 0)
+        return sizes
+
+    def __init__(self, lens, dim, dev, layers=1, heads=4, sizes=None):
+        import torch
+        self.torch = torch
+        self.dim, self.heads, self.layers = dim, heads, layers
+        lens = np.asarray(lens, np.int64)
+        starts = np.concatenate([[0], np.cumsum(lens)[:-1]])
+        sizes = sizes or self.bucket_sizes([lens])
+        self.buckets = []
+        for (lo, hi), bsz in zip(zip(self.EDGES[:-1], self.EDGES[1:]), sizes):
+            if bsz == 0:
+                continue
+            sel = np.nonzero((lens >= max(lo, 1)) & (lens < hi))[0]
+            Lb = hi - 1 if hi > 64 else 64
+            Lb = ((Lb + 63) // 64) * 64
+            # gather index [bsz, Lb]: token positions, padding -> -1 (a zero row)
+            j = np.arange(Lb)[None, :]
+            idx = np.full((bsz, Lb), -1, np.int64)
+            idx[:sel.size] = np.where(j < lens[sel][:, None], starts[sel][:, None] + j, -1)
+            self.buckets.append(torch.from_numpy(idx).to(dev))
+        self.n = int(lens.sum())
+        g = torch.Generator(device=dev)
+        g.manual_seed(5)
+        self.wqkv = [(torch.randn(dim, 3 * dim, generator=g, device=dev) / dim ** 0.5).to(torch.bfloat16)
+                     for _ in range(layers)]
+        self.wo = [(torch.randn(dim, dim, generator=g, device=dev) / dim ** 0.5).to(torch.bfloat16)
+                   for _ in range(layers)]
+
+    def step(self, rows):
+        """rows: [n, dim] fp32 embedding output -> grads [n, dim] fp32."""
+        torch = self.torch
+        F = torch.nn.functional
+        x = rows.detach().requires_grad_(True)
+        xb = torch.cat([x.to(torch.bfloat16), torch.zeros((1, self.dim), dtype=torch.bfloat16,
+                                                            device=x.device)])
+        loss = 0
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+        with sdpa_kernel([SDPBackend.CUDNN_ATTENTION]):
+            loss = self._layers(xb)
+        loss.backward()
+        return x.grad
+
+    def _layers(self, xb):
+        torch = self.torch
+        F = torch.nn.functional
+        loss = 0
+        for idx in self.buckets:
+            h = xb[idx.clamp(min=-1)]  # [b, Lb, dim], pad rows = 0
+            b, Lb, _ = h.shape
+            for layer in range(self.layers):
+                qkv = (h @ self.wqkv[layer]).view(b, Lb, 3, self.heads, self.dim // self.heads)
+                q, k, v = (t.contiguous() for t in qkv.permute(2, 0, 3, 1, 4))
+                a = F.scaled_dot_product_attention(q, k, v, is_causal=True)
+                h = a.transpose(1, 2).reshape(b, Lb, self.dim) @ self.wo[layer]
+            loss = loss + h.float().sum()
+        return loss
 
 
 # ---- CPU baseline (the reference library, oracle/_ref) --------------------------
@@ -213,9 +300,10 @@ def main():
     comm = fabric.communicator(rank)
 
     W, K = max(args.warmup, 3), args.steps
-    iters = W + 2 * K + 2
+    cfg5 = args.cfg5 if args.cfg5 >= 0 else int(world > 1)
+    iters = W + 2 * K + min(K, 5) + 2 + (2 * K + 4 if cfg5 else 0)
     t_gen = time.time()
-    batches = batches_for(args, rank, world, iters)
+    batches, blens = batches_for(args, rank, world, iters, with_lens=True)
     t_gen = time.time() - t_gen
     cap = int(max(b.size for b in batches) * 1.05) + 1024
     if world > 1:  # every rank's engine must use the same capacity (same window layout)
@@ -230,7 +318,8 @@ def main():
     shard = E.ShardView(geom, rank, 0.05, 7, dtype="f32", ctx=ctx)
     t_init = time.time() - t0
     cls = E.PrioritizedEmbedding if args.mode == "prio" else E.SynchronizedEmbedding
-    eng = cls(shard, comm, max_occurrences=cap, reduce_chunk=args.reduce_chunk)
+    transport = args.transport or ("ce" if args.mode == "prio" or world == 1 else "nccl")
+    eng = cls(shard, comm, max_occurrences=cap, reduce_chunk=args.reduce_chunk, transport=transport)
 
     stream = torch.cuda.Stream(device=dev)
     d_ids = [torch.from_numpy(b.view(np.int64)).to(dev) for b in batches]
@@ -294,6 +383,8 @@ def main():
             eng.set_profiling(True)
             eng.phase_ms()  # reset
         launches0 = ctx.launches()
+        if args.mode == "prio":
+            eng.exposed_ms()  # reset the accumulator
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with Clocks(local) as clk:
             barrier()
@@ -304,15 +395,15 @@ def main():
             barrier()
         ms_dev = ev0.elapsed_time(ev1)
         launches = ctx.launches() - launches0
+        exp_timed = eng.exposed_ms() / K
         phases = eng.phase_ms() if args.profile_phases and hasattr(eng, "set_profiling") else {}
         if hasattr(eng, "set_profiling"):
             eng.set_profiling(False)
-        # exposed comm per iteration: separate short pass (syncs per step)
-        exp = []
+        # a few untimed steps between the sections
         for i in range(W + K, W + K + min(K, 5)):
             step(i)
-            exp.append(eng.exposed_ms())
         barrier()
+        eng.exposed_ms()
         # end-to-end: host ids -> device each step, stats read back
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         first_e2e = W + K + min(K, 5)
@@ -327,6 +418,80 @@ def main():
         barrier()
         ms_e2e = e0.elapsed_time(e1)
     stats = eng.stats() if args.mode == "prio" else []
+
+    # ---- config 5: embedding + victim, blocking NCCL vs prioritized CE ----
+    cfg5_out = None
+    if cfg5 and args.mode == "prio":
+        it0 = first_e2e + n_e2e  # next iteration of the prioritized engine
+        vsizes = Victim.bucket_sizes([blens[i] for i in range(it0, min(it0 + K + 1, iters))])
+        victims = {i: Victim(blens[i], args.dim, dev, args.victim_layers, sizes=vsizes)
+                   for i in range(it0, min(it0 + K + 1, iters))}
+        vt0, vt1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+        def victim_only(i):
+            n = batches[i].size
+            return victims[i].step(out[:n])
+
+        with torch.cuda.stream(stream):
+            # (0) victim alone (no embedding traffic): its undisturbed time
+            for i in range(it0, it0 + 2):
+                victim_only(i)
+            barrier()
+            vt0.record(stream)
+            for i in range(it0, it0 + K):
+                victim_only(i)
+            vt1.record(stream)
+            barrier()
+            victim_alone = vt0.elapsed_time(vt1) / K
+            # (B) prioritized + copy engines, victim between forward and backward
+            res = {}
+            eng.exposed_ms()
+            barrier()
+            e0.record(stream)
+            for i in range(it0, it0 + K):
+                n = batches[i].size
+                eng.forward(d_ids[i], d_ids[i + 1], out=out[:n], stream=stream)
+                g = victims[i].step(out[:n])
+                eng.backward(g, stream=stream)
+            e1.record(stream)
+            barrier()
+            res["prio_ce"] = (e0.elapsed_time(e1) / K, eng.exposed_ms() / K)
+        # (A) the blocking baseline: synchronized engine, NCCL all-to-all (N>1)
+        base_tr = "nccl" if world > 1 else "ce"
+        sync_eng = E.SynchronizedEmbedding(shard, comm, max_occurrences=cap,
+                                           reduce_chunk=args.reduce_chunk, transport=base_tr)
+        with torch.cuda.stream(stream):
+            for i in range(it0, it0 + 2):
+                n = batches[i].size
+                sync_eng.forward(d_ids[i], out=out[:n], stream=stream)
+                sync_eng.backward(victims[i].step(out[:n]), stream=stream)
+            barrier()
+            sync_eng.exposed_ms()
+            e0.record(stream)
+            for i in range(it0, it0 + K):
+                n = batches[i].size
+                sync_eng.forward(d_ids[i], out=out[:n], stream=stream)
+                sync_eng.backward(victims[i].step(out[:n]), stream=stream)
+            e1.record(stream)
+            barrier()
+            res["sync_" + base_tr] = (e0.elapsed_time(e1) / K, sync_eng.exposed_ms() / K)
+        sync_eng.close()
+        b_key = "sync_" + base_tr
+        step_b = max_over_ranks(res[b_key][0])
+        step_p = max_over_ranks(res["prio_ce"][0])
+        exp_b = max_over_ranks(res[b_key][1])
+        exp_p = max_over_ranks(res["prio_ce"][1])
+        cfg5_out = {
+            "workload": "config 5: config-4 embeddings + 1-layer HSTU-style attention victim (bucketed SDPA, "
+                        "bf16) between forward and backward, real gradients",
+            "baseline": f"SynchronizedEmbedding, blocking {base_tr.upper()} all-to-all on the compute stream",
+            "freescale": "PrioritizedEmbedding, copy-engine all-to-all on side lanes",
+            "exposed_ms_per_iter": {b_key: round(exp_b, 4), "prio_ce": round(exp_p, 4)},
+            "exposed_reduction_pct": round(100.0 * (1 - exp_p / exp_b), 2) if exp_b > 0 else None,
+            "step_ms": {b_key: round(step_b, 4), "prio_ce": round(step_p, 4)},
+            "victim_alone_ms": round(max_over_ranks(victim_alone), 4),
+            "comm_sms": {b_key: "NCCL kernels" if base_tr == "nccl" else 0, "prio_ce": 0},
+        }
 
     ms_dev = max_over_ranks(ms_dev)
     ms_e2e = max_over_ranks(ms_e2e)
@@ -346,8 +511,8 @@ def main():
     rows_e2e = sum_over_ranks(rows_e2e)
     value = rows_timed / (ms_dev * 1e-3)
     e2e_value = rows_e2e / (ms_e2e * 1e-3)
-    exposed_ms = max_over_ranks(float(np.mean(exp)) if exp else 0.0)
-    exposed_sum = sum_over_ranks(float(np.mean(exp)) if exp else 0.0)
+    exposed_ms = max_over_ranks(exp_timed)
+    exposed_sum = sum_over_ranks(exp_timed)
 
     # roofline of the dominant row-moving phase (rank 0's view)
     rb = args.dim * 4
@@ -408,7 +573,7 @@ def main():
                                    "2048 UIH samples/GPU/iter (16K global at 8 GPUs), Zipf(1.1) ids, "
                                    "power-law UIH 16..8192, row-wise gid mod N, prioritized collision-first "
                                    "update",
-                       "mode": args.mode, "tables": tables, "rows_per_table": args.rows_per_table,
+                       "mode": args.mode, "transport": transport, "tables": tables, "rows_per_table": args.rows_per_table,
                        "dim": args.dim, "samples_per_rank": args.samples,
                        "ids_per_rank_per_iter": int(np.mean([b.size for b in timed])),
                        "reduce_chunk": args.reduce_chunk, "grads": "fixed synthetic upstream gradient",
@@ -423,6 +588,7 @@ def main():
             "roofline": roof,
             "phases_ms_per_step": {k: round(v[0] / K, 4) for k, v in phases.items() if v[1]},
             "cpu_baseline": cpu,
+            "cfg5": cfg5_out,
             "clocks": clocks,
             "setup_s": {"workload_gen": round(t_gen, 2), "table_init": round(t_init, 2)},
             "collision_fraction": round(float(np.mean([s.collision_fraction for s in stats[W:W + K]])), 4)

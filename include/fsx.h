@@ -174,8 +174,12 @@ int fsx_engine_finalize(fsx_engine* e, void* stream);
  * unique_next_rows, blocking_bytes]; synchronizes. Returns FSX_ERR_OUT_OF_RANGE
  * past the last forward. */
 int fsx_engine_stats(fsx_engine* e, int iter, uint64_t* out3);
-/* exposed wait of the last iteration: ms the caller's stream spent waiting
- * on embedding traffic (event pairs around each wait), synchronizes */
+/* exposed embedding communication: total ms the caller's stream spent
+ * blocked on embedding traffic since the last call — waits on the side lanes'
+ * results (prioritized) and blocking all-to-alls on the caller's stream
+ * (synchronized) — measured with CUDA event pairs around each wait; the
+ * reference's Main/Wait + blocking collective time (sim.cpp:25-35).
+ * Synchronizes; resets the accumulator. */
 int fsx_engine_exposed_ms(fsx_engine* e, double* ms);
 
 /* Live per-phase device timing (CUDA event pairs on the stream each phase

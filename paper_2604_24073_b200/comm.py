@@ -44,6 +44,15 @@ class Communicator:
     def connect(self, engine_handle) -> None:
         self.fabric.connect(self._rank, engine_handle)
 
+    def connect_nccl(self, engine_handle) -> None:
+        self.fabric.connect_nccl(self._rank, engine_handle)
+
+
+def _nccl_id() -> bytes:
+    buf = (C.c_ubyte * 128)()
+    _lib.call("fsx_nccl_unique_id", buf)
+    return bytes(buf)
+
 
 class DeviceFabric:
     def __init__(self, world_size: int, devices: list[int] | None = None):
@@ -74,6 +83,15 @@ class DeviceFabric:
         for peer in range(self.world_size):
             if peer != rank:
                 _lib.call("fsx_engine_connect_local", engine_handle, peer, self._engines[peer][k])
+        self._wait()
+
+    def connect_nccl(self, rank: int, engine_handle) -> None:
+        """NCCL baseline: rank 0 makes the unique id, every rank joins."""
+        if rank == 0:
+            self._nccl_uid = _nccl_id()
+        self._wait()
+        buf = (C.c_ubyte * 128).from_buffer_copy(self._nccl_uid)
+        _lib.call("fsx_engine_connect_nccl", engine_handle, buf)
         self._wait()
 
     def _wait(self) -> None:
@@ -135,4 +153,12 @@ class ProcessGroupFabric:
             if peer != rank:
                 buf = (C.c_ubyte * len(b)).from_buffer_copy(b)
                 _lib.call("fsx_engine_connect_ipc", engine_handle, peer, buf, len(b))
+        dist.barrier()
+
+    def connect_nccl(self, rank: int, engine_handle) -> None:
+        import torch.distributed as dist
+        obj = [_nccl_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        buf = (C.c_ubyte * 128).from_buffer_copy(obj[0])
+        _lib.call("fsx_engine_connect_nccl", engine_handle, buf)
         dist.barrier()

@@ -26,12 +26,53 @@
 #include <memory>
 #include <vector>
 
+#include <dlfcn.h>
+
 #include "capi_util.cuh"
 #include "engine_kernels.cuh"
+#include "nccl.h"
 
 namespace fsx {
 
 enum Channel : int { CH_IDS, CH_ROWS, CH_GRADS, CH_EX, CH_MASK, CH_COG, CH_EXG, CH_COR, CH_IDX, NCH };
+
+// ---- NCCL, loaded at run time (baseline transport only) ----------------------
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  static NcclApi& get() {
+    static NcclApi a = [] {
+      NcclApi n;
+      // prefer the NCCL torch already loaded into this process
+      n.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);
+      if (!n.h) n.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+      if (!n.h) return n;
+      n.GetUniqueId = reinterpret_cast<decltype(n.GetUniqueId)>(dlsym(n.h, "ncclGetUniqueId"));
+      n.CommInitRank = reinterpret_cast<decltype(n.CommInitRank)>(dlsym(n.h, "ncclCommInitRank"));
+      n.CommDestroy = reinterpret_cast<decltype(n.CommDestroy)>(dlsym(n.h, "ncclCommDestroy"));
+      n.GroupStart = reinterpret_cast<decltype(n.GroupStart)>(dlsym(n.h, "ncclGroupStart"));
+      n.GroupEnd = reinterpret_cast<decltype(n.GroupEnd)>(dlsym(n.h, "ncclGroupEnd"));
+      n.Send = reinterpret_cast<decltype(n.Send)>(dlsym(n.h, "ncclSend"));
+      n.Recv = reinterpret_cast<decltype(n.Recv)>(dlsym(n.h, "ncclRecv"));
+      n.GetErrorString = reinterpret_cast<decltype(n.GetErrorString)>(dlsym(n.h, "ncclGetErrorString"));
+      return n;
+    }();
+    if (!a.h || !a.Send) raise(FSX_ERR_CONFIG, "fsx: libnccl.so.2 not available for the NCCL baseline");
+    return a;
+  }
+};
+
+inline void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    raise(FSX_ERR_COLLECTIVE, std::string("nccl: ") + what + ": " + NcclApi::get().GetErrorString(r));
+}
 
 namespace {
 
@@ -195,6 +236,7 @@ struct Engine {
   size_t flags_off = 0;
   DevBuf<char> stage;         // send staging, same layout as the channel region of win
   PeerView peer[kMaxRanks];
+  ncclComm_t nccl = nullptr;  // FSX_TRANSPORT_NCCL (blocking baseline)
   uint32_t seq[NCH] = {};
   cudaStream_t lo = nullptr, hi = nullptr, ux = nullptr;  // ux: deferred exclusive updates
   std::vector<cudaEvent_t> ev_pool;
@@ -292,6 +334,8 @@ struct Engine {
     if (e) FSX_CUDA(cudaStreamWaitEvent(s, e, 0));
   }
   cudaEvent_t timing_event() {
+    // pairs accumulate across iterations until fsx_engine_exposed_ms reads
+    // them; only then is the pool recycled
     if (timing_next == timing_pool.size()) {
       cudaEvent_t e;
       FSX_CUDA(cudaEventCreate(&e));
@@ -320,8 +364,75 @@ struct Engine {
   // copy-engine all-to-all of channel `ch` (parity `par`): bytes[d] to rank d.
   // Self messages are already in place. Returns after enqueueing; `s` then
   // waits for every peer's message to this rank.
-  void a2a(int ch, int par, const std::vector<uint64_t>& bytes, cudaStream_t s) {
+  // Byte all-to-all of channel `ch` (parity `par`): bytes[d] to rank d; self
+  // messages are already in place. recv_bytes (NCCL only) = what each peer
+  // sends here. On the caller's compute stream the whole exchange is blocking
+  // main-lane communication and is timed as exposed (sim.cpp:25-35).
+  void a2a(int ch, int par, const std::vector<uint64_t>& bytes, cudaStream_t s,
+           const std::vector<uint64_t>* recv_bytes = nullptr) {
     if (p == 1) return;
+    cudaEvent_t t0 = nullptr;
+    if (s == cur_c) {
+      t0 = timing_event();
+      FSX_CUDA(cudaEventRecord(t0, s));
+    }
+    if (nccl) {
+      a2a_nccl(ch, par, bytes, recv_bytes, s);
+    } else {
+      a2a_ce(ch, par, bytes, s);
+    }
+    if (t0) {
+      cudaEvent_t t1 = timing_event();
+      FSX_CUDA(cudaEventRecord(t1, s));
+      waits.emplace_back(t0, t1);
+    }
+  }
+
+  void a2a_nccl(int ch, int par, const std::vector<uint64_t>& bytes,
+                const std::vector<uint64_t>* recv_bytes, cudaStream_t s) {
+    Span sp(this, FSX_PHASE_A2A, s);
+    NcclApi& N = NcclApi::get();
+    std::vector<uint64_t> rb_local;
+    if (!recv_bytes) {
+      // size round first (comm.cpp:328-341): every peer's 16-byte header
+      nccl_check(N.GroupStart(), "group start");
+      for (int k = 1; k < p; ++k) {
+        const int d = (me + k) % p;
+        nccl_check(N.Send(stage_slot(ch, par, d), kHdr, ncclChar, d, nccl, s), "send header");
+        nccl_check(N.Recv(recv_slot(ch, par, d), kHdr, ncclChar, d, nccl, s), "recv header");
+      }
+      nccl_check(N.GroupEnd(), "group end");
+      rb_local.assign(p, 0);
+      std::vector<uint64_t> hdr(2 * p);
+      for (int d = 0; d < p; ++d)
+        if (d != me) FSX_CUDA(cudaMemcpyAsync(&hdr[2 * d], recv_slot(ch, par, d), kHdr, cudaMemcpyDeviceToHost, s));
+      FSX_CUDA(cudaStreamSynchronize(s));
+      for (int d = 0; d < p; ++d)
+        if (d != me) rb_local[d] = hdr[2 * d] * elem_bytes(ch);
+      recv_bytes = &rb_local;
+      nccl_check(N.GroupStart(), "group start");
+      for (int k = 1; k < p; ++k) {
+        const int d = (me + k) % p;
+        if (bytes[d] > kHdr)
+          nccl_check(N.Send(stage_slot(ch, par, d) + kHdr, bytes[d] - kHdr, ncclChar, d, nccl, s), "send");
+        if ((*recv_bytes)[d])
+          nccl_check(N.Recv(recv_slot(ch, par, d) + kHdr, (*recv_bytes)[d], ncclChar, d, nccl, s), "recv");
+      }
+      nccl_check(N.GroupEnd(), "group end");
+      return;
+    }
+    nccl_check(N.GroupStart(), "group start");
+    for (int k = 1; k < p; ++k) {
+      const int d = (me + k) % p;
+      if (bytes[d]) nccl_check(N.Send(stage_slot(ch, par, d), bytes[d], ncclChar, d, nccl, s), "send");
+      if ((*recv_bytes)[d]) nccl_check(N.Recv(recv_slot(ch, par, d), (*recv_bytes)[d], ncclChar, d, nccl, s), "recv");
+    }
+    nccl_check(N.GroupEnd(), "group end");
+  }
+  // payload bytes per counted element of a channel (after the header)
+  uint64_t elem_bytes(int ch) const { return ch == CH_IDS ? 8 : ch == CH_MASK ? 1 : ch == CH_IDX ? 4 : rb; }
+
+  void a2a_ce(int ch, int par, const std::vector<uint64_t>& bytes, cudaStream_t s) {
     const uint32_t v = seq[ch];
     if (debug)
       std::fprintf(stderr, "[fsx r%d] a2a ch=%d seq=%u par=%d stream=%s\n", me, ch, v, par,
@@ -436,9 +547,12 @@ struct Engine {
     launch_copy_rows(ctx, lm, o.m_cap, o.srt.d_n(), rb, s);
     FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, o.cnt.p + 2, 1, cap, ctx->d_err);
     if (p > 1) {
-      std::vector<uint64_t> bytes(p);
-      for (int d = 0; d < p; ++d) bytes[d] = kHdr + rb * o.h_recv[d];
-      a2a(CH_ROWS, par, bytes, s);
+      std::vector<uint64_t> bytes(p), rbytes(p);
+      for (int d = 0; d < p; ++d) {
+        bytes[d] = kHdr + rb * o.h_recv[d];
+        rbytes[d] = kHdr + rb * r.h_send[d];
+      }
+      a2a(CH_ROWS, par, bytes, s, &rbytes);
     }
     RequesterScatterMap sm{recv_slots(CH_ROWS, par), r.send_pos.p, r.send_dst.p, r.send_off(),
                            static_cast<char*>(d_out), rb};
@@ -455,9 +569,12 @@ struct Engine {
     launch_copy_rows(ctx, gm, r.n, nullptr, rb, s);
     FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, r.tot.p, 1, cap, ctx->d_err);
     if (p > 1) {
-      std::vector<uint64_t> bytes(p);
-      for (int d = 0; d < p; ++d) bytes[d] = kHdr + rb * r.h_send[d];
-      a2a(CH_GRADS, par, bytes, s);
+      std::vector<uint64_t> bytes(p), rbytes(p);
+      for (int d = 0; d < p; ++d) {
+        bytes[d] = kHdr + rb * r.h_send[d];
+        rbytes[d] = kHdr + rb * o.h_recv[d];
+      }
+      a2a(CH_GRADS, par, bytes, s, &rbytes);
     }
     update(o, CH_GRADS, par, nullptr, 0, false, s);
   }
@@ -786,6 +903,7 @@ struct Engine {
     cudaDeviceSynchronize();
     for (int d = 0; d < kMaxRanks; ++d)
       if (peer[d].ipc && peer[d].base) cudaIpcCloseMemHandle(peer[d].base);
+    if (nccl) NcclApi::get().CommDestroy(nccl);
     for (auto e : ev_pool) cudaEventDestroy(e);
     for (auto e : timing_pool) cudaEventDestroy(e);
     for (auto e : prof_pool) cudaEventDestroy(e);
@@ -823,8 +941,10 @@ int fsx_engine_create(fsx_ctx* ctx, fsx_table* table, const fsx_engine_config* c
   DeviceGuard dg(ctx->device);
   if (!cfg || (cfg->mode != FSX_MODE_SYNC && cfg->mode != FSX_MODE_PRIO))
     raise(FSX_ERR_INVALID_ARGUMENT, "fsx: bad engine mode");
-  if (cfg->transport != FSX_TRANSPORT_CE)
-    raise(FSX_ERR_CONFIG, "fsx: only the copy-engine transport is built into this engine");
+  if (cfg->transport != FSX_TRANSPORT_CE && cfg->transport != FSX_TRANSPORT_NCCL)
+    raise(FSX_ERR_CONFIG, "fsx: unknown transport");
+  if (cfg->transport == FSX_TRANSPORT_NCCL && cfg->mode != FSX_MODE_SYNC)
+    raise(FSX_ERR_CONFIG, "fsx: the NCCL transport is the blocking baseline (synchronized mode only)");
   if (table->g.p != ctx->world || table->g.shard != ctx->rank)
     raise(FSX_ERR_INVALID_ARGUMENT, "fsx: table shard does not match the context rank/world");
   if (ctx->world > kMaxRanks) raise(FSX_ERR_INVALID_ARGUMENT, "fsx: at most 16 ranks");
@@ -945,13 +1065,24 @@ int fsx_engine_connect_ipc(fsx_engine* e, int peer, const void* blob, uint64_t l
   FSX_API_END
 }
 
-int fsx_nccl_unique_id(void*) {
-  capi_set_error("fsx: NCCL baseline transport not built");
-  return FSX_ERR_CONFIG;
+int fsx_nccl_unique_id(void* id128) {
+  FSX_API_BEGIN
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  nccl_check(NcclApi::get().GetUniqueId(&id), "get unique id");
+  std::memcpy(id128, &id, 128);
+  FSX_API_END
 }
-int fsx_engine_connect_nccl(fsx_engine*, const void*) {
-  capi_set_error("fsx: NCCL baseline transport not built");
-  return FSX_ERR_CONFIG;
+
+int fsx_engine_connect_nccl(fsx_engine* e, const void* id128) {
+  FSX_API_BEGIN
+  DeviceGuard dg(e->ctx->device);
+  if (e->cfg.transport != FSX_TRANSPORT_NCCL)
+    raise(FSX_ERR_CONFIG, "fsx: engine was not created for the NCCL transport");
+  ncclUniqueId id;
+  std::memcpy(&id, id128, 128);
+  nccl_check(NcclApi::get().CommInitRank(&e->nccl, e->p, id, e->me), "comm init");
+  FSX_API_END
 }
 
 int fsx_engine_forward(fsx_engine* e, const uint64_t* d_ids_cur, uint64_t n_cur,
@@ -959,8 +1090,6 @@ int fsx_engine_forward(fsx_engine* e, const uint64_t* d_ids_cur, uint64_t n_cur,
   FSX_API_BEGIN
   DeviceGuard dg(e->ctx->device);
   e->cur_c = S(stream);
-  e->waits.clear();
-  e->timing_next = 0;
   if (e->cfg.mode == FSX_MODE_SYNC)
     e->sync_forward(d_ids_cur, n_cur, d_out, S(stream));
   else
@@ -1006,6 +1135,8 @@ int fsx_engine_exposed_ms(fsx_engine* e, double* ms) {
     total += x;
   }
   *ms = total;
+  e->waits.clear();
+  e->timing_next = 0;
   FSX_API_END
 }
 

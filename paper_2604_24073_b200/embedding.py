@@ -290,7 +290,7 @@ class _Engine:
     _mode = _lib.FSX_MODE_SYNC
 
     def __init__(self, shard: ShardView, comm=None, max_occurrences: int = 1 << 16,
-                 reduce_chunk: int = 0):
+                 reduce_chunk: int = 0, transport: str = "ce"):
         from .comm import DeviceFabric
         self.shard = shard
         if comm is None:
@@ -298,13 +298,18 @@ class _Engine:
         self.comm = comm
         if comm.world_size() != shard.geom.num_shards or comm.rank() != shard.shard_id:
             raise InvalidArgument("embedding: shard geometry does not match the communicator")
-        cfg = _lib.EngineConfig(self._mode, _lib.FSX_TRANSPORT_CE, max_occurrences, reduce_chunk)
+        tr = {"ce": _lib.FSX_TRANSPORT_CE, "nccl": _lib.FSX_TRANSPORT_NCCL}[transport]
+        cfg = _lib.EngineConfig(self._mode, tr, max_occurrences, reduce_chunk)
         h = C.c_void_p()
         _lib.call("fsx_engine_create", shard.ctx.h, shard.h, C.byref(cfg), C.byref(h))
         self.h = h
+        self.transport = transport
         self.max_occurrences = max_occurrences
         self._n_cur = None
-        comm.connect(h)
+        if transport == "nccl":
+            comm.connect_nccl(h)
+        else:
+            comm.connect(h)
 
     def _ids(self, ids) -> torch.Tensor:
         return _dev_u64(ids, self.shard.ctx.torch_device)
