@@ -1168,4 +1168,45 @@ int fsx_engine_phase_ms(fsx_engine* e, int phase, double* total_ms, uint64_t* co
 
 uint64_t fsx_engine_slot_bytes(const fsx_engine* e) { return e ? e->ch_slot[CH_GRADS] - kHdr : 0; }
 
+// Byte all-to-all over the engine's GRADS channel (comm.cpp:308-365 shape:
+// size round, then payloads); collective, between iterations only.
+int fsx_a2a_ce(fsx_engine* e, const void* d_send, const uint64_t* h_send_offsets,
+               const uint64_t* h_send_bytes, void* d_recv, uint64_t slot_bytes, uint64_t* h_recv_bytes,
+               void* stream) {
+  FSX_API_BEGIN
+  DeviceGuard dg(e->ctx->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint64_t cap = e->ch_slot[CH_GRADS] - kHdr;
+  const int p = e->p;
+  for (int d = 0; d < p; ++d)
+    if (h_send_bytes[d] > cap || h_send_bytes[d] > slot_bytes)
+      raise(FSX_ERR_COLLECTIVE, "all_to_all: payload of " + std::to_string(h_send_bytes[d]) +
+                                    " bytes exceeds the slot capacity");
+  const int par = e->next_par(CH_GRADS);
+  std::vector<uint64_t> bytes(p);
+  for (int d = 0; d < p; ++d) {
+    char* slot = e->stage_slot(CH_GRADS, par, d);
+    const uint64_t hdr[2] = {h_send_bytes[d], 0};
+    FSX_CUDA(cudaMemcpyAsync(slot, hdr, kHdr, cudaMemcpyHostToDevice, s));
+    if (h_send_bytes[d])
+      FSX_CUDA(cudaMemcpyAsync(slot + kHdr, static_cast<const char*>(d_send) + h_send_offsets[d],
+                               h_send_bytes[d], cudaMemcpyDeviceToDevice, s));
+    bytes[d] = kHdr + h_send_bytes[d];
+  }
+  FSX_CUDA(cudaStreamSynchronize(s));  // host headers above are stack memory
+  e->a2a(CH_GRADS, par, bytes, s);
+  std::vector<uint64_t> hdr(2 * p);
+  for (int d = 0; d < p; ++d)
+    FSX_CUDA(cudaMemcpyAsync(&hdr[2 * d], e->recv_slot(CH_GRADS, par, d), kHdr, cudaMemcpyDeviceToHost, s));
+  FSX_CUDA(cudaStreamSynchronize(s));
+  for (int d = 0; d < p; ++d) {
+    h_recv_bytes[d] = hdr[2 * d];
+    if (hdr[2 * d])
+      FSX_CUDA(cudaMemcpyAsync(static_cast<char*>(d_recv) + d * slot_bytes, e->recv_slot(CH_GRADS, par, d) + kHdr,
+                               hdr[2 * d], cudaMemcpyDeviceToDevice, s));
+  }
+  FSX_CUDA(cudaStreamSynchronize(s));
+  FSX_API_END
+}
+
 }  // extern "C"
