@@ -64,7 +64,8 @@ struct RouteOp {
 #pragma unroll
     for (int q = 0; q < NC; ++q) c[q] = (q == o && id < total_rows) ? 1u : 0u;
   }
-  __device__ void emit(uint64_t i, const uint32_t (&ex)[NC], const uint32_t (&c)[NC]) const {
+  __device__ void emit(uint64_t i, const uint32_t (&ex)[NC], const uint32_t (&c)[NC],
+                       const uint32_t (&tot)[NC]) const {
     const uint64_t id = ids[i];
     if (id >= total_rows) {
       report(err, kErrRowRange, id, total_rows);
@@ -72,7 +73,7 @@ struct RouteOp {
     }
     const int o = static_cast<int>(id % static_cast<uint64_t>(p));
     uint64_t base = 0;
-    for (int q = 0; q < o; ++q) base += totals[q];
+    for (int q = 0; q < o; ++q) base += tot[q];
     uint32_t r = 0;
 #pragma unroll
     for (int q = 0; q < NC; ++q)
@@ -161,7 +162,8 @@ struct OwnerPackOp {
       c[2 * q + 1] = has & f;
     }
   }
-  __device__ void emit(uint64_t u, const uint32_t (&ex)[NC], const uint32_t (&c)[NC]) const {
+  __device__ void emit(uint64_t u, const uint32_t (&ex)[NC], const uint32_t (&c)[NC],
+                       const uint32_t (&tot)[NC]) const {
     const uint32_t b = bits[u];
     const uint32_t f = co[u] ? 1u : 0u;
     uint64_t base_ex = 0, base_co = 0;
@@ -173,8 +175,8 @@ struct OwnerPackOp {
         else ex_list[base_ex + e.rank] = e;
         rank_us[u * kMaxRanks + q] = e.rank;
       }
-      base_ex += totals[2 * q];
-      base_co += totals[2 * q + 1];
+      base_ex += tot[2 * q];
+      base_co += tot[2 * q + 1];
     }
   }
 };
@@ -227,7 +229,8 @@ struct OccRankOp {
 #pragma unroll
     for (int q = 0; q < NC; ++q) c[q] = (q == 2 * s + static_cast<int>(f)) ? 1u : 0u;
   }
-  __device__ void emit(uint64_t j, const uint32_t (&ex)[NC], const uint32_t (&c)[NC]) const {
+  __device__ void emit(uint64_t j, const uint32_t (&ex)[NC], const uint32_t (&c)[NC],
+                       const uint32_t (&tot)[NC]) const {
     const int s = occ_src[j];
     const uint32_t f = co ? (co[inverse[j]] ? 1u : 0u) : 0u;
     uint32_t r = 0;
@@ -266,7 +269,8 @@ struct SplitOp {
 #pragma unroll
     for (int q = 0; q < NC; ++q) c[q] = (q == 2 * d + static_cast<int>(fl)) ? 1u : 0u;
   }
-  __device__ void emit(uint64_t k, const uint32_t (&ex)[NC], const uint32_t (&c)[NC]) const {
+  __device__ void emit(uint64_t k, const uint32_t (&ex)[NC], const uint32_t (&c)[NC],
+                       const uint32_t (&tot)[NC]) const {
     const int d = send_dst[k];
     const uint32_t fl = f(k);
     uint32_t r = 0;

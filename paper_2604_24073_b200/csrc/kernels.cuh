@@ -171,7 +171,8 @@ struct UniqueOp {
   __device__ void count(uint64_t k, uint32_t (&c)[1]) const {
     c[0] = (k == 0 || keys[k] != keys[k - 1]) ? 1u : 0u;
   }
-  __device__ void emit(uint64_t k, const uint32_t (&ex)[1], const uint32_t (&c)[1]) const {
+  __device__ void emit(uint64_t k, const uint32_t (&ex)[1], const uint32_t (&c)[1],
+                       const uint32_t (&tot)[1]) const {
     const uint32_t slot = ex[0] + c[0] - 1;
     if (c[0]) {
       const uint64_t key = static_cast<uint64_t>(keys[k]);
@@ -202,7 +203,8 @@ struct OwnerPartitionOp {
 #pragma unroll
     for (int q = 0; q < NC; ++q) c[q] = (q == o && id < total_rows) ? 1u : 0u;
   }
-  __device__ void emit(uint64_t i, const uint32_t (&ex)[NC], const uint32_t (&c)[NC]) const {
+  __device__ void emit(uint64_t i, const uint32_t (&ex)[NC], const uint32_t (&c)[NC],
+                       const uint32_t (&tot)[NC]) const {
     const uint64_t id = ids[i];
     if (id >= total_rows) {
       report(err, kErrRowRange, id, total_rows);
@@ -210,7 +212,7 @@ struct OwnerPartitionOp {
     }
     const int o = static_cast<int>(id % static_cast<uint64_t>(p));
     uint64_t base = 0;
-    for (int q = 0; q < o; ++q) base += totals[q];
+    for (int q = 0; q < o; ++q) base += tot[q];
     uint32_t r = 0;
 #pragma unroll
     for (int q = 0; q < NC; ++q)
@@ -238,7 +240,8 @@ struct SplitByFlagOp {
     c[0] = f;
     c[1] = 1u - f;
   }
-  __device__ void emit(uint64_t i, const uint32_t (&ex)[2], const uint32_t (&c)[2]) const {
+  __device__ void emit(uint64_t i, const uint32_t (&ex)[2], const uint32_t (&c)[2],
+                       const uint32_t (&tot)[2]) const {
     if (c[0]) {
       if (out_true) out_true[ex[0]] = v[i];
     } else if (out_false) {
@@ -302,7 +305,8 @@ struct SgdPlanOp {
     c[1] = k > 1 ? 1u : 0u;
     c[2] = k > 1 ? k : 0u;
   }
-  __device__ void emit(uint64_t u, const uint32_t (&ex)[3], const uint32_t (&c)[3]) const {
+  __device__ void emit(uint64_t u, const uint32_t (&ex)[3], const uint32_t (&c)[3],
+                       const uint32_t (&tot)[3]) const {
     for (uint32_t q = 0; q < c[0]; ++q) work[ex[0] + q] = make_uint2(static_cast<uint32_t>(u), q);
     if (c[1]) {
       multi[ex[1]] = static_cast<uint32_t>(u);
@@ -355,13 +359,15 @@ __device__ __forceinline__ void sgd_apply_vec(const SgdArgs<T>& a, uint32_t u, u
   if (bad) report(a.err, kErrNonFinite, l * static_cast<uint64_t>(a.g.p) + a.g.shard, 0);
 }
 
-// One warp per work item (a row, or one `chunk`-occurrence slice of a hot
-// row). Each lane owns NV vectors of VE consecutive elements (16-byte loads
-// when the row pitch allows), so one pass covers 32*VE*NV columns; the
-// occurrence loop is unrolled 4-wide with all loads issued before the
+// One warp per (work item, column block): a work item is a row, or one
+// `chunk`-occurrence slice of a hot row; blockIdx.y picks the 32*VE*NV-column
+// block (16-byte loads when the row pitch allows). Splitting columns across
+// warps keeps per-warp registers small, so more warps (and more independent
+// 16-byte loads) are in flight to hide the index -> gradient latency chain.
+// The occurrence loop is unrolled 4-wide with all loads issued before the
 // in-order f64 adds.
 template <class T, int VE, int NV>
-__global__ void __launch_bounds__(128, 6) k_sgd_chunks(SgdArgs<T> a) {
+__global__ void __launch_bounds__(128, 8) k_sgd_chunks(SgdArgs<T> a) {
   using V = VecOf<T, VE>;
   constexpr int COLS = 32 * VE * NV;
   const uint64_t nwork = *a.d_work_n;
@@ -369,6 +375,7 @@ __global__ void __launch_bounds__(128, 6) k_sgd_chunks(SgdArgs<T> a) {
   const uint64_t wid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const unsigned lane = threadIdx.x & 31u;
   const uint32_t dim = a.g.dim;
+  const uint32_t c0 = blockIdx.y * COLS;
   for (uint64_t w = wid; w < nwork; w += warps) {
     const uint2 item = a.work[w];
     const uint32_t u = item.x;
@@ -376,7 +383,7 @@ __global__ void __launch_bounds__(128, 6) k_sgd_chunks(SgdArgs<T> a) {
     const bool single = a.chunk == 0 || e - s <= a.chunk;
     const uint32_t kb = single ? s : s + item.y * a.chunk;
     const uint32_t ke = single ? e : min(e, kb + a.chunk);
-    for (uint32_t c0 = 0; c0 < dim; c0 += COLS) {
+    {
       double acc[NV][VE];
 #pragma unroll
       for (int v = 0; v < NV; ++v)
@@ -388,10 +395,10 @@ __global__ void __launch_bounds__(128, 6) k_sgd_chunks(SgdArgs<T> a) {
         const uint32_t cnt = min(32u, ke - kb2);
         const T* mine = lane < cnt ? a.gr.row(a.rs.perm[kb2 + lane]) : nullptr;
         uint32_t q0 = 0;
-        for (; q0 + 2 <= cnt; q0 += 2) {
-          V g[2][NV];
+        for (; q0 + 4 <= cnt; q0 += 4) {
+          V g[4][NV];
 #pragma unroll
-          for (int q = 0; q < 2; ++q) {
+          for (int q = 0; q < 4; ++q) {
             const T* row = reinterpret_cast<const T*>(
                 __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(mine), q0 + q));
 #pragma unroll
@@ -401,7 +408,7 @@ __global__ void __launch_bounds__(128, 6) k_sgd_chunks(SgdArgs<T> a) {
             }
           }
 #pragma unroll
-          for (int q = 0; q < 2; ++q)
+          for (int q = 0; q < 4; ++q)
 #pragma unroll
             for (int v = 0; v < NV; ++v)
 #pragma unroll

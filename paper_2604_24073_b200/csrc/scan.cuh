@@ -5,10 +5,13 @@
 // pack lists, co/ex gradient splits. One primitive covers them all: an Op gives
 // each item a small vector of NC counts; the primitive computes, for every
 // item, the exclusive prefix of those vectors over the item order and calls
-// Op::emit with it. Three launches, no host round trip, no spin waits:
+// Op::emit with it (and the grand totals). Two launches, no host round trip,
+// no spin waits:
 //   1. k_tile_reduce : per-tile sums            (one CTA per 2048-item tile)
-//   2. k_scan_tiles  : exclusive scan of tile sums + grand totals (one CTA)
-//   3. k_tile_emit   : re-count, block scan (warp shuffles), emit
+//   2. k_tile_emit   : every CTA sums the tile sums before it (its prefix) and
+//                      all of them (the grand totals, CTA 0 also stores them)
+//                      from L2, then re-counts, block-scans (warp shuffles),
+//                      and emits
 // Item counts may live on the device (d_n); grids are sized by capacity and
 // tiles beyond *d_n exit early, so chains of these never need a host sync.
 #pragma once
@@ -144,16 +147,55 @@ static __global__ void __launch_bounds__(1024) k_scan_tiles(uint32_t* tile_sums,
 
 template <class Op>
 static __global__ void __launch_bounds__(kScanThreads) k_tile_emit(Op op, uint64_t n_cap,
-                                                            const uint64_t* d_n,
-                                                            const uint32_t* tile_prefix) {
+                                                                   const uint64_t* d_n,
+                                                                   const uint32_t* tile_sums,
+                                                                   unsigned tiles,
+                                                                   uint64_t* d_totals) {
   constexpr int NC = Op::NC;
+  __shared__ uint32_t s_pre[NC], s_tot[NC];
   const uint64_t n = scan_n(n_cap, d_n);
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile;
-  if (base >= n) return;  // whole CTA exits together: no barrier hazard
-  const uint64_t first = base + static_cast<uint64_t>(threadIdx.x) * kScanIPT;
-  uint32_t run[NC];
+  if (base >= n && blockIdx.x != 0) return;  // whole CTA exits together
+  // prefix of this tile and grand totals, straight from the tile sums (L2)
+  {
+    uint32_t pre[NC], all[NC];
 #pragma unroll
-  for (int c = 0; c < NC; ++c) run[c] = 0;
+    for (int c = 0; c < NC; ++c) pre[c] = all[c] = 0;
+    for (unsigned t = threadIdx.x; t < tiles; t += blockDim.x)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const uint32_t x = tile_sums[static_cast<uint64_t>(t) * NC + c];
+        all[c] += x;
+        pre[c] += t < blockIdx.x ? x : 0u;
+      }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        pre[c] += __shfl_xor_sync(0xffffffffu, pre[c], o);
+        all[c] += __shfl_xor_sync(0xffffffffu, all[c], o);
+      }
+    }
+    __shared__ uint32_t w_pre[kScanThreads / 32][NC], w_all[kScanThreads / 32][NC];
+    const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    if (lane == 0)
+#pragma unroll
+      for (int c = 0; c < NC; ++c) { w_pre[warp][c] = pre[c]; w_all[warp][c] = all[c]; }
+    __syncthreads();
+    if (threadIdx.x < NC) {
+      uint32_t p = 0, a = 0;
+      for (int w = 0; w < kScanThreads / 32; ++w) { p += w_pre[w][threadIdx.x]; a += w_all[w][threadIdx.x]; }
+      s_pre[threadIdx.x] = p;
+      s_tot[threadIdx.x] = a;
+      if (blockIdx.x == 0 && d_totals) d_totals[threadIdx.x] = a;
+    }
+    __syncthreads();
+  }
+  if (base >= n) return;  // CTA 0 of an empty input: totals stored, nothing to emit
+  const uint64_t first = base + static_cast<uint64_t>(threadIdx.x) * kScanIPT;
+  uint32_t run[NC], tot[NC];
+#pragma unroll
+  for (int c = 0; c < NC; ++c) { run[c] = 0; tot[c] = s_tot[c]; }
 #pragma unroll
   for (int q = 0; q < kScanIPT; ++q) {
     const uint64_t i = first + q;
@@ -167,14 +209,14 @@ static __global__ void __launch_bounds__(kScanThreads) k_tile_emit(Op op, uint64
   uint32_t total[NC];
   block_exclusive_scan<NC>(run, total);
 #pragma unroll
-  for (int c = 0; c < NC; ++c) run[c] += tile_prefix[static_cast<uint64_t>(blockIdx.x) * NC + c];
+  for (int c = 0; c < NC; ++c) run[c] += s_pre[c];
 #pragma unroll
   for (int q = 0; q < kScanIPT; ++q) {
     const uint64_t i = first + q;
     if (i < n) {
       uint32_t cnt[NC];
       op.count(i, cnt);
-      op.emit(i, run, cnt);
+      op.emit(i, run, cnt, tot);
 #pragma unroll
       for (int c = 0; c < NC; ++c) run[c] += cnt[c];
     }
@@ -202,8 +244,8 @@ void run_scan(Ctx* ctx, const Op& op, uint64_t n_cap, const uint64_t* d_n, ScanS
   s.ensure(n_cap, NC);
   const unsigned tiles = ceil_div(n_cap, kScanTile);
   FSX_LAUNCH(ctx, k_tile_reduce<Op>, tiles, kScanThreads, 0, stream, op, n_cap, d_n, s.tiles.p);
-  FSX_LAUNCH(ctx, k_scan_tiles<NC>, 1, 1024, 0, stream, s.tiles.p, tiles, d_totals);
-  FSX_LAUNCH(ctx, k_tile_emit<Op>, tiles, kScanThreads, 0, stream, op, n_cap, d_n, s.tiles.p);
+  FSX_LAUNCH(ctx, k_tile_emit<Op>, tiles, kScanThreads, 0, stream, op, n_cap, d_n, s.tiles.p, tiles,
+             d_totals);
 }
 
 }  // namespace fsx

@@ -58,21 +58,17 @@ void sgd_update_rows(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_ca
   SgdArgs<T> a{static_cast<T*>(t.values), t.g, t.lr, rs, gr, chunk, s.work.p, s.d_tot.p,
                s.multi.p, s.d_tot.p + 1, s.part_base.p, s.partials.p, rows_out, ctx->d_err};
   const uint64_t work_cap = rows_cap + (chunk ? occ_cap / chunk + 1 : 0);
-  const unsigned g1 = grid_for(ctx, work_cap, 4, 16), g2 = grid_for(ctx, rows_cap, 1, 8);
+  const unsigned g2 = grid_for(ctx, rows_cap, 1, 8);
   const uint32_t rb = t.row_bytes();
   constexpr int VE16 = static_cast<int>(16 / sizeof(T));
-  if (rb % 16 == 0) {
-    // 16-byte vectors; NV vectors per lane per pass
-    const uint32_t per_pass = 32 * VE16;
-    if (t.g.dim <= per_pass)
-      FSX_LAUNCH(ctx, (k_sgd_chunks<T, VE16, 1>), g1, 128, 0, stream, a);
-    else if (t.g.dim <= 2 * per_pass)
-      FSX_LAUNCH(ctx, (k_sgd_chunks<T, VE16, 2>), g1, 128, 0, stream, a);
-    else
-      FSX_LAUNCH(ctx, (k_sgd_chunks<T, VE16, 4>), g1, 128, 0, stream, a);
-  } else {
-    FSX_LAUNCH(ctx, (k_sgd_chunks<T, 1, 4>), g1, 128, 0, stream, a);
-  }
+  const int ve = rb % 16 == 0 ? VE16 : 1;
+  const unsigned cols = 32u * static_cast<unsigned>(ve);  // NV = 1: one vector per lane per block
+  const unsigned ycols = (t.g.dim + cols - 1) / cols;
+  dim3 g1(grid_for(ctx, work_cap, 4, 16 / (ycols < 4 ? ycols : 4)), ycols);
+  if (ve == VE16)
+    FSX_LAUNCH(ctx, (k_sgd_chunks<T, VE16, 1>), g1, 128, 0, stream, a);
+  else
+    FSX_LAUNCH(ctx, (k_sgd_chunks<T, 1, 1>), g1, 128, 0, stream, a);
   if (chunk) {
     if (t.g.dim % 2 == 0)
       FSX_LAUNCH(ctx, (k_sgd_combine<T, 2>), g2, 128, 0, stream, a);
