@@ -1,4 +1,5 @@
-// Stable LSD radix sort of (key, u32 payload) pairs, 8-bit digits.
+// Stable LSD radix sort of (key, u32 payload) pairs, up-to-9-bit digits
+// (passes = ceil(nbits / 9); 27-bit row keys sort in 3 passes).
 //
 // Per digit pass, three launches:
 //   k_radix_hist    per-2048-key tile digit histogram; equal digits inside a
@@ -24,38 +25,45 @@ namespace fsx {
 
 constexpr int kRadixThreads = 256;
 constexpr int kRadixWarps = kRadixThreads / 32;
-constexpr int kRadixWarpItems = 256;  // per warp per tile
+constexpr int kRadixWarpItems = 128;  // per warp per tile (1024-key tiles: >= 1 CTA per SM at 150K keys)
 constexpr int kRadixTile = kRadixWarps * kRadixWarpItems;
 constexpr int kRadixRounds = kRadixWarpItems / 32;
+constexpr int kRadixMaxBits = 9;
+constexpr int kRadixBins = 1 << kRadixMaxBits;  // 512
+constexpr int kBinsPerThread = kRadixBins / kRadixThreads;
 
 template <class K>
 __global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const K* __restrict__ keys,
                                                               uint64_t n_cap, const uint64_t* d_n,
-                                                              int shift, uint32_t* counts,
+                                                              int shift, unsigned mask, uint32_t* counts,
                                                               unsigned tiles) {
-  __shared__ uint32_t hist[256];
+  __shared__ uint32_t hist[kRadixBins];
   const uint64_t n = scan_n(n_cap, d_n);
-  hist[threadIdx.x] = 0;
+  for (int b = 0; b < kBinsPerThread; ++b) hist[threadIdx.x + b * kRadixThreads] = 0;
   __syncthreads();
   const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kRadixTile + warp * kRadixWarpItems;
 #pragma unroll 4
   for (int r = 0; r < kRadixRounds; ++r) {
     const uint64_t i = base + r * 32 + lane;
-    const unsigned d = i < n ? static_cast<unsigned>((keys[i] >> shift) & 0xffu) : 256u;
+    const unsigned d = i < n ? static_cast<unsigned>((keys[i] >> shift) & mask) : 0xffffu;
     const unsigned peers = __match_any_sync(0xffffffffu, d);
-    if (d < 256u && (peers & lanemask_lt()) == 0) atomicAdd(&hist[d], __popc(peers));
+    if (d <= mask && (peers & lanemask_lt()) == 0) atomicAdd(&hist[d], __popc(peers));
   }
   __syncthreads();
-  counts[static_cast<uint64_t>(threadIdx.x) * tiles + blockIdx.x] = hist[threadIdx.x];
+  for (int b = 0; b < kBinsPerThread; ++b) {
+    const unsigned d = threadIdx.x + b * kRadixThreads;
+    if (d <= mask) counts[static_cast<uint64_t>(d) * tiles + blockIdx.x] = hist[d];
+  }
 }
 
 // one warp per digit: exclusive scan of counts[d][0..tiles) in place, total[d]
 static __global__ void __launch_bounds__(256) k_radix_rows(uint32_t* __restrict__ counts,
-                                                           unsigned tiles, uint32_t* __restrict__ total) {
+                                                           unsigned tiles, unsigned bins,
+                                                           uint32_t* __restrict__ total) {
   const unsigned lane = threadIdx.x & 31u;
   const unsigned d = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (d >= 256) return;
+  if (d >= bins) return;
   uint32_t* row = counts + static_cast<uint64_t>(d) * tiles;
   uint32_t carry = 0;
   for (unsigned t0 = 0; t0 < tiles; t0 += 32) {
@@ -76,20 +84,28 @@ static __global__ void __launch_bounds__(256) k_radix_rows(uint32_t* __restrict_
 template <class K>
 __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(
     const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
-    uint32_t* __restrict__ vout, uint64_t n_cap, const uint64_t* d_n, int shift,
+    uint32_t* __restrict__ vout, uint64_t n_cap, const uint64_t* d_n, int shift, unsigned mask,
     const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ digit_total, unsigned tiles) {
-  __shared__ uint32_t wcount[kRadixWarps][256];
-  __shared__ uint32_t tile_off[256];
+  __shared__ uint32_t wcount[kRadixWarps][kRadixBins];
+  __shared__ uint32_t tile_off[kRadixBins];
   __shared__ uint32_t wsum[kRadixWarps];
   const uint64_t n = scan_n(n_cap, d_n);
   const uint64_t tile_base = static_cast<uint64_t>(blockIdx.x) * kRadixTile;
   if (tile_base >= n) return;
   const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
-  for (int w = 0; w < kRadixWarps; ++w) wcount[w][threadIdx.x] = 0;
+  const unsigned bins = mask + 1;
+  for (int w = 0; w < kRadixWarps; ++w)
+    for (int b = 0; b < kBinsPerThread; ++b) wcount[w][threadIdx.x + b * kRadixThreads] = 0;
   {
-    // digit base = exclusive scan of the digit totals (256 threads, 1 each)
-    const uint32_t tot = digit_total[threadIdx.x];
-    uint32_t x = tot;
+    // digit base = exclusive scan of the digit totals; each thread owns
+    // kBinsPerThread consecutive digits
+    uint32_t tot[kBinsPerThread], own = 0;
+    for (int b = 0; b < kBinsPerThread; ++b) {
+      const unsigned d = threadIdx.x * kBinsPerThread + b;
+      tot[b] = d < bins ? digit_total[d] : 0u;
+      own += tot[b];
+    }
+    uint32_t x = own;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
@@ -97,9 +113,13 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(
     }
     if (lane == 31) wsum[warp] = x;
     __syncthreads();
-    uint32_t before = 0;
-    for (unsigned w = 0; w < warp; ++w) before += wsum[w];
-    tile_off[threadIdx.x] = before + x - tot + offsets[static_cast<uint64_t>(threadIdx.x) * tiles + blockIdx.x];
+    uint32_t run = x - own;
+    for (unsigned w = 0; w < warp; ++w) run += wsum[w];
+    for (int b = 0; b < kBinsPerThread; ++b) {
+      const unsigned d = threadIdx.x * kBinsPerThread + b;
+      if (d < bins) tile_off[d] = run + offsets[static_cast<uint64_t>(d) * tiles + blockIdx.x];
+      run += tot[b];
+    }
   }
   __syncthreads();
   const uint64_t base = tile_base + warp * kRadixWarpItems;
@@ -112,25 +132,26 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(
     const bool valid = i < n;
     k[r] = valid ? kin[i] : K(0);
     v[r] = valid ? (vin ? vin[i] : static_cast<uint32_t>(i)) : 0u;
-    dg[r] = valid ? static_cast<unsigned>((k[r] >> shift) & 0xffu) : 256u;
+    dg[r] = valid ? static_cast<unsigned>((k[r] >> shift) & mask) : 0xffffu;
   }
 #pragma unroll
   for (int r = 0; r < kRadixRounds; ++r) {
     const unsigned d = dg[r];
     const unsigned peers = __match_any_sync(0xffffffffu, d);
     const unsigned before = __popc(peers & lanemask_lt());
-    uint32_t run = d < 256u ? wcount[warp][d] : 0u;
+    uint32_t run = d <= mask ? wcount[warp][d] : 0u;
     rk[r] = run + before;
     __syncwarp();
-    if (d < 256u && before == 0) wcount[warp][d] = run + __popc(peers);
+    if (d <= mask && before == 0) wcount[warp][d] = run + __popc(peers);
     __syncwarp();
   }
   __syncthreads();
-  {
+  for (int b = 0; b < kBinsPerThread; ++b) {
+    const unsigned d = threadIdx.x + b * kRadixThreads;
     uint32_t run = 0;
     for (int w = 0; w < kRadixWarps; ++w) {
-      uint32_t x = wcount[w][threadIdx.x];
-      wcount[w][threadIdx.x] = run;
+      const uint32_t x = wcount[w][d];
+      wcount[w][d] = run;
       run += x;
     }
   }
@@ -138,7 +159,7 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(
 #pragma unroll
   for (int r = 0; r < kRadixRounds; ++r) {
     const unsigned d = dg[r];
-    if (d < 256u) {
+    if (d <= mask) {
       const uint32_t pos = tile_off[d] + wcount[warp][d] + rk[r];
       kout[pos] = k[r];
       vout[pos] = v[r];
@@ -159,10 +180,12 @@ void radix_sort_pairs(Ctx* ctx, K* k0, uint32_t* v0, K* k1, uint32_t* v1, uint64
                       const uint64_t* d_n, int nbits, RadixScratch& s, cudaStream_t stream,
                       K** k_out, uint32_t** v_out, const uint32_t* v_init = nullptr) {
   if (nbits < 1) nbits = 1;
-  const int passes = (nbits + 7) / 8;
+  const int passes = (nbits + kRadixMaxBits - 1) / kRadixMaxBits;
+  const int dbits = (nbits + passes - 1) / passes;
+  const unsigned mask = (1u << dbits) - 1u, bins = mask + 1;
   const unsigned tiles = ceil_div(n_cap > 0 ? n_cap : 1, kRadixTile);
-  s.counts.ensure(static_cast<size_t>(tiles) * 256 + 256);
-  uint32_t* totals = s.counts.p + static_cast<size_t>(tiles) * 256;
+  s.counts.ensure(static_cast<size_t>(tiles) * kRadixBins + kRadixBins);
+  uint32_t* totals = s.counts.p + static_cast<size_t>(tiles) * kRadixBins;
   K* kin = k0;
   K* kout = k1;
   const uint32_t* vin = v_init;
@@ -174,12 +197,12 @@ void radix_sort_pairs(Ctx* ctx, K* k0, uint32_t* v0, K* k1, uint32_t* v1, uint64
     return;
   }
   for (int p = 0; p < passes; ++p) {
-    const int shift = 8 * p;
-    FSX_LAUNCH(ctx, k_radix_hist<K>, tiles, kRadixThreads, 0, stream, kin, n_cap, d_n, shift,
+    const int shift = dbits * p;
+    FSX_LAUNCH(ctx, k_radix_hist<K>, tiles, kRadixThreads, 0, stream, kin, n_cap, d_n, shift, mask,
                s.counts.p, tiles);
-    FSX_LAUNCH(ctx, k_radix_rows, 32, 256, 0, stream, s.counts.p, tiles, totals);
+    FSX_LAUNCH(ctx, k_radix_rows, ceil_div(bins, 8), 256, 0, stream, s.counts.p, tiles, bins, totals);
     FSX_LAUNCH(ctx, k_radix_scatter<K>, tiles, kRadixThreads, 0, stream, kin, vin, kout, vout,
-               n_cap, d_n, shift, s.counts.p, totals, tiles);
+               n_cap, d_n, shift, mask, s.counts.p, totals, tiles);
     // next pass reads what this one wrote
     K* kt = kin;
     kin = kout;

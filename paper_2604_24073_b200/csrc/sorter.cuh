@@ -52,7 +52,7 @@ struct SortedIds {
     if (!d_counts.p) d_counts.alloc(4);
     // every scratch buffer is sized up front: a lazy cudaMalloc/cudaFree in
     // the middle of a multi-rank iteration can serialize the device
-    radix.counts.ensure(static_cast<size_t>(ceil_div(cap, kRadixTile)) * 256 + 256);
+    radix.counts.ensure(static_cast<size_t>(ceil_div(cap, kRadixTile)) * kRadixBins + kRadixBins);
     scan.ensure(cap, 1);
   }
   void reserve64() {
