@@ -113,16 +113,22 @@ __global__ void k_count_flags(const uint8_t* f, const uint64_t* d_n, unsigned lo
 // IterationStats.blocking_bytes (embedding.cpp:498-593) in the reference's
 // accounting (8-byte values): collision grads sent + received, E_co
 // messages sent + received.
+// (single rank: E_co is a message to self carrying every collision row)
 __global__ void k_blocking_bytes(int p, uint64_t rb8, const uint64_t* split_tot,
                                  const uint64_t* occ_tot, const uint64_t* pack_tot, CSlots cor_recv,
-                                 int have_grads, int have_eco, uint64_t* out) {
+                                 const uint64_t* co_count, int have_grads, int have_eco, uint64_t* out) {
   if (threadIdx.x != 0) return;
   uint64_t b = 0;
   if (have_grads)
     for (int d = 0; d < p; ++d) b += rb8 * (split_tot[2 * d + 1] + occ_tot[2 * d + 1]);
-  if (have_eco)
-    for (int d = 0; d < p; ++d)
-      b += 8 + pack_tot[2 * d + 1] * (8 + rb8) + 8 + slot_n(cor_recv.p[d]) * (8 + rb8);
+  if (have_eco) {
+    if (p == 1) {
+      b += 2 * (8 + co_count[0] * (8 + rb8));
+    } else {
+      for (int d = 0; d < p; ++d)
+        b += 8 + pack_tot[2 * d + 1] * (8 + rb8) + 8 + slot_n(cor_recv.p[d]) * (8 + rb8);
+    }
+  }
   *out = b;
 }
 
@@ -592,6 +598,15 @@ struct Engine {
                reinterpret_cast<unsigned long long*>(oc.misc.p));
     oc.has_co = true;
     on.has_co = false;
+    if (p == 1) {
+      // single rank: every message would go to self, and self rows are
+      // merged straight from the table — no pack lists, no copies. The
+      // merge must still see the deferred exclusive update first.
+      wait(s, ev_ex_applied);
+      rn.ex_par = -1;
+      rn.idx_par = -1;
+      return;
+    }
     // pack lists over next's unique rows: ex -> E_ex now, co -> E_co later
     FSX_CUDA(cudaMemsetAsync(on.pack_tot(), 0, 32 * 8, s));
     if (nc2() == 8) {
@@ -605,14 +620,14 @@ struct Engine {
     Slots send = send_slots(CH_EX, par);
     FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, on.pack_tot(), 2, cap, ctx->d_err);
     IdRowPackMap pm{static_cast<const char*>(t->values), on.srt.uniq.p, on.srt.uniq_g.p, on.ex_list.p,
-                    send, on.pack_tot(), 0, rb};
+                    send, on.pack_tot(), 0, rb, me};
     FSX_LAUNCH(ctx, k_sum_pairs, 1, 32, 0, s, on.pack_tot(), p, on.misc.p + 2);
     wait(s, ev_ex_applied);  // rows of the previous exclusive set may be prefetched now
     {
       Span sp2(this, FSX_PHASE_PREFETCH, s);
       launch_copy_rows(ctx, pm, on.m_cap * static_cast<uint64_t>(p), on.misc.p + 2, rb, s);
     }
-    if (p > 1) {
+    {
       on.h_pack = fetch(on.pack_tot(), 2 * p, s);
       std::vector<uint64_t> bytes(p);
       for (int d = 0; d < p; ++d) bytes[d] = idrows_rows_off(on.h_pack[2 * d]) + rb * on.h_pack[2 * d];
@@ -624,14 +639,15 @@ struct Engine {
     Slots isend = send_slots(CH_IDX, ipar);
     FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, isend, p, on.cnt.p + 2, 1, cap, ctx->d_err);
     FSX_LAUNCH(ctx, k_idx_pack, grid_for(ctx, on.m_cap, 256, 8), 256, 0, s, on.srt.inverse.p, on.occ_src.p,
-               on.occ_idx.p, on.srt.d_n(), on.rank_us.p, on.co.p, isend);
-    if (p > 1) {
+               on.occ_idx.p, on.srt.d_n(), on.rank_us.p, on.co.p, isend, me);
+    {
       std::vector<uint64_t> bytes(p);
       for (int d = 0; d < p; ++d) bytes[d] = kHdr + 4 * on.h_recv[d];
       a2a(CH_IDX, ipar, bytes, s);
     }
     rn.idx_par = ipar;
   }
+
   // MASK messages for the current batch + requester flags + split plan
   // (embedding.cpp:392-408, 524-536)
   void masks_and_split(OwnBatch& oc, ReqBatch& rc, bool with_co, cudaStream_t s) {
@@ -688,11 +704,12 @@ struct Engine {
   // owner: E_co rows of the next batch (embedding.cpp:560-590)
   int send_eco(OwnBatch& on, cudaStream_t s) {
     Span sp(this, FSX_PHASE_ECO, s);
+    if (p == 1) return -1;  // the merge reads the updated rows from the table
     const int par = next_par(CH_COR);
     Slots send = send_slots(CH_COR, par);
     FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, on.pack_tot() + 1, 2, cap, ctx->d_err);
     IdRowPackMap pm{static_cast<const char*>(t->values), on.srt.uniq.p, on.srt.uniq_g.p, on.co_list.p,
-                    send, on.pack_tot(), 1, rb};
+                    send, on.pack_tot(), 1, rb, me};
     launch_copy_rows(ctx, pm, on.m_cap * static_cast<uint64_t>(p), on.misc.p + 3, rb, s);
     if (p > 1) {
       std::vector<uint64_t> bytes(p);
@@ -706,11 +723,10 @@ struct Engine {
   void merge(ReqBatch& r, void* d_out, cudaStream_t s) {
     Span sp(this, FSX_PHASE_MERGE, s);
     CSlots co{};
-    if (r.cor_par >= 0) co = recv_slots(CH_COR, r.cor_par);
-    else co = recv_slots(CH_EX, r.ex_par);  // no collision rows were sent
-    MergeMap mm{recv_slots(CH_IDX, r.idx_par), recv_slots(CH_EX, r.ex_par), co, nullptr,
-                r.send_pos.p, r.send_dst.p, r.send_off(), r.ids.p, static_cast<char*>(d_out), rb,
-                ctx->d_err};
+    if (p > 1) co = r.cor_par >= 0 ? recv_slots(CH_COR, r.cor_par) : recv_slots(CH_EX, r.ex_par);
+    MergeMap mm{recv_slots(CH_IDX, r.idx_par), recv_slots(CH_EX, r.ex_par), co,
+                static_cast<const char*>(t->values), r.send_pos.p, r.send_dst.p, r.send_off(), r.ids.p,
+                static_cast<char*>(d_out), rb, me, p, ctx->d_err};
     launch_copy_rows(ctx, mm, r.n, nullptr, rb, s);
   }
 
@@ -895,7 +911,7 @@ struct Engine {
     CSlots cor{};
     if (cor_par >= 0) cor = recv_slots(CH_COR, cor_par);
     FSX_LAUNCH(ctx, k_blocking_bytes, 1, 32, 0, s, p, 8ull * t->g.dim, rc.split_tot.p, oc.occ_tot(),
-               on.pack_tot(), cor, have_grads ? 1 : 0, have_eco ? 1 : 0, d);
+               on.pack_tot(), cor, oc.misc.p, have_grads ? 1 : 0, have_eco ? 1 : 0, d);
     FSX_CUDA(cudaMemcpyAsync(stat_row(i) + 2, d, 8, cudaMemcpyDeviceToHost, s));
   }
 

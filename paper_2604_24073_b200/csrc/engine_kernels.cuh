@@ -193,12 +193,13 @@ static __global__ void k_idx_pack(const uint32_t* __restrict__ inverse,
                                   const uint8_t* __restrict__ occ_src,
                                   const uint32_t* __restrict__ occ_idx, const uint64_t* d_m,
                                   const uint32_t* __restrict__ rank_us,
-                                  const uint8_t* __restrict__ co, Slots send) {
+                                  const uint8_t* __restrict__ co, Slots send, int self) {
   const uint64_t m = *d_m;
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < m;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint32_t u = inverse[j];
     const int s = occ_src[j];
+    if (s == self) continue;  // self rows are merged straight from the table
     const uint32_t v = rank_us[static_cast<uint64_t>(u) * kMaxRanks + s] | (co[u] ? 0x80000000u : 0u);
     reinterpret_cast<uint32_t*>(send.p[s] + kHdr)[occ_idx[j]] = v;
   }
@@ -348,8 +349,11 @@ struct IdRowPackMap {
   const uint64_t* totals;  // per-source counts: totals[2*s + which]
   int which;
   uint32_t row_bytes;
+  int self;                // rows for this rank itself are never copied: its
+                           // merge reads them from the table (MergeMap)
   __device__ const char* src(uint64_t i) const {
     const PackEntry e = list[i];
+    if (static_cast<int>(e.src) == self) return nullptr;
     // the id rides in the same pass
     reinterpret_cast<uint64_t*>(send.p[e.src] + kHdr)[e.rank] = uniq_g[e.u];
     return table + uniq_local[e.u] * row_bytes;
@@ -364,18 +368,24 @@ struct IdRowPackMap {
 // requester merge (embedding.cpp:453-484): occurrence k of owner d takes row
 // IDX[d][q] of that owner's E_ex or E_co message; the id stored next to the
 // row must be the id asked for ("missing from both prefetched buffers").
+// Rows this rank owns itself are read straight from the table: at merge time
+// the table holds exactly what E_ex / E_co would carry (exclusive rows of i
+// are not updated between their prefetch and this merge; collision rows were
+// updated before E_co was released), so self traffic moves no rows at all.
 struct MergeMap {
   CSlots idx, ex, co;
-  const uint64_t* send_ids_dummy;
+  const char* table;
   const uint32_t* send_pos;
   const uint8_t* send_dst;
   const uint64_t* send_off;
   const uint64_t* ids;  // batch ids (position order)
   char* out;
   uint32_t row_bytes;
+  int self, p;
   DevErr* err;
   __device__ const char* src(uint64_t k) const {
     const int d = send_dst[k];
+    if (d == self) return table + (ids[send_pos[k]] / static_cast<uint64_t>(p)) * row_bytes;
     const uint64_t q = k - send_off[d];
     const uint32_t v = reinterpret_cast<const uint32_t*>(idx.p[d] + kHdr)[q];
     const char* s = (v & 0x80000000u) ? co.p[d] : ex.p[d];
