@@ -15,6 +15,9 @@
 // (cuStreamWriteValue32 after each copy-engine copy, cuStreamWaitValue32 on
 // the receiving lane) — no SM ever spins and no kernel touches a peer.
 #include <algorithm>
+#include <deque>
+#include <functional>
+#include <thread>
 #include <chrono>
 #include <condition_variable>
 #include <map>
@@ -225,8 +228,77 @@ struct Hub {
   }
 };
 
+// Host side lane: one thread per engine that issues the low-priority lane's
+// work (route / dedup / collide / prefetch / masks of iteration i+1 and the
+// deferred exclusive update). With more than one rank those steps need host
+// round trips for copy-engine sizes; on this thread they never stall the
+// caller, which only issues compute-stream work and waits (in backward) for
+// the masks of its own iteration — by then its model compute is queued.
+struct SideLane {
+  std::thread th;
+  std::mutex mu;
+  std::condition_variable cv;
+  std::deque<std::function<void()>> q;
+  uint64_t posted = 0, done = 0;
+  bool stop = false;
+  std::exception_ptr err;
+  void start(int device) {
+    th = std::thread([this, device] {
+      cudaSetDevice(device);
+      for (;;) {
+        std::function<void()> f;
+        {
+          std::unique_lock<std::mutex> lk(mu);
+          cv.wait(lk, [&] { return stop || !q.empty(); });
+          if (q.empty()) return;
+          f = std::move(q.front());
+          q.pop_front();
+        }
+        try {
+          f();
+        } catch (...) {
+          std::lock_guard<std::mutex> lk(mu);
+          if (!err) err = std::current_exception();
+        }
+        {
+          std::lock_guard<std::mutex> lk(mu);
+          ++done;
+        }
+        cv.notify_all();
+      }
+    });
+  }
+  void post(std::function<void()> f) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      q.push_back(std::move(f));
+      ++posted;
+    }
+    cv.notify_all();
+  }
+  void drain() {
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [&] { return done == posted; });
+    if (err) {
+      auto e = err;
+      err = nullptr;
+      std::rethrow_exception(e);
+    }
+  }
+  ~SideLane() {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      stop = true;
+    }
+    cv.notify_all();
+    if (th.joinable()) th.join();
+  }
+};
+
 struct Engine {
   Ctx* ctx = nullptr;
+  std::unique_ptr<SideLane> side;  // p > 1 only
+  std::mutex ev_mu;                // event pools are shared by both host threads
   Table* t = nullptr;
   fsx_engine_config cfg{};
   int p = 1, me = 0;
@@ -257,6 +329,7 @@ struct Engine {
   std::vector<cudaEvent_t> prof_pool;
   size_t prof_next = 0;
   cudaEvent_t prof_event() {
+    std::lock_guard<std::mutex> lk(ev_mu);
     if (prof_next == prof_pool.size()) {
       cudaEvent_t e;
       FSX_CUDA(cudaEventCreate(&e));
@@ -279,6 +352,7 @@ struct Engine {
       if (a) {
         cudaEvent_t b = e->prof_event();
         cudaEventRecord(b, s);
+        std::lock_guard<std::mutex> lk(e->ev_mu);
         e->spans[phase].emplace_back(a, b);
       }
     }
@@ -325,14 +399,15 @@ struct Engine {
   int next_par(int ch) { return static_cast<int>(++seq[ch] & 1u); }
 
   cudaEvent_t record(cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(ev_mu);
     if (ev_next == ev_pool.size()) {
       cudaEvent_t e;
       FSX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       ev_pool.push_back(e);
     }
     cudaEvent_t e = ev_pool[ev_next];
-    ev_next = (ev_next + 1) % 64;
-    if (ev_pool.size() < 64 && ev_next == 0) ev_next = ev_pool.size();
+    ev_next = (ev_next + 1) % 256;
+    if (ev_pool.size() < 256 && ev_next == 0) ev_next = ev_pool.size();
     FSX_CUDA(cudaEventRecord(e, s));
     return e;
   }
@@ -485,7 +560,7 @@ struct Engine {
     r.reserve(cap);
     r.n = n;
     r.has_flags = false;
-    if (n) FSX_CUDA(cudaMemcpyAsync(r.ids.p, d_ids, n * 8, cudaMemcpyDeviceToDevice, s));
+    if (n && d_ids != r.ids.p) FSX_CUDA(cudaMemcpyAsync(r.ids.p, d_ids, n * 8, cudaMemcpyDeviceToDevice, s));
     const int par = next_par(CH_IDS);
     Slots send = send_slots(CH_IDS, par);
     FSX_CUDA(cudaMemsetAsync(r.tot.p, 0, 48 * 8, s));
@@ -766,43 +841,58 @@ struct Engine {
       receive(oc, par, c);
       rc.cor_par = -1;
       ev_cur = record(c);
-    } else {
-      if (rc.n != n_cur)
-        raise(FSX_ERR_PROTOCOL, "embedding: current batch does not match the prefetched ids");
-      apply_deferred();
+    } else if (rc.n != n_cur) {
+      raise(FSX_ERR_PROTOCOL, "embedding: current batch does not match the prefetched ids");
     }
     // ---- side lane L: prepare iteration i+1 (embedding.cpp:355-420) ----
     // everything the caller enqueued on C so far (e.g. the H2D of ids_next)
-    // happens-before the side lane reads it
+    // happens-before the side lane reads it; the ids are copied now so the
+    // caller's buffer is free once forward returns
     wait(lo, record(c));
     wait(lo, ev_cur);
     wait(lo, ev_merged);  // slots of the parity reused below were read by the last merge
     if (ids_next) {
       ReqBatch& rn = R(i + 1);
-      OwnBatch& on = O(i + 1);
-      const int par = route(rn, ids_next, n_next, lo);
-      receive(on, par, lo);
-      rn.cor_par = -1;
-      collide_and_prefetch(oc, on, rn, lo);
-      ev_next_ready = record(lo);
-      rn_ex_ready = ev_next_ready;
-      if (!bootstrap) masks_and_split(oc, rc, true, lo);
-    } else {
-      oc.has_co = false;
-      ev_next_ready = nullptr;
-      if (!bootstrap) masks_and_split(oc, rc, false, lo);
+      if (n_next > cap)
+        raise(FSX_ERR_INVALID_ARGUMENT, "embedding: batch of " + std::to_string(n_next) +
+                                            " ids exceeds engine capacity " + std::to_string(cap));
+      rn.reserve(cap);
+      if (n_next) FSX_CUDA(cudaMemcpyAsync(rn.ids.p, ids_next, n_next * 8, cudaMemcpyDeviceToDevice, lo));
     }
-    ev_mask = bootstrap ? nullptr : record(lo);
-    stats_forward(i, ids_next != nullptr);
+    stats_reserve(i + 1);
+    const bool with_next = ids_next != nullptr;
+    auto prep = [this, i, bootstrap, with_next, n_next]() {
+      ReqBatch& rc2 = R(i);
+      OwnBatch& oc2 = O(i);
+      if (!bootstrap) apply_deferred();
+      if (with_next) {
+        ReqBatch& rn = R(i + 1);
+        OwnBatch& on = O(i + 1);
+        const int par = route(rn, rn.ids.p, n_next, lo);
+        receive(on, par, lo);
+        rn.cor_par = -1;
+        collide_and_prefetch(oc2, on, rn, lo);
+        ev_next_ready = record(lo);
+        rn_ex_ready = ev_next_ready;
+        if (!bootstrap) masks_and_split(oc2, rc2, true, lo);
+      } else {
+        oc2.has_co = false;
+        ev_next_ready = nullptr;
+        if (!bootstrap) masks_and_split(oc2, rc2, false, lo);
+      }
+      ev_mask = bootstrap ? nullptr : record(lo);
+      stats_forward(i, with_next);
+    };
+    cudaEvent_t ex_ready_cur = cur_ex_ready;  // E_ex(i), recorded by the previous prep
+    if (side) side->post(prep); else prep();
     // ---- compute stream C: serve iteration i ----
     if (bootstrap) {
       serve_blocking(rc, oc, out, c);
     } else {
-      exposed_wait(c, {cur_ex_ready, cur_co_ready});
+      exposed_wait(c, {ex_ready_cur, cur_co_ready});
       merge(rc, out, c);
     }
     ev_merged = record(c);
-    cur_ex_ready = rn_ex_ready;
     forward_done = true;
     has_next = ids_next != nullptr;
   }
@@ -831,6 +921,8 @@ struct Engine {
 
   void prio_backward(const void* grads, cudaStream_t c) {
     if (!forward_done) raise(FSX_ERR_PROTOCOL, "embedding: backward before forward");
+    if (side) side->drain();  // masks + split counts of this iteration are issued
+    cur_ex_ready = rn_ex_ready;
     const int i = iter;
     ReqBatch& rc = R(i);
     OwnBatch& oc = O(i);
@@ -879,6 +971,7 @@ struct Engine {
   }
 
   void finalize(cudaStream_t c) {
+    if (side) side->drain();
     apply_deferred();
     wait(c, record(lo));
     wait(c, record(hi));
@@ -916,6 +1009,7 @@ struct Engine {
   }
 
   ~Engine() {
+    side.reset();
     cudaDeviceSynchronize();
     for (int d = 0; d < kMaxRanks; ++d)
       if (peer[d].ipc && peer[d].base) cudaIpcCloseMemHandle(peer[d].base);
@@ -1004,6 +1098,10 @@ int fsx_engine_create(fsx_ctx* ctx, fsx_table* table, const fsx_engine_config* c
   FSX_CUDA(cudaStreamCreateWithPriority(&e->lo, cudaStreamNonBlocking, lo_prio));
   FSX_CUDA(cudaStreamCreateWithPriority(&e->hi, cudaStreamNonBlocking, hi_prio));
   FSX_CUDA(cudaStreamCreateWithPriority(&e->ux, cudaStreamNonBlocking, lo_prio));
+  if (e->p > 1) {
+    e->side = std::make_unique<SideLane>();
+    e->side->start(ctx->device);
+  }
   e->d_stats.alloc(16);
   const uint64_t m = static_cast<uint64_t>(e->p) * cap;
   for (int k = 0; k < 3; ++k) {
@@ -1134,6 +1232,7 @@ int fsx_engine_finalize(fsx_engine* e, void* stream) {
 int fsx_engine_stats(fsx_engine* e, int iter, uint64_t* out3) {
   FSX_API_BEGIN
   DeviceGuard dg(e->ctx->device);
+  if (e->side) e->side->drain();
   if (iter < 0 || iter >= e->stats_n) raise(FSX_ERR_OUT_OF_RANGE, "fsx: no stats for iteration " + std::to_string(iter));
   FSX_CUDA(cudaDeviceSynchronize());
   std::memcpy(out3, e->stat_row(iter), 24);
@@ -1143,6 +1242,7 @@ int fsx_engine_stats(fsx_engine* e, int iter, uint64_t* out3) {
 int fsx_engine_exposed_ms(fsx_engine* e, double* ms) {
   FSX_API_BEGIN
   DeviceGuard dg(e->ctx->device);
+  if (e->side) e->side->drain();
   double total = 0;
   for (auto& w : e->waits) {
     FSX_CUDA(cudaEventSynchronize(w.second));
@@ -1165,6 +1265,7 @@ int fsx_engine_set_profiling(fsx_engine* e, int on) {
 int fsx_engine_phase_ms(fsx_engine* e, int phase, double* total_ms, uint64_t* count) {
   FSX_API_BEGIN
   DeviceGuard dg(e->ctx->device);
+  if (e->side) e->side->drain();
   if (phase < 0 || phase >= FSX_NUM_PHASES) raise(FSX_ERR_OUT_OF_RANGE, "fsx: bad phase");
   double t = 0;
   for (auto& sp : e->spans[phase]) {
