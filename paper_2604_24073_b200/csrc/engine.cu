@@ -317,6 +317,7 @@ struct Engine {
   ncclComm_t nccl = nullptr;  // FSX_TRANSPORT_NCCL (blocking baseline)
   uint32_t seq[NCH] = {};
   cudaStream_t lo = nullptr, hi = nullptr, ux = nullptr;  // ux: deferred exclusive updates
+  cudaStream_t cstream[kMaxRanks] = {};                    // per-peer copy streams
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_next = 0;
   // exposed-wait timing on the compute stream
@@ -519,22 +520,30 @@ struct Engine {
       std::fprintf(stderr, "[fsx r%d] a2a ch=%d seq=%u par=%d stream=%s\n", me, ch, v, par,
                    s == lo ? "L" : s == hi ? "H" : "C");
     Span sp(this, FSX_PHASE_A2A, s);
+    // fork: each peer's copy + flag on its own copy stream (parallel copy
+    // engines), join back into `s` below
+    cudaEvent_t fork = record(s);
     for (int k = 1; k < p; ++k) {
       const int d = (me + k) % p;  // stagger destinations across the NVSwitch
       const PeerView& pv = peer[d];
       if (!pv.base) raise(FSX_ERR_COLLECTIVE, "all_to_all: peer " + std::to_string(d) + " not connected");
+      cudaStream_t cs = cstream[d];
+      wait(cs, fork);
       char* dst = pv.base + ch_off[ch] + (static_cast<size_t>(par) * p + me) * ch_slot[ch];
-      if (bytes[d]) FSX_CUDA(cudaMemcpyAsync(dst, stage_slot(ch, par, d), bytes[d], cudaMemcpyDefault, s));
+      if (bytes[d]) FSX_CUDA(cudaMemcpyAsync(dst, stage_slot(ch, par, d), bytes[d], cudaMemcpyDefault, cs));
       if (pv.local) {
         cudaEvent_t ev;
         FSX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        FSX_CUDA(cudaEventRecord(ev, s));
+        FSX_CUDA(cudaEventRecord(ev, cs));
         Hub::get().post(pv.local, ch, v, me, ev);
       } else {
-        FSX_CU(drv::write_value32()(reinterpret_cast<CUstream>(s),
+        FSX_CU(drv::write_value32()(reinterpret_cast<CUstream>(cs),
                                     reinterpret_cast<CUdeviceptr>(pv.flags + ch * kMaxRanks + me), v,
                                     CU_STREAM_WRITE_VALUE_DEFAULT));
       }
+      // the sender's staging slot is reused two uses later: `s` must not run
+      // ahead of this copy
+      wait(s, record(cs));
     }
     for (int k = 1; k < p; ++k) {
       const int src = (me + p - k) % p;
@@ -1020,6 +1029,8 @@ struct Engine {
     if (lo) cudaStreamDestroy(lo);
     if (hi) cudaStreamDestroy(hi);
     if (ux) cudaStreamDestroy(ux);
+    for (auto cs : cstream)
+      if (cs) cudaStreamDestroy(cs);
     if (win) cudaFree(win);
     for (auto* h : h_stats) cudaFreeHost(h);
   }
@@ -1093,11 +1104,19 @@ int fsx_engine_create(fsx_ctx* ctx, fsx_table* table, const fsx_engine_config* c
   e->flags = reinterpret_cast<uint32_t*>(e->win + e->flags_off);
   FSX_CUDA(cudaMemset(e->flags, 0, NCH * kMaxRanks * sizeof(uint32_t)));
   if (e->p > 1) e->stage.alloc(off);
-  int lo_prio = 0, hi_prio = 0;
-  FSX_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
-  FSX_CUDA(cudaStreamCreateWithPriority(&e->lo, cudaStreamNonBlocking, lo_prio));
-  FSX_CUDA(cudaStreamCreateWithPriority(&e->hi, cudaStreamNonBlocking, hi_prio));
-  FSX_CUDA(cudaStreamCreateWithPriority(&e->ux, cudaStreamNonBlocking, lo_prio));
+  // Priorities (lower number = higher): the collision chain highest, the
+  // next-iteration prep above the caller's compute (it gates the next merge),
+  // the deferred exclusive update lowest (it has an iteration of slack).
+  int least = 0, greatest = 0;
+  FSX_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+  const int mid = greatest < least ? greatest + 1 : greatest;
+  FSX_CUDA(cudaStreamCreateWithPriority(&e->lo, cudaStreamNonBlocking, mid));
+  FSX_CUDA(cudaStreamCreateWithPriority(&e->hi, cudaStreamNonBlocking, greatest));
+  FSX_CUDA(cudaStreamCreateWithPriority(&e->ux, cudaStreamNonBlocking, least));
+  // one copy stream per peer: outgoing copies of an all-to-all run on
+  // several copy engines at once instead of queueing on one
+  for (int d = 0; d < e->p; ++d)
+    if (d != e->me) FSX_CUDA(cudaStreamCreateWithPriority(&e->cstream[d], cudaStreamNonBlocking, greatest));
   if (e->p > 1) {
     e->side = std::make_unique<SideLane>();
     e->side->start(ctx->device);

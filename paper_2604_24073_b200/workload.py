@@ -9,7 +9,13 @@
 * lengths — UIH lengths from DistSpec::empirical with hist[k] = k^-2 on
           [16, 8192] (the power-law of BASELINE.json configs 2/4/5);
 * cfg4/cfg5 tokens — table t ~ U[0, T) and row ~ Zipf(1.1) over 10M rows,
-          fused gid = t * rows_per_table + row.
+          fused gid = t * rows_per_table + scramble(t, row), where scramble
+          is the per-table bijection row -> (7919 * row + off_t) mod
+          rows_per_table, off_t = splitmix64(t) mod rows_per_table: Zipf
+          rank is not tied to small ids (production ids are hashed), so the
+          hot rows of the 10M-row tables (10M = 0 mod 8) do not all land on
+          shard 0 under the reference's `gid mod p` sharding (SURVEY §7,
+          hard part 6).
 
 The k-th draw of a stream is splitmix(seed + k * golden), so whole streams
 vectorise in numpy.
@@ -85,7 +91,15 @@ def cfg_tokens(seed: int, iteration: int, rank: int, samples: int, tables: int,
     n = int(lens.sum())
     t = (splitmix_stream(base ^ 0x2222, n) % np.uint64(tables)).astype(np.uint64)
     r = zipf_ids(base ^ 0x3333, n, rows_per_table, s)
+    r = scramble_rows(t, r, rows_per_table)
     return lens, t * np.uint64(rows_per_table) + r
+
+
+def scramble_rows(t: np.ndarray, r: np.ndarray, rows: int) -> np.ndarray:
+    """Per-table bijection of [0, rows) (gcd(7919, rows) == 1 for 10^k)."""
+    with np.errstate(over="ignore"):
+        off = _mix(np.asarray(t, np.uint64) + GOLDEN) % np.uint64(rows)
+        return (r.astype(np.uint64) * np.uint64(7919) + off) % np.uint64(rows)
 
 
 def zipf_batch(seed: int, n: int, rows: int, s: float = 1.1, offset: int = 0) -> np.ndarray:
