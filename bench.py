@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--dim", type=int, default=256)
     ap.add_argument("--samples", type=int, default=2048, help="UIH samples per rank per iteration")
     ap.add_argument("--reduce-chunk", type=int, default=64)
+    ap.add_argument("--presum", type=int, default=-1,
+                    help="prioritized: pre-sum collision gradients per (source, row) before the "
+                         "collision all-to-all (-1: on when N>1)")
     ap.add_argument("--seed", type=int, default=20261018)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-phases", type=int, default=1)
@@ -69,6 +72,33 @@ def batches_for(args, rank, world, iters, with_lens=False):
         out.append(ids)
         lens.append(ln)
     return (out, lens) if with_lens else out
+
+
+def balance_batches(args, world, rank, iters, first, ctx):
+    """Config 5's load-balancing stage (partition.cpp:157-176, FBS on the
+    GPU): for every iteration >= first, the global batch (every rank's UIH
+    samples, regenerated deterministically here) is partitioned across ranks
+    by uih length — equal sample counts, snake order — and this rank keeps
+    its assigned samples in receive order. Replaces batches/lens in place."""
+    from paper_2604_24073_b200 import partition as P
+    from paper_2604_24073_b200 import workload
+    tables = args.tables_per_rank * world
+    out_ids, out_lens = {}, {}
+    for i in range(first, iters):
+        per = [workload.cfg_tokens(args.seed, i, r, args.samples, tables, args.rows_per_table)
+               for r in range(world)]
+        metas = [P.GlobalSampleMeta(r, k, int(l)) for r in range(world) for k, l in enumerate(per[r][0])]
+        plan = P.fbs_partition(metas, world, ctx=ctx)
+        offs = [np.concatenate([[0], np.cumsum(per[r][0].astype(np.int64))]) for r in range(world)]
+        ids, lens = [], []
+        for g in plan.receive_order[rank]:
+            m = metas[int(g)]
+            o = offs[m.origin_rank]
+            ids.append(per[m.origin_rank][1][o[m.local_index]:o[m.local_index + 1]])
+            lens.append(m.uih_len)
+        out_ids[i] = np.concatenate(ids) if ids else np.zeros(0, np.uint64)
+        out_lens[i] = np.asarray(lens, np.uint64)
+    return out_ids, out_lens
 
 
 def work_rows(batches, world=1):
@@ -146,16 +176,23 @@ class Victim:
         self.b = torch.randn(4096, 1024, generator=g, device=dev).to(torch.bfloat16)
         self.c = torch.empty(4096, 1024, device=dev, dtype=torch.bfloat16)
         self.c0, self.c1, self.c2 = c0, c1, c2
-        for _ in range(3):
+        for _ in range(20):
             torch.matmul(self.a, self.b, out=self.c)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(20):
+        for _ in range(100):
             torch.matmul(self.a, self.b, out=self.c)
         e1.record()
         torch.cuda.synchronize()
-        self.unit_us = e0.elapsed_time(e1) * 1e3 / 20
+        self.unit_us = e0.elapsed_time(e1) * 1e3 / 100
+        # one unit size for every rank (same GPUs): the victim's per-rank time
+        # then follows the cost model alone, not each GPU's calibration noise
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+            t = torch.tensor([self.unit_us], dtype=torch.float64, device=dev)
+            dist.all_reduce(t)
+            self.unit_us = float(t.item()) / dist.get_world_size()
 
     def cost_us(self, lens):
         lens = np.asarray(lens, np.float64)
@@ -267,6 +304,12 @@ def main():
     iters = W + 2 * K + min(K, 5) + 2 + (2 * K + 4 if cfg5 else 0)
     t_gen = time.time()
     batches, blens = batches_for(args, rank, world, iters, with_lens=True)
+    ctx = E.Context(local, rank, world)
+    cfg5_first = W + 2 * K + min(K, 5)
+    if cfg5 and world > 1 and args.mode == "prio":
+        bi, bl = balance_batches(args, world, rank, iters, cfg5_first, ctx)
+        for i in bi:
+            batches[i], blens[i] = bi[i], bl[i]
     t_gen = time.time() - t_gen
     cap = int(max(b.size for b in batches) * 1.05) + 1024
     if world > 1:  # every rank's engine must use the same capacity (same window layout)
@@ -276,15 +319,18 @@ def main():
     tables = args.tables_per_rank * world
     total_rows = tables * args.rows_per_table
     geom = E.TableGeometry(total_rows, args.dim, world)
-    ctx = E.Context(local, rank, world)
     t0 = time.time()
     shard = E.ShardView(geom, rank, 0.05, 7, dtype="f32", ctx=ctx)
     t_init = time.time() - t0
     cls = E.PrioritizedEmbedding if args.mode == "prio" else E.SynchronizedEmbedding
     transport = args.transport or ("ce" if args.mode == "prio" or world == 1 else "nccl")
-    eng = cls(shard, comm, max_occurrences=cap, reduce_chunk=args.reduce_chunk, transport=transport)
+    presum = args.mode == "prio" and (args.presum > 0 or (args.presum < 0 and world > 1))
+    kw = {"presum": True} if presum else {}
+    eng = cls(shard, comm, max_occurrences=cap, reduce_chunk=args.reduce_chunk, transport=transport, **kw)
 
     stream = torch.cuda.Stream(device=dev)
+    if hasattr(eng, "set_ids_ready"):
+        eng.set_ids_ready(True)  # the resident id tensors are uploaded before timing
     d_ids = [torch.from_numpy(b.view(np.int64)).to(dev) for b in batches]
     h_ids = [torch.from_numpy(b.view(np.int64)).pin_memory() for b in batches]
     slots = [torch.empty(cap, dtype=torch.int64, device=dev) for _ in range(3)]
@@ -305,8 +351,9 @@ def main():
         n = batches[i].size
         if args.mode == "prio":
             if e2e:
-                nxt = upload(i + 1)
-                eng.forward(slots[i % 3][:n], nxt, out=out[:n], stream=stream)
+                # the next batch's ids go from pinned host memory straight to
+                # the engine's side lane (its own H2D)
+                eng.forward(h_ids[i], h_ids[i + 1], out=out[:n], stream=stream)
             else:
                 eng.forward(d_ids[i], d_ids[i + 1], out=out[:n], stream=stream)
         else:
@@ -370,7 +417,6 @@ def main():
         # end-to-end: host ids -> device each step, stats read back
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         first_e2e = W + K + min(K, 5)
-        upload(first_e2e)
         barrier()
         e0.record(stream)
         n_e2e = 0
@@ -386,6 +432,7 @@ def main():
     cfg5_out = None
     if cfg5 and args.mode == "prio":
         it0 = first_e2e + n_e2e  # next iteration of the prioritized engine
+        assert world == 1 or it0 >= cfg5_first
         victim = Victim(dev)
         vt0, vt1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         res = {}
@@ -440,6 +487,8 @@ def main():
         exp_b_sum = sum_over_ranks(res[b_key][1])
         exp_p_sum = sum_over_ranks(res["prio_ce"][1])
         cfg5_out = {
+            "load_balancer": ("FBS (partition.cpp:157-176) over the global batch of each iteration, on the GPU"
+                              if world > 1 else "none (1 rank)"),
             "workload": ("config 5: config-4 embeddings + synthetic HSTU-style compute between forward and "
                          f"backward, per-rank cost c0+c1*sum(L)+c2*sum(L^2) = {victim.c0}+{victim.c1}*sum(L)+"
                          f"{victim.c2}*sum(L^2) us as bf16 GEMMs"),
@@ -536,7 +585,7 @@ def main():
                        "mode": args.mode, "transport": transport, "tables": tables, "rows_per_table": args.rows_per_table,
                        "dim": args.dim, "samples_per_rank": args.samples,
                        "ids_per_rank_per_iter": int(np.mean([b.size for b in timed])),
-                       "reduce_chunk": args.reduce_chunk, "grads": "fixed synthetic upstream gradient",
+                       "reduce_chunk": args.reduce_chunk, "presum": presum, "grads": "fixed synthetic upstream gradient",
                        "l2": "inputs larger than L2 (82 GB table, ~1 GB moved per step)",
                        "parallelism": f"row-wise sharded x{world}"},
             "exposed_comm_ms_per_iter": round(exposed_ms, 4),

@@ -133,6 +133,14 @@ int fsx_table_upload(fsx_table* t, const double* h_values);
 /* ---- engines: Synchronized / Prioritized embedding ------------------------ */
 typedef struct fsx_engine fsx_engine;
 
+/* engine flags */
+#define FSX_ENGINE_PRESUM 1u /* prioritized: requesters pre-sum their collision
+                                gradients per row before the collision
+                                all-to-all (one row per (source, row) on the
+                                blocking chain instead of one per occurrence).
+                                Fixed two-level association: fp32 tolerance,
+                                not bitwise with the reference. */
+
 typedef struct fsx_engine_config {
   int mode;                  /* FSX_MODE_SYNC | FSX_MODE_PRIO */
   int transport;             /* FSX_TRANSPORT_CE | FSX_TRANSPORT_NCCL (N>1) */
@@ -142,6 +150,7 @@ typedef struct fsx_engine_config {
                                 are summed as fixed k-occurrence chunks, then
                                 chunk partials in order (deterministic, shared
                                 by both modes) */
+  uint32_t flags;            /* FSX_ENGINE_* */
 } fsx_engine_config;
 
 int fsx_engine_create(fsx_ctx* ctx, fsx_table* table, const fsx_engine_config* cfg,
@@ -163,7 +172,11 @@ int fsx_engine_connect_nccl(fsx_engine* e, const void* id128);
  * and, for the prioritized engine, of the next one (d_ids_next, n_next; pass
  * NULL on the final iteration). Writes n_cur x dim rows batch-major to d_out
  * on `stream` (the caller's compute stream). Host returns once the work is
- * enqueued; device-side errors surface at fsx_ctx_sync / later calls. */
+ * enqueued; device-side errors surface at fsx_ctx_sync / later calls.
+ * Id pointers may be device memory or (pinned) host memory; host ids are
+ * copied on the engine's side lane. Device ids are ordered after the work
+ * already on `stream` unless fsx_engine_set_ids_ready(e, 1) declared that the
+ * caller passes only completed buffers. */
 int fsx_engine_forward(fsx_engine* e, const uint64_t* d_ids_cur, uint64_t n_cur,
                        const uint64_t* d_ids_next, uint64_t n_next, void* d_out, void* stream);
 /* backward: n_cur x dim gradients of the last forward, on `stream`. */
@@ -197,8 +210,14 @@ int fsx_engine_exposed_ms(fsx_engine* e, double* ms);
 #define FSX_PHASE_SERVE 10    /* C: blocking per-occurrence lookup + scatter    */
 #define FSX_PHASE_UPDATE 11   /* C: blocking full update                        */
 #define FSX_PHASE_A2A 12      /* copy-engine transfers (any lane)               */
-#define FSX_NUM_PHASES 13
+#define FSX_PHASE_EXPOSED 13  /* C: compute stream stalled on embedding traffic   */
+#define FSX_NUM_PHASES 14
 int fsx_engine_set_profiling(fsx_engine* e, int on);
+/* timeline of the recorded spans: out[3k..3k+2] = (phase, start ms, end ms)
+ * relative to the earliest span; consumes them (synchronizes) */
+int fsx_engine_spans(fsx_engine* e, double* out, uint64_t max_spans, uint64_t* n_spans);
+/* device ids handed to forward are complete (no pending writes on any stream) */
+int fsx_engine_set_ids_ready(fsx_engine* e, int ready);
 /* total ms and number of spans of `phase` since the last call for that
  * phase (synchronizes; resets the phase) */
 int fsx_engine_phase_ms(fsx_engine* e, int phase, double* total_ms, uint64_t* spans);

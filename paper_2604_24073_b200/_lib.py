@@ -20,7 +20,7 @@ FSX_F32, FSX_F64 = 0, 1
 FSX_MODE_SYNC, FSX_MODE_PRIO = 0, 1
 FSX_TRANSPORT_CE, FSX_TRANSPORT_NCCL = 0, 1
 PHASES = ["merge", "split", "co_update", "ex_update", "prefetch", "eco", "route", "dedup",
-          "collide", "masks", "serve", "update", "a2a"]
+          "collide", "masks", "serve", "update", "a2a", "exposed"]
 
 _lock = threading.Lock()
 _lib = None
@@ -33,9 +33,12 @@ dbl = C.c_double
 P = C.POINTER
 
 
+FSX_ENGINE_PRESUM = 1
+
+
 class EngineConfig(C.Structure):
     _fields_ = [("mode", C.c_int), ("transport", C.c_int), ("max_occurrences", C.c_uint64),
-                ("reduce_chunk", C.c_uint32)]
+                ("reduce_chunk", C.c_uint32), ("flags", C.c_uint32)]
 
 
 # name -> (argtypes, restype)
@@ -70,6 +73,8 @@ _SIGS = {
     "fsx_engine_stats": ([vp, i32, P(u64)], i32),
     "fsx_engine_exposed_ms": ([vp, P(dbl)], i32),
     "fsx_engine_set_profiling": ([vp, i32], i32),
+    "fsx_engine_set_ids_ready": ([vp, i32], i32),
+    "fsx_engine_spans": ([vp, vp, u64, P(u64)], i32),
     "fsx_engine_phase_ms": ([vp, i32, P(dbl), P(u64)], i32),
     "fsx_cost_estimate": ([vp, vp, vp, i32, dbl, dbl, dbl, vp, vp], i32),
     "fsx_fbs_partition": ([vp, vp, vp, vp, u64, i32, vp, vp, vp], i32),

@@ -320,7 +320,7 @@ void EngineBase::ensure(std::size_t n) {
     cap = std::max(cap, v);
   }
   cap_ = cap;
-  fsx_engine_config cfg{mode, FSX_TRANSPORT_CE, cap_, 0};
+  fsx_engine_config cfg{mode, FSX_TRANSPORT_CE, cap_, 0, 0};
   fsx_ok(fsx_engine_create(shard_.ctx(), shard_.handle(), &cfg, &eng_));
   std::vector<std::uint8_t> me(sizeof(void*));
   std::memcpy(me.data(), &eng_, sizeof(void*));

@@ -37,7 +37,7 @@
 
 namespace fsx {
 
-enum Channel : int { CH_IDS, CH_ROWS, CH_GRADS, CH_EX, CH_MASK, CH_COG, CH_EXG, CH_COR, CH_IDX, NCH };
+enum Channel : int { CH_IDS, CH_ROWS, CH_GRADS, CH_EX, CH_MASK, CH_COG, CH_EXG, CH_COR, CH_IDX, CH_GRP, NCH };
 
 // ---- NCCL, loaded at run time (baseline transport only) ----------------------
 struct NcclApi {
@@ -149,10 +149,16 @@ struct ReqBatch {  // requester view of one iteration's ids
   std::vector<uint64_t> h_send, h_split;
   bool has_flags = false;
   int ex_par = -1, cor_par = -1, idx_par = -1;  // channel parities of E_ex / E_co / IDX
+  // PRESUM: flattened (owner, slot) segments of the collision occurrences
+  DevBuf<uint32_t> seg_flat, perm_flat;
+  DevBuf<char*> out_ptr;
+  DevBuf<uint64_t> bases;  // k_grp_bases layout
+  std::vector<uint64_t> h_slots;  // collision rows per owner (pre-summed message rows)
   void reserve(uint64_t cap) {
     if (ids.n >= cap && ids.p) return;
     ids.alloc(cap); send_pos.alloc(cap); split_rank.alloc(cap); send_dst.alloc(cap); flag.alloc(cap);
     tot.alloc(48); split_tot.alloc(32);
+    seg_flat.alloc(cap + kMaxRanks + 1); perm_flat.alloc(cap); out_ptr.alloc(cap + kMaxRanks); bases.alloc(64);
   }
   const uint64_t* send_off() const { return tot.p + 16; }
 };
@@ -165,6 +171,7 @@ struct OwnBatch {  // owner view: occurrences received for this shard
   DevBuf<uint64_t> misc; // [0] co count, [8..40) pack totals (2p), [40..72) occ totals, [72..88) mask totals
   DevBuf<PackEntry> ex_list, co_list;
   DevBuf<uint32_t> rank_us;  // [unique row][kMaxRanks] position in each source's message
+  DevBuf<uint32_t> slot_us;  // PRESUM: [unique row][kMaxRanks] slot in the GRP message
   SortedIds srt;
   ScanScratch scan;
   std::vector<uint64_t> h_recv, h_pack, h_mask;
@@ -174,14 +181,16 @@ struct OwnBatch {  // owner view: occurrences received for this shard
     if (m_cap >= cap && ids.p) return;
     m_cap = cap;
     ids.alloc(cap); occ_src.alloc(cap); co.alloc(cap); occ_idx.alloc(cap); occ_rank.alloc(cap);
-    bits.alloc(cap); cnt.alloc(2 + 2 * kMaxRanks + 8); misc.alloc(96); ex_list.alloc(cap);
+    bits.alloc(cap); cnt.alloc(2 + 2 * kMaxRanks + 8); misc.alloc(128); ex_list.alloc(cap);
     co_list.alloc(cap);
     rank_us.alloc(cap * kMaxRanks);
+    slot_us.alloc(cap * kMaxRanks);
     srt.reserve(cap);
   }
   uint64_t* pack_tot() { return misc.p + 8; }
   uint64_t* occ_tot() { return misc.p + 40; }
   uint64_t* mask_tot() { return misc.p + 72; }
+  uint64_t* grp_tot() { return misc.p + 96; }
 };
 
 struct PeerView {
@@ -315,9 +324,23 @@ struct Engine {
   DevBuf<char> stage;         // send staging, same layout as the channel region of win
   PeerView peer[kMaxRanks];
   ncclComm_t nccl = nullptr;  // FSX_TRANSPORT_NCCL (blocking baseline)
+  bool ids_ready = false;     // device ids handed to forward need no stream ordering
+  static bool is_host_ptr(const void* ptr) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+      cudaGetLastError();
+      return true;  // unregistered host memory
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeUnregistered;
+  }
   uint32_t seq[NCH] = {};
   cudaStream_t lo = nullptr, hi = nullptr, ux = nullptr;  // ux: deferred exclusive updates
-  cudaStream_t cstream[kMaxRanks] = {};                    // per-peer copy streams
+  // per-(lane, peer) copy streams: a lane's copies never queue behind another
+  // lane's (the collision chain must not wait for prefetch or deferred
+  // traffic issued earlier on the same peer)
+  static constexpr int kLanes = 4;  // L, H, ux, caller
+  cudaStream_t cstream[kLanes][kMaxRanks] = {};
+  int lane_of(cudaStream_t s) const { return s == lo ? 0 : s == hi ? 1 : s == ux ? 2 : 3; }
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_next = 0;
   // exposed-wait timing on the compute stream
@@ -427,6 +450,7 @@ struct Engine {
   }
   // compute stream waits on embedding traffic; the pair measures the stall
   void exposed_wait(cudaStream_t c, std::initializer_list<cudaEvent_t> evs) {
+    Span sp(this, FSX_PHASE_EXPOSED, c);
     cudaEvent_t a = timing_event(), b = timing_event();
     FSX_CUDA(cudaEventRecord(a, c));
     for (cudaEvent_t e : evs) wait(c, e);
@@ -513,6 +537,7 @@ struct Engine {
   }
   // payload bytes per counted element of a channel (after the header)
   uint64_t elem_bytes(int ch) const { return ch == CH_IDS ? 8 : ch == CH_MASK ? 1 : ch == CH_IDX ? 4 : rb; }
+  bool presum() const { return (cfg.flags & FSX_ENGINE_PRESUM) != 0; }
 
   void a2a_ce(int ch, int par, const std::vector<uint64_t>& bytes, cudaStream_t s) {
     const uint32_t v = seq[ch];
@@ -527,7 +552,7 @@ struct Engine {
       const int d = (me + k) % p;  // stagger destinations across the NVSwitch
       const PeerView& pv = peer[d];
       if (!pv.base) raise(FSX_ERR_COLLECTIVE, "all_to_all: peer " + std::to_string(d) + " not connected");
-      cudaStream_t cs = cstream[d];
+      cudaStream_t cs = cstream[lane_of(s)][d];
       wait(cs, fork);
       char* dst = pv.base + ch_off[ch] + (static_cast<size_t>(par) * p + me) * ch_slot[ch];
       if (bytes[d]) FSX_CUDA(cudaMemcpyAsync(dst, stage_slot(ch, par, d), bytes[d], cudaMemcpyDefault, cs));
@@ -655,7 +680,7 @@ struct Engine {
     const int par = next_par(CH_GRADS);
     Slots send = send_slots(CH_GRADS, par);
     GradPackMap gm{static_cast<const char*>(d_grads), r.send_pos.p, r.send_dst.p, r.send_off(),
-                   nullptr, nullptr, send, send, rb};
+                   nullptr, nullptr, send, send, rb, 0};
     launch_copy_rows(ctx, gm, r.n, nullptr, rb, s);
     FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, r.tot.p, 1, cap, ctx->d_err);
     if (p > 1) {
@@ -736,7 +761,34 @@ struct Engine {
   // (embedding.cpp:392-408, 524-536)
   void masks_and_split(OwnBatch& oc, ReqBatch& rc, bool with_co, cudaStream_t s) {
     Span sp(this, FSX_PHASE_MASKS, s);
-    if (with_co) {
+    if (with_co && presum()) {
+      // GRP messages: each source's collision occurrences grouped by row
+      const int par = next_par(CH_GRP);
+      Slots send = send_slots(CH_GRP, par);
+      FSX_CUDA(cudaMemsetAsync(oc.grp_tot(), 0, 32 * 8, s));
+      if (nc2() == 8) {
+        GroupOp<8> op{oc.srt.perm, oc.srt.inverse.p, oc.srt.seg_start.p, oc.occ_src.p, oc.occ_idx.p,
+                      oc.co.p, send, oc.slot_us.p};
+        run_scan(ctx, op, oc.m_cap, oc.srt.d_n(), oc.scan, oc.grp_tot(), s);
+      } else {
+        GroupOp<16> op{oc.srt.perm, oc.srt.inverse.p, oc.srt.seg_start.p, oc.occ_src.p, oc.occ_idx.p,
+                       oc.co.p, send, oc.slot_us.p};
+        run_scan(ctx, op, oc.m_cap, oc.srt.d_n(), oc.scan, oc.grp_tot(), s);
+      }
+      FSX_LAUNCH(ctx, k_grp_headers, 1, 32, 0, s, send, p, oc.grp_tot());
+      if (p > 1) {
+        const std::vector<uint64_t> g = fetch(oc.grp_tot(), 2 * p, s);
+        std::vector<uint64_t> bytes(p);
+        for (int d = 0; d < p; ++d) bytes[d] = grp_list_off(g[2 * d + 1]) + 4 * g[2 * d];
+        a2a(CH_GRP, par, bytes, s);
+      }
+      FSX_CUDA(cudaMemsetAsync(rc.flag.p, 0, rc.n ? rc.n : 1, s));
+      CSlots grp = recv_slots(CH_GRP, par);
+      FSX_LAUNCH(ctx, k_grp_bases, 1, 32, 0, s, grp, p, rc.bases.p);
+      FSX_LAUNCH(ctx, k_grp_flatten, grid_for(ctx, static_cast<uint64_t>(p) * (cap + 1), 256, 8), 256, 0, s,
+                 grp, p, cap, rc.bases.p, rc.send_off(), rc.send_pos.p, send_slots(CH_COG, cog_par_next()),
+                 rb, rc.flag.p, rc.seg_flat.p, rc.perm_flat.p, rc.out_ptr.p);
+    } else if (with_co) {
       const int par = next_par(CH_MASK);
       Slots send = send_slots(CH_MASK, par);
       FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, oc.cnt.p + 2, 1, cap, ctx->d_err);
@@ -771,19 +823,81 @@ struct Engine {
       OccRankOp<16> op{oc.occ_src.p, oc.srt.inverse.p, with_co ? oc.co.p : nullptr, oc.occ_rank.p};
       run_scan(ctx, op, oc.m_cap, oc.srt.d_n(), oc.scan, oc.occ_tot(), s);
     }
-    if (p > 1) rc.h_split = fetch(rc.split_tot.p, 2 * p, s);
+    if (p > 1 && with_co && presum()) {
+      // split counts + collision rows per owner, one host round trip
+      rc.h_split.resize(2 * p);
+      rc.h_slots.resize(p);
+      FSX_CUDA(cudaMemcpyAsync(rc.h_split.data(), rc.split_tot.p, 16 * p, cudaMemcpyDeviceToHost, s));
+      FSX_CUDA(cudaMemcpyAsync(rc.h_slots.data(), rc.bases.p + 34, 8 * p, cudaMemcpyDeviceToHost, s));
+      FSX_CUDA(cudaStreamSynchronize(s));
+    } else if (p > 1) {
+      rc.h_split = fetch(rc.split_tot.p, 2 * p, s);
+    }
+  }
+  // the CO_G parity the coming backward will use (next_par is taken there)
+  int cog_par_next() const { return static_cast<int>((seq[CH_COG] + 1) & 1u); }
+
+  // owner, PRESUM: collision rows from the sources' pre-summed rows
+  void co_apply(OwnBatch& oc, int cog_par, cudaStream_t s) {
+    CSlots cog = recv_slots(CH_COG, cog_par);
+    const unsigned grid = grid_for(ctx, oc.m_cap, 4, 16);
+    const bool v16 = rb % 16 == 0;
+    if (t->dtype == FSX_F32) {
+      if (v16)
+        FSX_LAUNCH(ctx, (k_co_apply<float, 4>), grid, 128, 0, s, static_cast<float*>(t->values), t->g, t->lr,
+                   oc.srt.uniq.p, oc.srt.d_u(), oc.co.p, oc.bits.p, oc.slot_us.p, cog, p, ctx->d_err);
+      else
+        FSX_LAUNCH(ctx, (k_co_apply<float, 1>), grid, 128, 0, s, static_cast<float*>(t->values), t->g, t->lr,
+                   oc.srt.uniq.p, oc.srt.d_u(), oc.co.p, oc.bits.p, oc.slot_us.p, cog, p, ctx->d_err);
+    } else {
+      if (v16)
+        FSX_LAUNCH(ctx, (k_co_apply<double, 2>), grid, 128, 0, s, static_cast<double*>(t->values), t->g, t->lr,
+                   oc.srt.uniq.p, oc.srt.d_u(), oc.co.p, oc.bits.p, oc.slot_us.p, cog, p, ctx->d_err);
+      else
+        FSX_LAUNCH(ctx, (k_co_apply<double, 1>), grid, 128, 0, s, static_cast<double*>(t->values), t->g, t->lr,
+                   oc.srt.uniq.p, oc.srt.d_u(), oc.co.p, oc.bits.p, oc.slot_us.p, cog, p, ctx->d_err);
+    }
   }
 
   // requester: split grads into CO_G / EX_G messages (embedding.cpp:526-536)
-  void split_grads(ReqBatch& r, const void* d_grads, int cog_par, int exg_par, cudaStream_t s) {
+  // collision half first (its chain is the exposed one), then the exclusive
+  // half, which overlaps the collision all-to-all
+  void split_co(ReqBatch& r, const void* d_grads, int cog_par, cudaStream_t s) {
     Span sp(this, FSX_PHASE_SPLIT, s);
-    Slots co = send_slots(CH_COG, cog_par), ex = send_slots(CH_EXG, exg_par);
+    Slots co = send_slots(CH_COG, cog_par);
+    if (!r.has_flags) {
+      FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, co, p, r.split_tot.p + 1, 2, cap, ctx->d_err);
+      return;
+    }
+    if (!presum()) {
+      GradPackMap gm{static_cast<const char*>(d_grads), r.send_pos.p, r.send_dst.p, r.send_off(),
+                     r.flag.p, r.split_rank.p, co, co, rb, 2};
+      launch_copy_rows(ctx, gm, r.n, nullptr, rb, s);
+      FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, co, p, r.split_tot.p + 1, 2, cap, ctx->d_err);
+      return;
+    }
+    // pre-sum the collision occurrences of each (owner, row) straight into
+    // the CO_G messages (same chunked reduce as the owner, reduce-only mode)
+    RowSegments rs{nullptr, r.seg_flat.p, r.perm_flat.p, r.bases.p + 16, nullptr, 0};
+    const uint64_t segs_cap = r.n;  // a segment holds >= 1 occurrence
+    if (t->dtype == FSX_F32) {
+      GradRows<float> gr{static_cast<const char*>(d_grads), 0, nullptr, nullptr, rb};
+      sgd_update_rows<float>(ctx, *t, rs, segs_cap, r.n, gr, cfg.reduce_chunk, sgd_for(s), nullptr, s, r.out_ptr.p);
+    } else {
+      GradRows<double> gr{static_cast<const char*>(d_grads), 0, nullptr, nullptr, rb};
+      sgd_update_rows<double>(ctx, *t, rs, segs_cap, r.n, gr, cfg.reduce_chunk, sgd_for(s), nullptr, s, r.out_ptr.p);
+    }
+    FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, co, p, r.bases.p + 34, 1, cap, ctx->d_err);
+  }
+  void split_ex(ReqBatch& r, const void* d_grads, int exg_par, cudaStream_t s) {
+    Span sp(this, FSX_PHASE_SPLIT, s);
+    Slots ex = send_slots(CH_EXG, exg_par);
     GradPackMap gm{static_cast<const char*>(d_grads), r.send_pos.p, r.send_dst.p, r.send_off(),
-                   r.has_flags ? r.flag.p : nullptr, r.split_rank.p, co, ex, rb};
+                   r.has_flags ? r.flag.p : nullptr, r.split_rank.p, ex, ex, rb, 1};
     launch_copy_rows(ctx, gm, r.n, nullptr, rb, s);
-    FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, co, p, r.split_tot.p + 1, 2, cap, ctx->d_err);
     FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, ex, p, r.split_tot.p, 2, cap, ctx->d_err);
   }
+
 
   // owner: E_co rows of the next batch (embedding.cpp:560-590)
   int send_eco(OwnBatch& on, cudaStream_t s) {
@@ -804,13 +918,13 @@ struct Engine {
   }
 
   // requester: merge E_ex / E_co into batch-major rows (embedding.cpp:453-484)
-  void merge(ReqBatch& r, void* d_out, cudaStream_t s) {
+  void merge(ReqBatch& r, void* d_out, cudaStream_t s, int part = 0) {
     Span sp(this, FSX_PHASE_MERGE, s);
     CSlots co{};
     if (p > 1) co = r.cor_par >= 0 ? recv_slots(CH_COR, r.cor_par) : recv_slots(CH_EX, r.ex_par);
     MergeMap mm{recv_slots(CH_IDX, r.idx_par), recv_slots(CH_EX, r.ex_par), co,
                 static_cast<const char*>(t->values), r.send_pos.p, r.send_dst.p, r.send_off(), r.ids.p,
-                static_cast<char*>(d_out), rb, me, p, ctx->d_err};
+                static_cast<char*>(d_out), rb, me, p, ctx->d_err, part};
     launch_copy_rows(ctx, mm, r.n, nullptr, rb, s);
   }
 
@@ -846,6 +960,14 @@ struct Engine {
     const bool bootstrap = i == 0;
     cudaEvent_t ev_cur = nullptr;
     if (bootstrap) {
+      if (ids_cur && is_host_ptr(ids_cur)) {
+        rc.reserve(cap);
+        if (n_cur > cap)
+          raise(FSX_ERR_INVALID_ARGUMENT, "embedding: batch of " + std::to_string(n_cur) +
+                                              " ids exceeds engine capacity " + std::to_string(cap));
+        if (n_cur) FSX_CUDA(cudaMemcpyAsync(rc.ids.p, ids_cur, n_cur * 8, cudaMemcpyHostToDevice, c));
+        ids_cur = rc.ids.p;
+      }
       const int par = route(rc, ids_cur, n_cur, c);
       receive(oc, par, c);
       rc.cor_par = -1;
@@ -854,10 +976,13 @@ struct Engine {
       raise(FSX_ERR_PROTOCOL, "embedding: current batch does not match the prefetched ids");
     }
     // ---- side lane L: prepare iteration i+1 (embedding.cpp:355-420) ----
-    // everything the caller enqueued on C so far (e.g. the H2D of ids_next)
-    // happens-before the side lane reads it; the ids are copied now so the
-    // caller's buffer is free once forward returns
-    wait(lo, record(c));
+    // The next batch's ids are copied now (the caller's buffer is free once
+    // forward returns). Host ids: H2D on L, no tie to the caller's stream.
+    // Device ids: ordered after everything the caller enqueued so far,
+    // unless the caller declared them ready (fsx_engine_set_ids_ready) —
+    // that tie would serialise this prep behind the previous backward.
+    const bool next_host = ids_next && is_host_ptr(ids_next);
+    if (ids_next && !next_host && !ids_ready) wait(lo, record(c));
     wait(lo, ev_cur);
     wait(lo, ev_merged);  // slots of the parity reused below were read by the last merge
     if (ids_next) {
@@ -866,7 +991,9 @@ struct Engine {
         raise(FSX_ERR_INVALID_ARGUMENT, "embedding: batch of " + std::to_string(n_next) +
                                             " ids exceeds engine capacity " + std::to_string(cap));
       rn.reserve(cap);
-      if (n_next) FSX_CUDA(cudaMemcpyAsync(rn.ids.p, ids_next, n_next * 8, cudaMemcpyDeviceToDevice, lo));
+      if (n_next)
+        FSX_CUDA(cudaMemcpyAsync(rn.ids.p, ids_next, n_next * 8,
+                                 next_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, lo));
     }
     stats_reserve(i + 1);
     const bool with_next = ids_next != nullptr;
@@ -898,8 +1025,12 @@ struct Engine {
     if (bootstrap) {
       serve_blocking(rc, oc, out, c);
     } else {
-      exposed_wait(c, {ex_ready_cur, cur_co_ready});
-      merge(rc, out, c);
+      // exclusive rows first: they only wait for the prefetch, so this half of
+      // the merge overlaps the tail of the collision chain
+      exposed_wait(c, {ex_ready_cur});
+      merge(rc, out, c, 1);
+      exposed_wait(c, {cur_co_ready});
+      merge(rc, out, c, 2);
     }
     ev_merged = record(c);
     forward_done = true;
@@ -912,12 +1043,16 @@ struct Engine {
   // on their own lane: they only have to land before the next exclusive
   // prefetch reads rows, so routing / dedup / collision overlap with them
   cudaEvent_t ev_ex_applied = nullptr;
+  cudaEvent_t ev_hchain = nullptr;  // end of the last backward's collision chain
   void apply_deferred() {
     ev_ex_applied = nullptr;
     if (!has_pending) return;
     OwnBatch& op = O(pending_iter);
     ReqBatch& rp = R(pending_iter);
     wait(ux, ev_pending_split);
+    // the collision chain of that iteration has the links first: the
+    // exclusive gradients have a whole iteration of slack
+    if (ev_hchain) wait(ux, ev_hchain);
     if (p > 1) {
       std::vector<uint64_t> bytes(p);
       for (int d = 0; d < p; ++d) bytes[d] = kHdr + rb * rp.h_split[2 * d];
@@ -945,20 +1080,31 @@ struct Engine {
       exposed_wait(c, {ev_mask});
       const int cog = next_par(CH_COG);
       exg_par = next_par(CH_EXG);
-      split_grads(rc, grads, cog, exg_par, c);
+      split_co(rc, grads, cog, c);
+      ev_chain_start = record(c);
+      split_ex(rc, grads, exg_par, c);
       ev_pending_split = record(c);
       pending_iter = i;
       has_pending = true;
-      ev_chain_start = ev_pending_split;
       if (oc.has_co) {
         // collision chain, high priority (embedding.cpp:539-557)
-        wait(hi, ev_pending_split);
-        if (p > 1) {
-          std::vector<uint64_t> bytes(p);
-          for (int d = 0; d < p; ++d) bytes[d] = kHdr + rb * rc.h_split[2 * d + 1];
-          a2a(CH_COG, cog, bytes, hi);
+        wait(hi, ev_chain_start);
+        if (presum()) {
+          if (p > 1) {
+            std::vector<uint64_t> bytes(p);
+            for (int d = 0; d < p; ++d) bytes[d] = kHdr + rb * rc.h_slots[d];
+            a2a(CH_COG, cog, bytes, hi);
+          }
+          Span sp(this, FSX_PHASE_CO_UPDATE, hi);
+          co_apply(oc, cog, hi);
+        } else {
+          if (p > 1) {
+            std::vector<uint64_t> bytes(p);
+            for (int d = 0; d < p; ++d) bytes[d] = kHdr + rb * rc.h_split[2 * d + 1];
+            a2a(CH_COG, cog, bytes, hi);
+          }
+          update(oc, CH_COG, cog, oc.co.p, 1, true, hi, FSX_PHASE_CO_UPDATE);
         }
-        update(oc, CH_COG, cog, oc.co.p, 1, true, hi, FSX_PHASE_CO_UPDATE);
         have_grads = true;
       }
     }
@@ -975,6 +1121,7 @@ struct Engine {
       cur_co_ready = nullptr;
       stats_backward(i, have_grads, false, rc, oc, oc, -1, i == 0 ? c : hi);
     }
+    ev_hchain = have_grads || has_next ? record(hi) : nullptr;
     forward_done = false;
     ++iter;
   }
@@ -1029,8 +1176,9 @@ struct Engine {
     if (lo) cudaStreamDestroy(lo);
     if (hi) cudaStreamDestroy(hi);
     if (ux) cudaStreamDestroy(ux);
-    for (auto cs : cstream)
-      if (cs) cudaStreamDestroy(cs);
+    for (auto& lane : cstream)
+      for (auto cs : lane)
+        if (cs) cudaStreamDestroy(cs);
     if (win) cudaFree(win);
     for (auto* h : h_stats) cudaFreeHost(h);
   }
@@ -1088,6 +1236,7 @@ int fsx_engine_create(fsx_ctx* ctx, fsx_table* table, const fsx_engine_config* c
     slot[CH_EX] = idrows_rows_off(cap) + cap * rb;
     slot[CH_MASK] = kHdr + align16(cap);
     slot[CH_IDX] = kHdr + align16(4 * cap);
+    if (cfg->flags & FSX_ENGINE_PRESUM) slot[CH_GRP] = grp_list_off(cap) + 4 * cap;
     slot[CH_COG] = kHdr + cap * rb;
     slot[CH_EXG] = kHdr + cap * rb;
     slot[CH_COR] = idrows_rows_off(cap) + cap * rb;
@@ -1115,8 +1264,9 @@ int fsx_engine_create(fsx_ctx* ctx, fsx_table* table, const fsx_engine_config* c
   FSX_CUDA(cudaStreamCreateWithPriority(&e->ux, cudaStreamNonBlocking, least));
   // one copy stream per peer: outgoing copies of an all-to-all run on
   // several copy engines at once instead of queueing on one
-  for (int d = 0; d < e->p; ++d)
-    if (d != e->me) FSX_CUDA(cudaStreamCreateWithPriority(&e->cstream[d], cudaStreamNonBlocking, greatest));
+  for (int l = 0; l < Engine::kLanes; ++l)
+    for (int d = 0; d < e->p; ++d)
+      if (d != e->me) FSX_CUDA(cudaStreamCreateWithPriority(&e->cstream[l][d], cudaStreamNonBlocking, greatest));
   if (e->p > 1) {
     e->side = std::make_unique<SideLane>();
     e->side->start(ctx->device);
@@ -1272,6 +1422,47 @@ int fsx_engine_exposed_ms(fsx_engine* e, double* ms) {
   *ms = total;
   e->waits.clear();
   e->timing_next = 0;
+  FSX_API_END
+}
+
+// Timeline dump of every recorded span: (phase, start ms, end ms) relative
+// to the earliest span start; consumes the spans like fsx_engine_phase_ms.
+int fsx_engine_spans(fsx_engine* e, double* out, uint64_t max_spans, uint64_t* n_out) {
+  FSX_API_BEGIN
+  DeviceGuard dg(e->ctx->device);
+  if (e->side) e->side->drain();
+  FSX_CUDA(cudaDeviceSynchronize());
+  cudaEvent_t base = nullptr;
+  float best = 0;
+  for (auto& v : e->spans)
+    for (auto& sp : v) {
+      if (!base) { base = sp.first; continue; }
+      float x = 0;
+      FSX_CUDA(cudaEventElapsedTime(&x, base, sp.first));
+      if (x < best) best = x;
+    }
+  uint64_t k = 0;
+  for (int ph = 0; ph < FSX_NUM_PHASES; ++ph) {
+    for (auto& sp : e->spans[ph]) {
+      if (k >= max_spans) break;
+      float a = 0, b = 0;
+      FSX_CUDA(cudaEventElapsedTime(&a, base, sp.first));
+      FSX_CUDA(cudaEventElapsedTime(&b, base, sp.second));
+      out[3 * k] = ph;
+      out[3 * k + 1] = a - best;
+      out[3 * k + 2] = b - best;
+      ++k;
+    }
+    e->spans[ph].clear();
+  }
+  e->prof_next = 0;
+  *n_out = k;
+  FSX_API_END
+}
+
+int fsx_engine_set_ids_ready(fsx_engine* e, int ready) {
+  FSX_API_BEGIN
+  e->ids_ready = ready != 0;
   FSX_API_END
 }
 

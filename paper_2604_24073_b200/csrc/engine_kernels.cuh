@@ -199,8 +199,9 @@ static __global__ void k_idx_pack(const uint32_t* __restrict__ inverse,
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint32_t u = inverse[j];
     const int s = occ_src[j];
-    if (s == self) continue;  // self rows are merged straight from the table
-    const uint32_t v = rank_us[static_cast<uint64_t>(u) * kMaxRanks + s] | (co[u] ? 0x80000000u : 0u);
+    // self rows are merged straight from the table: only their collision bit
+    const uint32_t v = (s == self ? 0u : rank_us[static_cast<uint64_t>(u) * kMaxRanks + s]) |
+                       (co[u] ? 0x80000000u : 0u);
     reinterpret_cast<uint32_t*>(send.p[s] + kHdr)[occ_idx[j]] = v;
   }
 }
@@ -328,7 +329,10 @@ struct GradPackMap {
   const uint32_t* split_rank; // nullable: rank = k - send_off[d]
   Slots co, ex;
   uint32_t row_bytes;
+  int part;                   // 0: every row; 1: exclusive only; 2: collision only
   __device__ const char* src(uint64_t k) const {
+    const bool f = flag && flag[k];
+    if ((part == 1 && f) || (part == 2 && !f)) return nullptr;
     return grads + static_cast<uint64_t>(send_pos[k]) * row_bytes;
   }
   __device__ char* dst(uint64_t k) const {
@@ -383,12 +387,15 @@ struct MergeMap {
   uint32_t row_bytes;
   int self, p;
   DevErr* err;
+  int part;  // 0: every row; 1: exclusive rows only; 2: collision rows only
   __device__ const char* src(uint64_t k) const {
     const int d = send_dst[k];
-    if (d == self) return table + (ids[send_pos[k]] / static_cast<uint64_t>(p)) * row_bytes;
     const uint64_t q = k - send_off[d];
     const uint32_t v = reinterpret_cast<const uint32_t*>(idx.p[d] + kHdr)[q];
-    const char* s = (v & 0x80000000u) ? co.p[d] : ex.p[d];
+    const bool is_co = (v & 0x80000000u) != 0;
+    if ((part == 1 && is_co) || (part == 2 && !is_co)) return nullptr;
+    if (d == self) return table + (ids[send_pos[k]] / static_cast<uint64_t>(p)) * row_bytes;
+    const char* s = is_co ? co.p[d] : ex.p[d];
     const uint64_t r = v & 0x7fffffffu;
     const uint64_t n = slot_n(s);
     const uint64_t want = ids[send_pos[k]];
@@ -400,5 +407,178 @@ struct MergeMap {
   }
   __device__ char* dst(uint64_t k) const { return out + static_cast<uint64_t>(send_pos[k]) * row_bytes; }
 };
+
+// ---- pre-summed collision gradients (FSX_ENGINE_PRESUM) ----------------------
+// The collision chain is the exposed part of the protocol: its bytes are one
+// gradient row per collision OCCURRENCE (embedding.cpp:526-546). With PRESUM
+// each requester first sums its own occurrences of each collision row, so the
+// chain carries one row per (source, collision row) and the owner adds at
+// most p rows per collision row. Association: per (row, source) the
+// source's occurrences in position order (chunked like the owner reduce),
+// then the sources in rank order — fixed, hence deterministic, but different
+// from the reference's single left fold, so this mode is held to the fp32
+// tolerance, not bitwise.
+//
+// GRP message (owner -> requester s), built from the owner's sorted order:
+//   [u64 n_slots][u64 n_occ][u32 seg[n_slots + 1]][pad16][u32 list[n_occ]]
+// list = s's collision occurrences (its own send-order indices) grouped by
+// row, rows ascending, positions ascending within a row; seg = slot starts.
+__host__ __device__ __forceinline__ uint64_t grp_list_off(uint64_t n_slots) {
+  return kHdr + align16(4 * (n_slots + 1));
+}
+
+template <int NC_>
+struct GroupOp {
+  static constexpr int NC = NC_;  // 2 counters per source
+  const uint32_t* perm;           // sorted position -> occurrence j
+  const uint32_t* inverse;        // occurrence -> row slot u
+  const uint32_t* seg_start;      // row segments in sorted order
+  const uint8_t* occ_src;
+  const uint32_t* occ_idx;
+  const uint8_t* co;              // collision flag per row
+  Slots send;                     // GRP send slots
+  uint32_t* slot_us;              // [u][kMaxRanks] -> slot of (row, source)
+  __device__ void classify(uint64_t k, int& s, bool& is_co, bool& first) const {
+    const uint32_t j = perm[k];
+    const uint32_t u = inverse[j];
+    s = occ_src[j];
+    is_co = co[u] != 0;
+    first = is_co && (k == seg_start[u] || occ_src[perm[k - 1]] != s);
+  }
+  __device__ void count(uint64_t k, uint32_t (&c)[NC]) const {
+    int s;
+    bool is_co, first;
+    classify(k, s, is_co, first);
+#pragma unroll
+    for (int q = 0; q < NC / 2; ++q) {
+      c[2 * q] = (q == s && is_co) ? 1u : 0u;
+      c[2 * q + 1] = (q == s && first) ? 1u : 0u;
+    }
+  }
+  __device__ void emit(uint64_t k, const uint32_t (&ex)[NC], const uint32_t (&c)[NC],
+                       const uint32_t (&tot)[NC]) const {
+    int s;
+    bool is_co, first;
+    classify(k, s, is_co, first);
+    if (!is_co) return;
+    uint32_t r_occ = 0, r_slot = 0, n_slots = 0;
+#pragma unroll
+    for (int q = 0; q < NC / 2; ++q)
+      if (q == s) { r_occ = ex[2 * q]; r_slot = ex[2 * q + 1]; n_slots = tot[2 * q + 1]; }
+    char* msg = send.p[s];
+    reinterpret_cast<uint32_t*>(msg + grp_list_off(n_slots))[r_occ] = occ_idx[perm[k]];
+    if (first) {
+      reinterpret_cast<uint32_t*>(msg + kHdr)[r_slot] = r_occ;
+      slot_us[static_cast<uint64_t>(inverse[perm[k]]) * kMaxRanks + s] = r_slot;
+    }
+  }
+};
+
+// headers + closing seg entry: tot[2s] = n_occ, tot[2s+1] = n_slots
+static __global__ void k_grp_headers(Slots send, int p, const uint64_t* tot) {
+  const int s = threadIdx.x;
+  if (s < p) {
+    const uint64_t n_occ = tot[2 * s], n_slots = tot[2 * s + 1];
+    reinterpret_cast<uint64_t*>(send.p[s])[0] = n_slots;
+    reinterpret_cast<uint64_t*>(send.p[s])[1] = n_occ;
+    reinterpret_cast<uint32_t*>(send.p[s] + kHdr)[n_slots] = static_cast<uint32_t>(n_occ);
+  }
+}
+
+// requester: per-owner bases of the received GRP messages.
+// bases[0..p] slot prefix, bases[17..17+p] occurrence prefix, bases[34+d] = n_slots_d
+static __global__ void k_grp_bases(CSlots grp, int p, uint64_t* bases) {
+  if (threadIdx.x == 0) {
+    uint64_t s = 0, o = 0;
+    for (int d = 0; d < p; ++d) {
+      bases[d] = s;
+      bases[17 + d] = o;
+      const uint64_t ns = reinterpret_cast<const uint64_t*>(grp.p[d])[0];
+      bases[34 + d] = ns;
+      s += ns;
+      o += reinterpret_cast<const uint64_t*>(grp.p[d])[1];
+    }
+    bases[p] = s;
+    bases[17 + p] = o;
+    bases[16] = s;  // live segment count for the reduce
+  }
+}
+
+// requester: collision flag of every sent occurrence + the flattened segment
+// view (one segment per (owner, slot)) the chunked reduce consumes:
+// seg_flat[] (starts into perm_flat), perm_flat[] (batch positions),
+// out_ptr[] (the CO_G staging row each segment sum is written to)
+static __global__ void k_grp_flatten(CSlots grp, int p, uint64_t cap, const uint64_t* bases,
+                                     const uint64_t* send_off, const uint32_t* send_pos, Slots cog,
+                                     uint32_t row_bytes, uint8_t* flag, uint32_t* seg_flat,
+                                     uint32_t* perm_flat, char** out_ptr) {
+  const uint64_t total = static_cast<uint64_t>(p) * (cap + 1);
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const int d = static_cast<int>(i / (cap + 1));
+    const uint64_t q = i - static_cast<uint64_t>(d) * (cap + 1);
+    const char* m = grp.p[d];
+    const uint64_t n_slots = reinterpret_cast<const uint64_t*>(m)[0];
+    const uint64_t n_occ = reinterpret_cast<const uint64_t*>(m)[1];
+    const uint32_t* seg = reinterpret_cast<const uint32_t*>(m + kHdr);
+    const uint32_t* list = reinterpret_cast<const uint32_t*>(m + grp_list_off(n_slots));
+    if (q < n_slots) {
+      seg_flat[bases[d] + q] = static_cast<uint32_t>(bases[17 + d] + seg[q]);
+      out_ptr[bases[d] + q] = cog.p[d] + kHdr + q * row_bytes;
+    }
+    if (q < n_occ) {
+      const uint64_t k = send_off[d] + list[q];
+      flag[k] = 1;
+      perm_flat[bases[17 + d] + q] = send_pos[k];
+    }
+    if (d == p - 1 && q == 0) seg_flat[bases[p]] = static_cast<uint32_t>(bases[17 + p]);
+  }
+}
+
+// owner: collision rows get the sum of the sources' pre-summed rows, sources
+// in rank order, then row -= lr * acc (f64, one rounding)
+template <class T, int VE>
+__global__ void __launch_bounds__(128) k_co_apply(T* __restrict__ table, ShardGeom g, double lr,
+                                                   const uint64_t* __restrict__ uniq_local,
+                                                   const uint64_t* d_u, const uint8_t* __restrict__ co,
+                                                   const uint32_t* __restrict__ bits,
+                                                   const uint32_t* __restrict__ slot_us, CSlots cog,
+                                                   int p, DevErr* err) {
+  using V = VecOf<T, VE>;
+  const uint64_t U = *d_u;
+  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+  const uint64_t wid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const unsigned lane = threadIdx.x & 31u;
+  const uint32_t rb = g.dim * sizeof(T);
+  for (uint64_t u = wid; u < U; u += warps) {
+    if (!co[u]) continue;
+    const uint32_t b = bits[u];
+    const uint64_t l = uniq_local[u];
+    if (l >= g.local_rows) continue;
+    for (uint32_t col = lane * VE; col < g.dim; col += 32 * VE) {
+      double acc[VE];
+#pragma unroll
+      for (int x = 0; x < VE; ++x) acc[x] = 0.0;
+      for (int s = 0; s < p; ++s) {
+        if (!((b >> s) & 1u)) continue;
+        const uint32_t slot = slot_us[u * kMaxRanks + s];
+        const V v = *reinterpret_cast<const V*>(cog.p[s] + kHdr + static_cast<uint64_t>(slot) * rb +
+                                                col * sizeof(T));
+#pragma unroll
+        for (int x = 0; x < VE; ++x) acc[x] = __dadd_rn(acc[x], static_cast<double>(v.v[x]));
+      }
+      V* cell = reinterpret_cast<V*>(table + l * g.dim + col);
+      V r = *cell;
+      bool bad = false;
+#pragma unroll
+      for (int x = 0; x < VE; ++x) {
+        r.v[x] = static_cast<T>(__dsub_rn(static_cast<double>(r.v[x]), __dmul_rn(lr, acc[x])));
+        bad |= !isfinite(static_cast<double>(r.v[x]));
+      }
+      *cell = r;
+      if (bad) report(err, kErrNonFinite, l * static_cast<uint64_t>(g.p) + g.shard, 0);
+    }
+  }
+}
 
 }  // namespace fsx

@@ -331,6 +331,8 @@ struct SgdArgs {
   double* partials;           // [work items x dim] f64
   T* rows_out;                // nullable: post-update rows by slot [U x dim]
   DevErr* err;
+  char* const* seg_out;       // nullable: reduce-only mode — segment u's sum is
+                              // written (as T) to seg_out[u] instead of updating
 };
 
 // vector of VE elements of T moved as one 4/8/16-byte access
@@ -342,6 +344,13 @@ struct alignas(sizeof(T) * VE) VecOf {
 template <class T, int VE>
 __device__ __forceinline__ void sgd_apply_vec(const SgdArgs<T>& a, uint32_t u, uint32_t col,
                                               const double (&acc)[VE]) {
+  if (a.seg_out) {
+    VecOf<T, VE> r;
+#pragma unroll
+    for (int e = 0; e < VE; ++e) r.v[e] = static_cast<T>(acc[e]);
+    *reinterpret_cast<VecOf<T, VE>*>(reinterpret_cast<T*>(a.seg_out[u]) + col) = r;
+    return;
+  }
   const uint64_t l = a.rs.uniq_local[u];
   if (l >= a.g.local_rows) return;  // never write outside the shard
   VecOf<T, VE>* cell = reinterpret_cast<VecOf<T, VE>*>(a.table + l * a.g.dim + col);

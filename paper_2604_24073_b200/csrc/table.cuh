@@ -47,16 +47,18 @@ struct Table {
 
 // Segmented deterministic SGD over the rows of `rs` (selected rows only),
 // gradients from `gr`. Issues plan scan + chunk kernel + combine kernel.
+// seg_out != nullptr: reduce only — each segment's gradient sum (same
+// chunked association) goes to seg_out[u]; the table is not touched.
 template <class T>
 void sgd_update_rows(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_cap,
                      uint64_t occ_cap, const GradRows<T>& gr, uint32_t chunk, SgdScratch& s,
-                     T* rows_out, cudaStream_t stream) {
+                     T* rows_out, cudaStream_t stream, char* const* seg_out = nullptr) {
   if (rows_cap == 0) return;
   s.reserve(rows_cap, occ_cap, t.g.dim, chunk);
   SgdPlanOp plan{rs, chunk, s.work.p, s.multi.p, s.part_base.p};
   run_scan(ctx, plan, rows_cap, rs.d_u, s.scan, s.d_tot.p, stream);
   SgdArgs<T> a{static_cast<T*>(t.values), t.g, t.lr, rs, gr, chunk, s.work.p, s.d_tot.p,
-               s.multi.p, s.d_tot.p + 1, s.part_base.p, s.partials.p, rows_out, ctx->d_err};
+               s.multi.p, s.d_tot.p + 1, s.part_base.p, s.partials.p, rows_out, ctx->d_err, seg_out};
   const uint64_t work_cap = rows_cap + (chunk ? occ_cap / chunk + 1 : 0);
   const unsigned g2 = grid_for(ctx, rows_cap, 1, 8);
   const uint32_t rb = t.row_bytes();

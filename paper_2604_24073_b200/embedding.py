@@ -290,7 +290,7 @@ class _Engine:
     _mode = _lib.FSX_MODE_SYNC
 
     def __init__(self, shard: ShardView, comm=None, max_occurrences: int = 1 << 16,
-                 reduce_chunk: int = 0, transport: str = "ce"):
+                 reduce_chunk: int = 0, transport: str = "ce", presum: bool = False):
         from .comm import DeviceFabric
         self.shard = shard
         if comm is None:
@@ -299,7 +299,8 @@ class _Engine:
         if comm.world_size() != shard.geom.num_shards or comm.rank() != shard.shard_id:
             raise InvalidArgument("embedding: shard geometry does not match the communicator")
         tr = {"ce": _lib.FSX_TRANSPORT_CE, "nccl": _lib.FSX_TRANSPORT_NCCL}[transport]
-        cfg = _lib.EngineConfig(self._mode, tr, max_occurrences, reduce_chunk)
+        cfg = _lib.EngineConfig(self._mode, tr, max_occurrences, reduce_chunk,
+                                _lib.FSX_ENGINE_PRESUM if presum else 0)
         h = C.c_void_p()
         _lib.call("fsx_engine_create", shard.ctx.h, shard.h, C.byref(cfg), C.byref(h))
         self.h = h
@@ -314,6 +315,10 @@ class _Engine:
     def _ids(self, ids) -> torch.Tensor:
         return _dev_u64(ids, self.shard.ctx.torch_device)
 
+    def set_ids_ready(self, ready: bool = True) -> None:
+        """Device id tensors passed to forward are complete when passed."""
+        _lib.call("fsx_engine_set_ids_ready", self.h, int(ready))
+
     def set_profiling(self, on: bool = True) -> None:
         _lib.call("fsx_engine_set_profiling", self.h, int(on))
 
@@ -325,6 +330,13 @@ class _Engine:
             _lib.call("fsx_engine_phase_ms", self.h, k, C.byref(t), C.byref(n))
             out[name] = (t.value, n.value)
         return out
+
+    def spans(self, max_spans: int = 100000):
+        """[(phase, start_ms, end_ms)] of every recorded span (synchronizes)."""
+        buf = np.zeros(3 * max_spans, np.float64)
+        n = C.c_uint64()
+        _lib.call("fsx_engine_spans", self.h, buf.ctypes.data, max_spans, C.byref(n))
+        return [(_lib.PHASES[int(buf[3 * k])], buf[3 * k + 1], buf[3 * k + 2]) for k in range(n.value)]
 
     def exposed_ms(self) -> float:
         v = C.c_double()
@@ -379,11 +391,17 @@ class PrioritizedEmbedding(_Engine):
 
     def forward(self, ids_cur, ids_next=None, out: torch.Tensor | None = None,
                 stream=None) -> torch.Tensor:
-        c = self._ids(ids_cur)
-        nx = None if ids_next is None else self._ids(ids_next)
+        # pinned host tensors go to the engine as host pointers (side-lane H2D)
+        c = ids_cur.contiguous() if isinstance(ids_cur, torch.Tensor) and not ids_cur.is_cuda and \
+            ids_cur.is_pinned() else self._ids(ids_cur)
+        if isinstance(ids_next, torch.Tensor) and not ids_next.is_cuda and ids_next.is_pinned():
+            nx = ids_next.contiguous()
+        else:
+            nx = None if ids_next is None else self._ids(ids_next)
         n = c.numel()
         if out is None:
-            out = torch.empty((n, self.shard.geom.dim), dtype=self.shard.torch_dtype, device=c.device)
+            out = torch.empty((n, self.shard.geom.dim), dtype=self.shard.torch_dtype,
+                              device=self.shard.ctx.torch_device)
         _lib.call("fsx_engine_forward", self.h, _ptr(c), n, _ptr(nx),
                   0 if nx is None else nx.numel(), _ptr(out), _stream(stream))
         self._keep = [c, nx, out]

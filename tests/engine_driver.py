@@ -8,7 +8,7 @@ from paper_2604_24073_b200.comm import DeviceFabric
 
 
 def run_engine(prioritized, batches, geom, lr, seed, dtype="f64", reduce_chunk=0,
-               grad_scale=0.125, grad_shift=0.0625, devices=None, with_stats=False):
+               grad_scale=0.125, grad_shift=0.0625, devices=None, with_stats=False, presum=False):
     """batches[i][r] = rank r's ids of iteration i. Returns the final table
     (f64, global order) and rank 0's IterationStats (prioritized)."""
     world = geom.num_shards
@@ -23,8 +23,11 @@ def run_engine(prioritized, batches, geom, lr, seed, dtype="f64", reduce_chunk=0
         ctx = E.Context(dev, rank, world)
         shard = E.ShardView(geom, rank, lr, seed, dtype=dtype, ctx=ctx)
         comm = fabric.communicator(rank)
-        cls = E.PrioritizedEmbedding if prioritized else E.SynchronizedEmbedding
-        eng = cls(shard, comm, max_occurrences=cap, reduce_chunk=reduce_chunk)
+        if prioritized:
+            eng = E.PrioritizedEmbedding(shard, comm, max_occurrences=cap, reduce_chunk=reduce_chunk,
+                                         presum=presum)
+        else:
+            eng = E.SynchronizedEmbedding(shard, comm, max_occurrences=cap, reduce_chunk=reduce_chunk)
         stream = torch.cuda.Stream(device=dev)
         with torch.cuda.stream(stream):
             for i in range(iters):

@@ -118,6 +118,41 @@ def test_f64_chunked_reduce_close(drv, oracle):
     assert frel(got, want) < 1e-12
 
 
+def test_presum_golden_cases_close(drv, ENG):
+    """FSX_ENGINE_PRESUM on every golden case (1-8 ranks, odd dims, empty
+    batches): the collision gradients are summed per (source, row) first, so
+    the f64 tables differ from the reference only by reassociation."""
+    from paper_2604_24073_b200.embedding import TableGeometry
+    for name, c in ENG.items():
+        geom = TableGeometry(c["rows"], c["dim"], c["world"])
+        got, stats = drv.run_engine(True, c["batches"], geom, c["lr"], c["seed"], presum=True, with_stats=True)
+        assert frel(got, c["table"]) < 1e-12, name
+        st = np.array([[s.collision_rows, s.unique_next_rows, s.blocking_bytes] for s in stats], np.uint64)
+        assert np.array_equal(st, c["stats"]), name
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_presum_fp32_zipf_within_tolerance(drv, oracle, world):
+    """PRESUM on fp32 tables: deterministic (two runs bitwise equal), within
+    1e-6 normwise of the f64 reference, and the IterationStats (reference
+    accounting) identical to the exact protocol's."""
+    from paper_2604_24073_b200 import workload
+    from paper_2604_24073_b200.embedding import TableGeometry
+    rows, dim, iters = 50_000, 64, 4
+    batches = [[workload.zipf_batch(200 + r, 3000, rows, offset=3000 * i) for r in range(world)]
+               for i in range(iters)]
+    geom = TableGeometry(rows, dim, world)
+    a, st_a = drv.run_engine(True, batches, geom, 0.05, 3, dtype="f32", reduce_chunk=64, presum=True,
+                             with_stats=True)
+    b, _ = drv.run_engine(True, batches, geom, 0.05, 3, dtype="f32", reduce_chunk=64, presum=True)
+    assert np.array_equal(_bits(a), _bits(b))
+    _, st_x = drv.run_engine(True, batches, geom, 0.05, 3, dtype="f32", reduce_chunk=64, with_stats=True)
+    key = lambda st: [(s.collision_rows, s.unique_next_rows, s.blocking_bytes) for s in st]  # noqa: E731
+    assert key(st_a) == key(st_x)
+    want, _ = oracle.run_engine(world, batches, rows, dim, 0.05, 3)
+    assert float(np.max(np.abs(a - want)) / np.max(np.abs(want))) < 1e-6
+
+
 def test_protocol_order_errors(cuda):
     # test_embedding.cpp:329-342
     import torch

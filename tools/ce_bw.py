@@ -1,0 +1,83 @@
+"""Debug tool: copy-engine peer bandwidth on this box (one process, all GPUs).
+  1. one GPU -> one peer, message split into k chunks on k streams;
+  2. all-to-all: every GPU sends a message to every peer at once (one copy
+     stream per (src, dst)), k chunks each.
+Reports GB/s per sending GPU (bytes sent / time). Timed with CUDA events on
+the source device after warm-up."""
+import itertools
+import sys
+
+import torch
+from cuda.bindings import runtime as rt
+
+
+def time_copies(pairs, nbytes, k, reps=20):
+    """pairs: [(src, dst)]. Returns ms per round (max over source devices)."""
+    bufs = {}
+    streams = {}
+    for s, d in pairs:
+        bufs[(s, d)] = (torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{s}"),
+                        torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{d}"))
+        streams[(s, d)] = [torch.cuda.Stream(device=s) for _ in range(k)]
+    chunk = (nbytes + k - 1) // k
+
+    def round_():
+        for (s, d), (a, b) in bufs.items():
+            for j, st in enumerate(streams[(s, d)]):
+                lo, hi = j * chunk, min(nbytes, (j + 1) * chunk)
+                if lo < hi:
+                    err, = rt.cudaMemcpyPeerAsync(b.data_ptr() + lo, d, a.data_ptr() + lo, s, hi - lo,
+                                                  st.cuda_stream)
+                    assert err == rt.cudaError_t.cudaSuccess, err
+
+    for _ in range(3):
+        round_()
+    for dev in range(torch.cuda.device_count()):
+        torch.cuda.synchronize(dev)
+    srcs = sorted({s for s, _ in pairs})
+    ev = {s: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for s in srcs}
+    # start events on every copy stream's device: join all streams into a marker stream
+    for s in srcs:
+        with torch.cuda.device(s):
+            ev[s][0].record(torch.cuda.current_stream(s))
+            for (a, d), sts in streams.items():
+                if a == s:
+                    for st in sts:
+                        st.wait_event(ev[s][0])
+    for _ in range(reps):
+        round_()
+    for s in srcs:
+        with torch.cuda.device(s):
+            cur = torch.cuda.current_stream(s)
+            for (a, d), sts in streams.items():
+                if a == s:
+                    for st in sts:
+                        cur.wait_stream(st)
+            ev[s][1].record(cur)
+    for dev in range(torch.cuda.device_count()):
+        torch.cuda.synchronize(dev)
+    return max(ev[s][0].elapsed_time(ev[s][1]) for s in srcs) / reps
+
+
+def main():
+    n = torch.cuda.device_count()
+    print(f"{n} GPUs", flush=True)
+    for a, b in itertools.permutations(range(n), 2):
+        rt.cudaSetDevice(a)
+        rt.cudaDeviceEnablePeerAccess(b, 0)
+    for mb in (1, 4, 16, 64):
+        for k in (1, 2, 4, 8):
+            ms = time_copies([(0, 1)], mb << 20, k)
+            print(f"p2p 0->1 {mb:4d} MiB k={k}: {ms * 1e3:8.1f} us {(mb << 20) / ms / 1e6:8.1f} GB/s", flush=True)
+    if n > 2:
+        pairs = [(s, d) for s in range(n) for d in range(n) if s != d]
+        for mb in (1, 4, 16, 64):
+            for k in (1, 2, 4):
+                ms = time_copies(pairs, mb << 20, k)
+                out = (n - 1) * (mb << 20)
+                print(f"a2a x{n} {mb:4d} MiB/peer k={k}: {ms * 1e3:8.1f} us {out / ms / 1e6:8.1f} GB/s out per GPU",
+                      flush=True)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
