@@ -172,6 +172,7 @@ struct OwnBatch {  // owner view: occurrences received for this shard
   DevBuf<PackEntry> ex_list, co_list;
   DevBuf<uint32_t> rank_us;  // [unique row][kMaxRanks] position in each source's message
   DevBuf<uint32_t> slot_us;  // PRESUM: [unique row][kMaxRanks] slot in the GRP message
+  DevBuf<uint32_t> partner;  // collision row -> its row in the next owner batch
   SortedIds srt;
   ScanScratch scan;
   std::vector<uint64_t> h_recv, h_pack, h_mask;
@@ -185,6 +186,7 @@ struct OwnBatch {  // owner view: occurrences received for this shard
     co_list.alloc(cap);
     rank_us.alloc(cap * kMaxRanks);
     slot_us.alloc(cap * kMaxRanks);
+    partner.alloc(cap);
     srt.reserve(cap);
   }
   uint64_t* pack_tot() { return misc.p + 8; }
@@ -702,7 +704,7 @@ struct Engine {
     FSX_CUDA(cudaMemsetAsync(on.co.p, 0, on.m_cap, s));
     FSX_CUDA(cudaMemsetAsync(oc.misc.p, 0, 8, s));
     FSX_LAUNCH(ctx, k_intersect_flags, grid_for(ctx, oc.m_cap, 256, 8), 256, 0, s, oc.srt.uniq_g.p,
-               oc.srt.d_u(), on.srt.uniq_g.p, on.srt.d_u(), oc.co.p, on.co.p);
+               oc.srt.d_u(), on.srt.uniq_g.p, on.srt.d_u(), oc.co.p, on.co.p, oc.partner.p);
     FSX_LAUNCH(ctx, k_count_flags, grid_for(ctx, oc.m_cap, 256, 4), 256, 0, s, oc.co.p, oc.srt.d_u(),
                reinterpret_cast<unsigned long long*>(oc.misc.p));
     oc.has_co = true;
@@ -837,29 +839,38 @@ struct Engine {
   // the CO_G parity the coming backward will use (next_par is taken there)
   int cog_par_next() const { return static_cast<int>((seq[CH_COG] + 1) & 1u); }
 
-  // owner, PRESUM: collision rows from the sources' pre-summed rows
-  void co_apply(OwnBatch& oc, int cog_par, cudaStream_t s) {
+  // owner, PRESUM: collision rows from the sources' pre-summed rows; with
+  // `on` the E_co messages of the next iteration are packed in the same pass
+  void co_apply(OwnBatch& oc, int cog_par, cudaStream_t s, OwnBatch* on = nullptr, int cor_par = -1) {
     CSlots cog = recv_slots(CH_COG, cog_par);
+    EcoOut eco{};
+    eco.self = me;
+    if (on) {
+      eco = EcoOut{oc.partner.p, on->bits.p, on->rank_us.p, on->pack_tot(), on->srt.uniq_g.p,
+                   send_slots(CH_COR, cor_par), me};
+      FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, eco.send, p, on->pack_tot() + 1, 2, cap, ctx->d_err);
+    }
     const unsigned grid = grid_for(ctx, oc.m_cap, 4, 16);
     const bool v16 = rb % 16 == 0;
+#define FSX_CO_APPLY_P(T, VE, P)                                                                     \
+  FSX_LAUNCH(ctx, (k_co_apply<T, VE, P>), grid, 128, 0, s, static_cast<T*>(t->values), t->g, t->lr,   \
+             oc.srt.uniq.p, oc.srt.d_u(), oc.co.p, oc.bits.p, oc.slot_us.p, cog, p, eco, ctx->d_err)
+#define FSX_CO_APPLY(T, VE)                                    \
+  do {                                                         \
+    if (p <= 2) FSX_CO_APPLY_P(T, VE, 2);                      \
+    else if (p <= 4) FSX_CO_APPLY_P(T, VE, 4);                 \
+    else if (p <= 8) FSX_CO_APPLY_P(T, VE, 8);                 \
+    else FSX_CO_APPLY_P(T, VE, 16);                            \
+  } while (0)
     if (t->dtype == FSX_F32) {
-      if (v16)
-        FSX_LAUNCH(ctx, (k_co_apply<float, 4>), grid, 128, 0, s, static_cast<float*>(t->values), t->g, t->lr,
-                   oc.srt.uniq.p, oc.srt.d_u(), oc.co.p, oc.bits.p, oc.slot_us.p, cog, p, ctx->d_err);
-      else
-        FSX_LAUNCH(ctx, (k_co_apply<float, 1>), grid, 128, 0, s, static_cast<float*>(t->values), t->g, t->lr,
-                   oc.srt.uniq.p, oc.srt.d_u(), oc.co.p, oc.bits.p, oc.slot_us.p, cog, p, ctx->d_err);
+      if (v16) FSX_CO_APPLY(float, 4); else FSX_CO_APPLY(float, 1);
     } else {
-      if (v16)
-        FSX_LAUNCH(ctx, (k_co_apply<double, 2>), grid, 128, 0, s, static_cast<double*>(t->values), t->g, t->lr,
-                   oc.srt.uniq.p, oc.srt.d_u(), oc.co.p, oc.bits.p, oc.slot_us.p, cog, p, ctx->d_err);
-      else
-        FSX_LAUNCH(ctx, (k_co_apply<double, 1>), grid, 128, 0, s, static_cast<double*>(t->values), t->g, t->lr,
-                   oc.srt.uniq.p, oc.srt.d_u(), oc.co.p, oc.bits.p, oc.slot_us.p, cog, p, ctx->d_err);
+      if (v16) FSX_CO_APPLY(double, 2); else FSX_CO_APPLY(double, 1);
     }
+#undef FSX_CO_APPLY_P
+#undef FSX_CO_APPLY
   }
 
-  // requester: split grads into CO_G / EX_G messages (embedding.cpp:526-536)
   // collision half first (its chain is the exposed one), then the exclusive
   // half, which overlaps the collision all-to-all
   void split_co(ReqBatch& r, const void* d_grads, int cog_par, cudaStream_t s) {
@@ -1072,6 +1083,7 @@ struct Engine {
     OwnBatch& oc = O(i);
     cudaEvent_t ev_chain_start = nullptr;
     bool have_grads = false;
+    int fused_cor = -1;  // E_co packed by the collision update itself
     if (i == 0) {
       update_blocking(rc, oc, grads, c);  // bootstrap: one synchronized update
       ev_chain_start = record(c);
@@ -1096,7 +1108,13 @@ struct Engine {
             a2a(CH_COG, cog, bytes, hi);
           }
           Span sp(this, FSX_PHASE_CO_UPDATE, hi);
-          co_apply(oc, cog, hi);
+          if (has_next && p > 1) {
+            wait(hi, ev_next_ready);
+            fused_cor = next_par(CH_COR);
+            co_apply(oc, cog, hi, &O(i + 1), fused_cor);
+          } else {
+            co_apply(oc, cog, hi);
+          }
         } else {
           if (p > 1) {
             std::vector<uint64_t> bytes(p);
@@ -1114,7 +1132,15 @@ struct Engine {
       ReqBatch& rn = R(i + 1);
       wait(hi, ev_chain_start);
       wait(hi, ev_next_ready);
-      rn.cor_par = send_eco(on, hi);
+      if (fused_cor >= 0) {
+        Span sp(this, FSX_PHASE_ECO, hi);
+        std::vector<uint64_t> bytes(p);
+        for (int d = 0; d < p; ++d) bytes[d] = idrows_rows_off(on.h_pack[2 * d + 1]) + rb * on.h_pack[2 * d + 1];
+        a2a(CH_COR, fused_cor, bytes, hi);
+        rn.cor_par = fused_cor;
+      } else {
+        rn.cor_par = send_eco(on, hi);
+      }
       cur_co_ready = record(hi);
       stats_backward(i, have_grads, true, rc, oc, on, rn.cor_par, hi);
     } else {

@@ -536,14 +536,27 @@ static __global__ void k_grp_flatten(CSlots grp, int p, uint64_t cap, const uint
 }
 
 // owner: collision rows get the sum of the sources' pre-summed rows, sources
-// in rank order, then row -= lr * acc (f64, one rounding)
-template <class T, int VE>
+// in rank order, then row -= lr * acc (f64, one rounding). Fused E_co pack
+// (eco.partner != nullptr): the updated row is also written straight into the
+// E_co message of every next-iteration requester of that row (the same bytes
+// IdRowPackMap would copy out of the table afterwards).
+struct EcoOut {
+  const uint32_t* partner;   // oc row -> row of the next owner batch; nullable: no E_co
+  const uint32_t* bits;      // next batch: requester bits per row
+  const uint32_t* rank_us;   // next batch: position of the row in each requester's E_co
+  const uint64_t* totals;    // next batch pack totals: [2s+1] = E_co rows for s
+  const uint64_t* uniq_g;    // next batch: global id per row
+  Slots send;                // COR send slots
+  int self;
+};
+
+template <class T, int VE, int P>  // P >= p: per-source registers
 __global__ void __launch_bounds__(128) k_co_apply(T* __restrict__ table, ShardGeom g, double lr,
                                                    const uint64_t* __restrict__ uniq_local,
                                                    const uint64_t* d_u, const uint8_t* __restrict__ co,
                                                    const uint32_t* __restrict__ bits,
                                                    const uint32_t* __restrict__ slot_us, CSlots cog,
-                                                   int p, DevErr* err) {
+                                                   int p, EcoOut eco, DevErr* err) {
   using V = VecOf<T, VE>;
   const uint64_t U = *d_u;
   const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
@@ -555,18 +568,44 @@ __global__ void __launch_bounds__(128) k_co_apply(T* __restrict__ table, ShardGe
     const uint32_t b = bits[u];
     const uint64_t l = uniq_local[u];
     if (l >= g.local_rows) continue;
+    // lane s < p: this row's slot in source s's CO_G message (and, fused,
+    // its position in requester s's E_co message); broadcast before the
+    // column loop, which only some lanes enter when dim < 32 * VE
+    const bool in_b = lane < static_cast<unsigned>(p) && ((b >> lane) & 1u);
+    const uint32_t my_slot = in_b ? slot_us[u * kMaxRanks + lane] : 0u;
+    uint32_t nb = 0, npos = 0;
+    if (eco.partner) {
+      const uint32_t un = eco.partner[u];
+      nb = eco.bits[un] & ~(1u << eco.self);
+      const bool in_nb = lane < static_cast<unsigned>(p) && ((nb >> lane) & 1u);
+      if (in_nb) {
+        npos = eco.rank_us[un * kMaxRanks + lane];
+        reinterpret_cast<uint64_t*>(eco.send.p[lane] + kHdr)[npos] = eco.uniq_g[un];
+      }
+    }
+    uint32_t slot[P], pos[P];
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      slot[s] = __shfl_sync(0xffffffffu, my_slot, s);
+      pos[s] = __shfl_sync(0xffffffffu, npos, s);
+    }
     for (uint32_t col = lane * VE; col < g.dim; col += 32 * VE) {
+      // issue every source's load before the ordered sum
+      V v[P];
+#pragma unroll
+      for (int s = 0; s < P; ++s)
+        if (s < p && ((b >> s) & 1u))
+          v[s] = *reinterpret_cast<const V*>(cog.p[s] + kHdr + static_cast<uint64_t>(slot[s]) * rb +
+                                             col * sizeof(T));
       double acc[VE];
 #pragma unroll
       for (int x = 0; x < VE; ++x) acc[x] = 0.0;
-      for (int s = 0; s < p; ++s) {
-        if (!((b >> s) & 1u)) continue;
-        const uint32_t slot = slot_us[u * kMaxRanks + s];
-        const V v = *reinterpret_cast<const V*>(cog.p[s] + kHdr + static_cast<uint64_t>(slot) * rb +
-                                                col * sizeof(T));
 #pragma unroll
-        for (int x = 0; x < VE; ++x) acc[x] = __dadd_rn(acc[x], static_cast<double>(v.v[x]));
-      }
+      for (int s = 0; s < P; ++s)
+        if (s < p && ((b >> s) & 1u)) {
+#pragma unroll
+          for (int x = 0; x < VE; ++x) acc[x] = __dadd_rn(acc[x], static_cast<double>(v[s].v[x]));
+        }
       V* cell = reinterpret_cast<V*>(table + l * g.dim + col);
       V r = *cell;
       bool bad = false;
@@ -577,6 +616,11 @@ __global__ void __launch_bounds__(128) k_co_apply(T* __restrict__ table, ShardGe
       }
       *cell = r;
       if (bad) report(err, kErrNonFinite, l * static_cast<uint64_t>(g.p) + g.shard, 0);
+#pragma unroll
+      for (int s = 0; s < P; ++s)
+        if (s < p && ((nb >> s) & 1u))
+          *reinterpret_cast<V*>(eco.send.p[s] + idrows_rows_off(eco.totals[2 * s + 1]) +
+                                static_cast<uint64_t>(pos[s]) * rb + col * sizeof(T)) = r;
     }
   }
 }

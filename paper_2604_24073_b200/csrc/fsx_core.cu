@@ -60,7 +60,8 @@ void Ctx::check_error(cudaStream_t s) {
 // ---- K3 ----------------------------------------------------------------------
 __global__ void k_intersect_flags(const uint64_t* __restrict__ a, const uint64_t* d_na,
                                   const uint64_t* __restrict__ b, const uint64_t* d_nb,
-                                  uint8_t* __restrict__ flag_a, uint8_t* __restrict__ flag_b) {
+                                  uint8_t* __restrict__ flag_a, uint8_t* __restrict__ flag_b,
+                                  uint32_t* __restrict__ partner_a) {
   const uint64_t na = *d_na, nb = *d_nb;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < na;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -73,6 +74,7 @@ __global__ void k_intersect_flags(const uint64_t* __restrict__ a, const uint64_t
     const bool hit = lo < nb && b[lo] == x;
     flag_a[i] = hit ? 1 : 0;
     if (hit && flag_b) flag_b[lo] = 1;
+    if (hit && partner_a) partner_a[i] = static_cast<uint32_t>(lo);
   }
 }
 

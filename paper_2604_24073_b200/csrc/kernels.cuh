@@ -226,7 +226,8 @@ struct OwnerPartitionOp {
 // a, b sorted unique. flag_a[i] = a[i] in b; flag_b[j] = b[j] in a.
 __global__ void k_intersect_flags(const uint64_t* __restrict__ a, const uint64_t* d_na,
                                   const uint64_t* __restrict__ b, const uint64_t* d_nb,
-                                  uint8_t* __restrict__ flag_a, uint8_t* __restrict__ flag_b);
+                                  uint8_t* __restrict__ flag_a, uint8_t* __restrict__ flag_b,
+                                  uint32_t* __restrict__ partner_a = nullptr);
 
 // compaction of a sorted list by a byte flag: out_true / out_false keep order
 struct SplitByFlagOp {
