@@ -13,7 +13,7 @@ import threading
 from . import errors
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfsx.so")
+LIB_PATH = os.environ.get("FSX_LIB") or os.path.join(HERE, "libfsx.so")
 CSRC = os.path.join(HERE, "csrc")
 
 FSX_F32, FSX_F64 = 0, 1

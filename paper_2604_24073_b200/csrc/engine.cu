@@ -15,6 +15,7 @@
 // (cuStreamWriteValue32 after each copy-engine copy, cuStreamWaitValue32 on
 // the receiving lane) — no SM ever spins and no kernel touches a peer.
 #include <algorithm>
+#include <numeric>
 #include <deque>
 #include <functional>
 #include <thread>
@@ -27,6 +28,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <numeric>
 #include <vector>
 
 #include <dlfcn.h>
@@ -636,18 +638,22 @@ struct Engine {
   }
 
   // full-row deterministic update of an owner batch from a grads channel
+  // self_grads != nullptr: this rank's own occurrences read the caller's
+  // gradient rows in place (row self_pos[e] for element e of its own message)
   void update(OwnBatch& o, int ch, int par, const uint8_t* select, uint8_t want, bool by_rank,
-              cudaStream_t s, int phase = FSX_PHASE_UPDATE) {
+              cudaStream_t s, int phase = FSX_PHASE_UPDATE, const void* self_grads = nullptr,
+              const uint32_t* self_pos = nullptr) {
     Span sp(this, phase, s);
     RowSegments rs{o.srt.uniq.p, o.srt.seg_start.p, o.srt.perm, o.srt.d_u(), select, want};
     const uint64_t m = o.m_cap;
+    const char* sb = static_cast<const char*>(self_grads);
     if (t->dtype == FSX_F32) {
       GradRows<float> gr{recv_slot(ch, par, 0) + kHdr, ch_slot[ch], o.occ_src.p,
-                         by_rank ? o.occ_rank.p : o.occ_idx.p, rb};
+                         by_rank ? o.occ_rank.p : o.occ_idx.p, rb, sb, self_pos, sb ? me : -1};
       sgd_update_rows<float>(ctx, *t, rs, m, m, gr, cfg.reduce_chunk, sgd_for(s), nullptr, s);
     } else {
       GradRows<double> gr{recv_slot(ch, par, 0) + kHdr, ch_slot[ch], o.occ_src.p,
-                          by_rank ? o.occ_rank.p : o.occ_idx.p, rb};
+                          by_rank ? o.occ_rank.p : o.occ_idx.p, rb, sb, self_pos, sb ? me : -1};
       sgd_update_rows<double>(ctx, *t, rs, m, m, gr, cfg.reduce_chunk, sgd_for(s), nullptr, s);
     }
   }
@@ -677,14 +683,20 @@ struct Engine {
   }
 
   // requester grads -> GRADS -> owner full update (embedding.cpp:276-295)
+  // The gradients of this rank's own rows are never staged: the update reads
+  // them from the caller's buffer (valid for the whole call: the update runs
+  // on the caller's stream).
   void update_blocking(ReqBatch& r, OwnBatch& o, const void* d_grads, cudaStream_t s) {
     Span sp(this, FSX_PHASE_UPDATE, s);
     const int par = next_par(CH_GRADS);
     Slots send = send_slots(CH_GRADS, par);
-    GradPackMap gm{static_cast<const char*>(d_grads), r.send_pos.p, r.send_dst.p, r.send_off(),
-                   nullptr, nullptr, send, send, rb, 0};
-    launch_copy_rows(ctx, gm, r.n, nullptr, rb, s);
-    FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, r.tot.p, 1, cap, ctx->d_err);
+    const uint64_t self_off = p > 1 ? std::accumulate(r.h_send.begin(), r.h_send.begin() + me, uint64_t{0}) : 0;
+    if (p > 1) {
+      GradPackMap gm{static_cast<const char*>(d_grads), r.send_pos.p, r.send_dst.p, r.send_off(),
+                     nullptr, nullptr, send, send, rb, 0, me};
+      launch_copy_rows(ctx, gm, r.n, nullptr, rb, s);
+      FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, r.tot.p, 1, cap, ctx->d_err);
+    }
     if (p > 1) {
       std::vector<uint64_t> bytes(p), rbytes(p);
       for (int d = 0; d < p; ++d) {
@@ -693,7 +705,7 @@ struct Engine {
       }
       a2a(CH_GRADS, par, bytes, s, &rbytes);
     }
-    update(o, CH_GRADS, par, nullptr, 0, false, s);
+    update(o, CH_GRADS, par, nullptr, 0, false, s, FSX_PHASE_UPDATE, d_grads, r.send_pos.p + self_off);
   }
 
   // ---- prioritized building blocks ----------------------------------------------------
@@ -711,11 +723,15 @@ struct Engine {
     on.has_co = false;
     if (p == 1) {
       // single rank: every message would go to self, and self rows are
-      // merged straight from the table — no pack lists, no copies. The
-      // merge must still see the deferred exclusive update first.
+      // merged straight from the table — no pack lists, no copies. IDX still
+      // carries each occurrence's collision bit (the merge's two halves).
+      // The merge must see the deferred exclusive update first.
+      const int ipar = next_par(CH_IDX);
+      FSX_LAUNCH(ctx, k_idx_pack, grid_for(ctx, on.m_cap, 256, 8), 256, 0, s, on.srt.inverse.p, on.occ_src.p,
+                 on.occ_idx.p, on.srt.d_n(), on.rank_us.p, on.co.p, send_slots(CH_IDX, ipar), me);
       wait(s, ev_ex_applied);
       rn.ex_par = -1;
-      rn.idx_par = -1;
+      rn.idx_par = ipar;
       return;
     }
     // pack lists over next's unique rows: ex -> E_ex now, co -> E_co later
@@ -931,6 +947,7 @@ struct Engine {
   // requester: merge E_ex / E_co into batch-major rows (embedding.cpp:453-484)
   void merge(ReqBatch& r, void* d_out, cudaStream_t s, int part = 0) {
     Span sp(this, FSX_PHASE_MERGE, s);
+    if (r.idx_par < 0) raise(FSX_ERR_PROTOCOL, "embedding: merge without IDX messages");
     CSlots co{};
     if (p > 1) co = r.cor_par >= 0 ? recv_slots(CH_COR, r.cor_par) : recv_slots(CH_EX, r.ex_par);
     MergeMap mm{recv_slots(CH_IDX, r.idx_par), recv_slots(CH_EX, r.ex_par), co,
@@ -1088,6 +1105,15 @@ struct Engine {
       update_blocking(rc, oc, grads, c);  // bootstrap: one synchronized update
       ev_chain_start = record(c);
       has_pending = false;
+    } else if (p == 1) {
+      // single rank: nothing to hide behind a transfer, so the whole update
+      // (collision rows first in row order is immaterial: rows are disjoint)
+      // runs at once on the caller's stream, reading the gradients in place
+      exposed_wait(c, {ev_mask});
+      update(oc, CH_GRADS, 0, nullptr, 0, false, c, FSX_PHASE_CO_UPDATE, grads, rc.send_pos.p);
+      ev_chain_start = record(c);
+      has_pending = false;
+      have_grads = true;
     } else {
       exposed_wait(c, {ev_mask});
       const int cog = next_par(CH_COG);

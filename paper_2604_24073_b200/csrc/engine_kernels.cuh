@@ -330,9 +330,11 @@ struct GradPackMap {
   Slots co, ex;
   uint32_t row_bytes;
   int part;                   // 0: every row; 1: exclusive only; 2: collision only
+  int skip_dst = -1;          // rows for this owner are not staged (read in place)
   __device__ const char* src(uint64_t k) const {
     const bool f = flag && flag[k];
     if ((part == 1 && f) || (part == 2 && !f)) return nullptr;
+    if (send_dst[k] == skip_dst) return nullptr;
     return grads + static_cast<uint64_t>(send_pos[k]) * row_bytes;
   }
   __device__ char* dst(uint64_t k) const {

@@ -78,12 +78,14 @@ __device__ __forceinline__ uint32_t ldg_nc(const uint32_t* p) { return __ldg(p);
 // kernel, which every caller guarantees.
 
 // Copy `row_bytes` for each item i in [0, n): dst(i) <- src(i). A Map returns
-// nullptr from src() to skip an item. One warp per item, kRowsPerWarp items in
-// flight per warp.
-constexpr int kRowsPerWarp = 4;
+// nullptr from src() to skip an item. Each warp takes 32 items per round: lane
+// j resolves item base+j (the Map's index chain, once per item, 32 chains in
+// parallel), then the warp copies the live rows kRowsPerWarp at a time with
+// every row's loads in flight before the stores.
+constexpr int kRowsPerWarp = 8;
 
 template <class Map, int VB>
-__global__ void __launch_bounds__(256) k_copy_rows(Map map, uint64_t n_cap, const uint64_t* d_n,
+__global__ void __launch_bounds__(256, 4) k_copy_rows(Map map, uint64_t n_cap, const uint64_t* d_n,
                                                    uint32_t row_bytes) {
   using V = typename VecT<VB>::type;
   const uint64_t n = scan_n(n_cap, d_n);
@@ -91,27 +93,36 @@ __global__ void __launch_bounds__(256) k_copy_rows(Map map, uint64_t n_cap, cons
   const uint64_t wid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const unsigned lane = threadIdx.x & 31u;
   const uint32_t nvec = row_bytes / VB;
-  for (uint64_t i0 = wid * kRowsPerWarp; i0 < n; i0 += warps * kRowsPerWarp) {
-    const V* src[kRowsPerWarp];
-    V* dst[kRowsPerWarp];
-#pragma unroll
-    for (int r = 0; r < kRowsPerWarp; ++r) {
-      const uint64_t i = i0 + r;
-      src[r] = nullptr;
-      dst[r] = nullptr;
-      if (i < n) {
-        src[r] = reinterpret_cast<const V*>(map.src(i));
-        if (src[r]) dst[r] = reinterpret_cast<V*>(map.dst(i));
-      }
+  for (uint64_t base = wid * 32; base < n; base += warps * 32) {
+    const uint64_t i = base + lane;
+    const V* s = nullptr;
+    V* d = nullptr;
+    if (i < n) {
+      s = reinterpret_cast<const V*>(map.src(i));
+      if (s) d = reinterpret_cast<V*>(map.dst(i));
     }
-    for (uint32_t c = lane; c < nvec; c += 32) {
-      V v[kRowsPerWarp];
+    unsigned live = __ballot_sync(0xffffffffu, s != nullptr);
+    while (live) {
+      const V* src[kRowsPerWarp];
+      V* dst[kRowsPerWarp];
 #pragma unroll
-      for (int r = 0; r < kRowsPerWarp; ++r)
-        if (src[r]) v[r] = ldg_nc(src[r] + c);
+      for (int r = 0; r < kRowsPerWarp; ++r) {
+        const int j = live ? __ffs(live) - 1 : 0;
+        const bool ok = live != 0;
+        live &= live - 1;
+        src[r] = reinterpret_cast<const V*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(s), j));
+        dst[r] = reinterpret_cast<V*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(d), j));
+        if (!ok) src[r] = nullptr;
+      }
+      for (uint32_t c = lane; c < nvec; c += 32) {
+        V v[kRowsPerWarp];
 #pragma unroll
-      for (int r = 0; r < kRowsPerWarp; ++r)
-        if (src[r]) dst[r][c] = v[r];
+        for (int r = 0; r < kRowsPerWarp; ++r)
+          if (src[r]) v[r] = ldg_nc(src[r] + c);
+#pragma unroll
+        for (int r = 0; r < kRowsPerWarp; ++r)
+          if (src[r]) dst[r][c] = v[r];
+      }
     }
   }
 }
@@ -126,7 +137,7 @@ template <class Map>
 void launch_copy_rows(Ctx* ctx, const Map& map, uint64_t n_cap, const uint64_t* d_n,
                       uint32_t row_bytes, cudaStream_t s) {
   if (n_cap == 0) return;
-  const unsigned grid = grid_for(ctx, n_cap, 8 * kRowsPerWarp, 8);
+  const unsigned grid = grid_for(ctx, n_cap, 8 * 32, 4);
   switch (vec_bytes_for(row_bytes)) {
     case 16: FSX_LAUNCH(ctx, (k_copy_rows<Map, 16>), grid, 256, 0, s, map, n_cap, d_n, row_bytes); break;
     case 8: FSX_LAUNCH(ctx, (k_copy_rows<Map, 8>), grid, 256, 0, s, map, n_cap, d_n, row_bytes); break;
@@ -268,10 +279,17 @@ struct GradRows {
   const uint8_t* occ_src;   // nullable: source slot of occurrence j
   const uint32_t* occ_idx;  // nullable: row of occurrence j inside its slot
   uint32_t row_bytes;
+  // nullable: occurrences from source `self_src` read the caller's gradient
+  // rows directly (row self_pos[r] of self_base) instead of a staged copy
+  const char* self_base = nullptr;
+  const uint32_t* self_pos = nullptr;
+  int self_src = -1;
   __device__ __forceinline__ const T* row(uint32_t j) const {
-    const uint64_t off = occ_src ? static_cast<uint64_t>(occ_src[j]) * slot_bytes : 0;
+    const int s = occ_src ? occ_src[j] : 0;
     const uint64_t r = occ_idx ? occ_idx[j] : j;
-    return reinterpret_cast<const T*>(base + off + r * row_bytes);
+    if (self_base && s == self_src)
+      return reinterpret_cast<const T*>(self_base + static_cast<uint64_t>(self_pos[r]) * row_bytes);
+    return reinterpret_cast<const T*>(base + static_cast<uint64_t>(s) * slot_bytes + r * row_bytes);
   }
 };
 
@@ -284,37 +302,89 @@ struct RowSegments {
   uint8_t want;
 };
 
-// Work list: every selected row contributes ceil(len / chunk) items (1 when
-// chunk == 0); multi-chunk rows are also listed for the combine pass.
+// Work lists. A selected row with exactly one occurrence becomes a "single"
+// (a pure gather-update: gradient row -> destination row); any other row
+// contributes ceil(len / chunk) items (1 when chunk == 0 or len <= chunk),
+// and multi-chunk rows are listed for the combine pass. Items are emitted
+// fully resolved — occurrence range, first gradient row, destination row —
+// so the update kernels' index chains start at the item itself.
+struct SgdItem {
+  uint32_t u, q, kb, ke;  // row slot, chunk index (bit 31: single-chunk row), occurrence range
+  char* dst;              // single-chunk rows: destination row; nullptr: none
+  const char* g0;         // gradient row of occurrence kb
+};
+constexpr uint32_t kSgdSingleChunk = 0x80000000u;
+
 struct SgdPlanOp {
-  static constexpr int NC = 3;
+  static constexpr int NC = 4;
   RowSegments rs;
   uint32_t chunk;
-  uint2* work;          // (row, chunk index)
+  SgdItem* singles;     // one-occurrence rows
+  SgdItem* work;        // every other row / chunk
   uint32_t* multi;      // rows with > 1 chunk
-  uint32_t* part_base;  // first work item of row u (indexes partials)
-  __device__ uint32_t nchunks(uint64_t u) const {
-    if (rs.select && rs.select[u] != rs.want) return 0;
-    const uint32_t len = rs.seg_start[u + 1] - rs.seg_start[u];
-    if (chunk == 0 || len <= chunk) return 1;
-    return (len + chunk - 1) / chunk;
+  uint32_t* part_base;  // first partial slot of row u
+  char* table;          // table base (row pitch row_bytes)
+  uint32_t row_bytes;
+  uint64_t local_rows;
+  char* const* seg_out; // nullable: reduce-only destinations
+  const char* const* gptr;  // gradient row per sorted occurrence
+  __device__ uint32_t len(uint64_t u) const { return rs.seg_start[u + 1] - rs.seg_start[u]; }
+  __device__ bool selected(uint64_t u) const { return !rs.select || rs.select[u] == rs.want; }
+  // c0: singles, c1: work items, c2: multi-chunk rows, c3: partial slots
+  __device__ void count(uint64_t u, uint32_t (&c)[4]) const {
+    c[0] = c[1] = c[2] = c[3] = 0;
+    if (!selected(u)) return;
+    const uint32_t n = len(u);
+    if (n == 1) { c[0] = 1; return; }
+    const uint32_t k = (chunk == 0 || n <= chunk) ? 1u : (n + chunk - 1) / chunk;
+    c[1] = k;
+    c[2] = k > 1 ? 1u : 0u;
+    c[3] = k > 1 ? k : 0u;
   }
-  // c0: work items, c1: multi-chunk rows, c2: partial slots (multi rows only)
-  __device__ void count(uint64_t u, uint32_t (&c)[3]) const {
-    const uint32_t k = nchunks(u);
-    c[0] = k;
-    c[1] = k > 1 ? 1u : 0u;
-    c[2] = k > 1 ? k : 0u;
-  }
-  __device__ void emit(uint64_t u, const uint32_t (&ex)[3], const uint32_t (&c)[3],
-                       const uint32_t (&tot)[3]) const {
-    for (uint32_t q = 0; q < c[0]; ++q) work[ex[0] + q] = make_uint2(static_cast<uint32_t>(u), q);
-    if (c[1]) {
-      multi[ex[1]] = static_cast<uint32_t>(u);
-      part_base[u] = ex[2];
+  __device__ void emit(uint64_t u, const uint32_t (&ex)[4], const uint32_t (&c)[4],
+                       const uint32_t (&tot)[4]) const {
+    if (c[0] == 0 && c[1] == 0) return;
+    const uint32_t s = rs.seg_start[u], e = rs.seg_start[u + 1];
+    char* dst = nullptr;
+    if (c[0] == 1 || c[1] == 1) {
+      if (seg_out) {
+        dst = seg_out[u];
+      } else {
+        const uint64_t l = rs.uniq_local[u];
+        dst = l < local_rows ? table + l * row_bytes : nullptr;  // never outside the shard
+      }
+    }
+    if (c[0]) {
+      singles[ex[0]] = SgdItem{static_cast<uint32_t>(u), kSgdSingleChunk, s, e, dst, gptr[s]};
+      return;
+    }
+    if (c[1] == 1) {
+      work[ex[1]] = SgdItem{static_cast<uint32_t>(u), kSgdSingleChunk, s, e, dst, gptr[s]};
+    } else {
+      // chunks of a hot row: plain stores (no dependent loads in this loop)
+      for (uint32_t q = 0; q < c[1]; ++q) {
+        const uint32_t kb = s + q * chunk;
+        work[ex[1] + q] = SgdItem{static_cast<uint32_t>(u), q, kb, min(e, kb + chunk), nullptr, nullptr};
+      }
+    }
+    if (c[2]) {
+      multi[ex[2]] = static_cast<uint32_t>(u);
+      part_base[u] = ex[3];
     }
   }
 };
+
+// Gradient row of every occurrence in sorted order (perm -> source / rank ->
+// row), resolved once by a fully parallel pass
+template <class T>
+__global__ void k_grad_ptrs(GradRows<T> gr, const uint32_t* __restrict__ perm,
+                            const uint32_t* __restrict__ seg_start, const uint64_t* d_u,
+                            const T** __restrict__ gptr) {
+  const uint64_t n = seg_start[*d_u];
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    gptr[k] = gr.row(perm[k]);
+}
 
 template <class T>
 struct SgdArgs {
@@ -324,16 +394,19 @@ struct SgdArgs {
   RowSegments rs;
   GradRows<T> gr;
   uint32_t chunk;
-  const uint2* work;
-  const uint64_t* d_work_n;   // device: number of work items (scan total 0)
+  const SgdItem* singles;
+  const uint64_t* d_single_n; // device: number of one-occurrence rows (scan total 0)
+  const SgdItem* work;
+  const uint64_t* d_work_n;   // device: number of work items (scan total 1)
   const uint32_t* multi;
-  const uint64_t* d_multi_n;  // device: number of multi-chunk rows (scan total 1)
+  const uint64_t* d_multi_n;  // device: number of multi-chunk rows (scan total 2)
   const uint32_t* part_base;
   double* partials;           // [work items x dim] f64
   T* rows_out;                // nullable: post-update rows by slot [U x dim]
   DevErr* err;
   char* const* seg_out;       // nullable: reduce-only mode — segment u's sum is
                               // written (as T) to seg_out[u] instead of updating
+  const T* const* gptr;       // gradient row per sorted occurrence (k_grad_ptrs)
 };
 
 // vector of VE elements of T moved as one 4/8/16-byte access
@@ -369,87 +442,129 @@ __device__ __forceinline__ void sgd_apply_vec(const SgdArgs<T>& a, uint32_t u, u
   if (bad) report(a.err, kErrNonFinite, l * static_cast<uint64_t>(a.g.p) + a.g.shard, 0);
 }
 
-// One warp per (work item, column block): a work item is a row, or one
-// `chunk`-occurrence slice of a hot row; blockIdx.y picks the 32*VE*NV-column
-// block (16-byte loads when the row pitch allows). Splitting columns across
-// warps keeps per-warp registers small, so more warps (and more independent
-// 16-byte loads) are in flight to hide the index -> gradient latency chain.
-// The occurrence loop is unrolled 4-wide with all loads issued before the
-// in-order f64 adds.
-template <class T, int VE, int NV>
-__global__ void __launch_bounds__(128, 8) k_sgd_chunks(SgdArgs<T> a) {
+// Store of one updated vector into a resolved destination row `dst`
+// (table row, or seg_out row in reduce-only mode); `old` = the row's current
+// value (table mode). Same arithmetic as sgd_apply_vec.
+template <class T, int VE>
+__device__ __forceinline__ void sgd_store_vec(const SgdArgs<T>& a, uint32_t u, T* dst, uint32_t col,
+                                              const double (&acc)[VE], VecOf<T, VE> old) {
+  VecOf<T, VE> r;
+  if (a.seg_out) {
+#pragma unroll
+    for (int e = 0; e < VE; ++e) r.v[e] = static_cast<T>(acc[e]);
+    *reinterpret_cast<VecOf<T, VE>*>(dst + col) = r;
+    return;
+  }
+  bool bad = false;
+#pragma unroll
+  for (int e = 0; e < VE; ++e) {
+    r.v[e] = static_cast<T>(__dsub_rn(static_cast<double>(old.v[e]), __dmul_rn(a.lr, acc[e])));
+    bad |= !isfinite(static_cast<double>(r.v[e]));
+  }
+  *reinterpret_cast<VecOf<T, VE>*>(dst + col) = r;
+  if (a.rows_out)
+    *reinterpret_cast<VecOf<T, VE>*>(a.rows_out + static_cast<uint64_t>(u) * a.g.dim + col) = r;
+  if (bad) report(a.err, kErrNonFinite, a.rs.uniq_local[u] * static_cast<uint64_t>(a.g.p) + a.g.shard, 0);
+}
+
+// Thread per (item, VE-column vector): every thread runs its own short index
+// chain (item -> gradient rows) and moves one 16-byte vector per occurrence,
+// so the grid's loads are independent — the memory-level parallelism a
+// gather/scatter over Zipf rows needs. The 64 threads of one 1 KB row share
+// the item load through L1.
+//
+// k_sgd_single: one-occurrence rows, two items per thread in flight.
+template <class T, int VE>
+__global__ void __launch_bounds__(256) k_sgd_single(SgdArgs<T> a, uint32_t vpr_shift) {
   using V = VecOf<T, VE>;
-  constexpr int COLS = 32 * VE * NV;
-  const uint64_t nwork = *a.d_work_n;
-  const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
-  const uint64_t wid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const unsigned lane = threadIdx.x & 31u;
+  const uint64_t n = *a.d_single_n;
   const uint32_t dim = a.g.dim;
-  const uint32_t c0 = blockIdx.y * COLS;
-  for (uint64_t w = wid; w < nwork; w += warps) {
-    const uint2 item = a.work[w];
-    const uint32_t u = item.x;
-    const uint32_t s = a.rs.seg_start[u], e = a.rs.seg_start[u + 1];
-    const bool single = a.chunk == 0 || e - s <= a.chunk;
-    const uint32_t kb = single ? s : s + item.y * a.chunk;
-    const uint32_t ke = single ? e : min(e, kb + a.chunk);
-    {
-      double acc[NV][VE];
+  const uint32_t vpr = dim / VE;
+  const uint64_t total = n * vpr;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i0 < total; i0 += 2 * stride) {
+    uint64_t ix[2] = {i0, i0 + stride};
+    SgdItem it[2];
+    uint32_t col[2];
+    bool ok[2];
 #pragma unroll
-      for (int v = 0; v < NV; ++v)
+    for (int h = 0; h < 2; ++h) {
+      ok[h] = ix[h] < total;
+      const uint64_t w = vpr_shift != 0xffffffffu ? ix[h] >> vpr_shift : ix[h] / vpr;
+      col[h] = static_cast<uint32_t>(ix[h] - w * vpr) * VE;
+      if (ok[h]) it[h] = a.singles[w];
+    }
+    V g[2], old[2];
 #pragma unroll
-        for (int x = 0; x < VE; ++x) acc[v][x] = 0.0;
-      // lanes resolve up to 32 occurrences' gradient row addresses at once
-      // (perm -> source/rank -> row), then the warp walks them in order
-      for (uint32_t kb2 = kb; kb2 < ke; kb2 += 32) {
-        const uint32_t cnt = min(32u, ke - kb2);
-        const T* mine = lane < cnt ? a.gr.row(a.rs.perm[kb2 + lane]) : nullptr;
-        uint32_t q0 = 0;
-        for (; q0 + 4 <= cnt; q0 += 4) {
-          V g[4][NV];
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const T* row = reinterpret_cast<const T*>(
-                __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(mine), q0 + q));
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-              const uint32_t col = c0 + (v * 32 + lane) * VE;
-              if (col < dim) g[q][v] = *reinterpret_cast<const V*>(row + col);
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-#pragma unroll
-            for (int v = 0; v < NV; ++v)
-#pragma unroll
-              for (int x = 0; x < VE; ++x) acc[v][x] = __dadd_rn(acc[v][x], static_cast<double>(g[q][v].v[x]));
-        }
-        for (; q0 < cnt; ++q0) {
-          const T* row = reinterpret_cast<const T*>(
-              __shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(mine), q0));
-#pragma unroll
-          for (int v = 0; v < NV; ++v) {
-            const uint32_t col = c0 + (v * 32 + lane) * VE;
-            if (col < dim) {
-              const V g = *reinterpret_cast<const V*>(row + col);
-#pragma unroll
-              for (int x = 0; x < VE; ++x) acc[v][x] = __dadd_rn(acc[v][x], static_cast<double>(g.v[x]));
-            }
-          }
-        }
+    for (int h = 0; h < 2; ++h) {
+      ok[h] = ok[h] && it[h].dst != nullptr;
+      if (ok[h]) {
+        g[h] = *reinterpret_cast<const V*>(reinterpret_cast<const T*>(it[h].g0) + col[h]);
+        if (!a.seg_out) old[h] = *reinterpret_cast<const V*>(reinterpret_cast<const T*>(it[h].dst) + col[h]);
       }
+    }
 #pragma unroll
-      for (int v = 0; v < NV; ++v) {
-        const uint32_t col = c0 + (v * 32 + lane) * VE;
-        if (col >= dim) continue;
-        if (single) {
-          sgd_apply_vec<T, VE>(a, u, col, acc[v]);
-        } else {
-          double* p = a.partials + (static_cast<uint64_t>(a.part_base[u]) + item.y) * dim + col;
+    for (int h = 0; h < 2; ++h)
+      if (ok[h]) {
+        double acc[VE];
 #pragma unroll
-          for (int x = 0; x < VE; ++x) p[x] = acc[v][x];
-        }
+        for (int x = 0; x < VE; ++x) acc[x] = __dadd_rn(0.0, static_cast<double>(g[h].v[x]));
+        sgd_store_vec<T, VE>(a, it[h].u, reinterpret_cast<T*>(it[h].dst), col[h], acc, old[h]);
       }
+  }
+}
+
+// k_sgd_flat: rows of 2+ occurrences (or one chunk of a hot row), summed in
+// order in f64 with kFlatBatch loads in flight; multi-chunk rows leave
+// partials for k_sgd_combine.
+constexpr int kFlatBatch = 8;
+template <class T, int VE>
+__global__ void __launch_bounds__(256, 3) k_sgd_flat(SgdArgs<T> a, uint32_t vpr_shift) {
+  using V = VecOf<T, VE>;
+  const uint64_t nwork = *a.d_work_n;
+  const uint32_t dim = a.g.dim;
+  const uint32_t vpr = dim / VE;  // vectors per row
+  const uint64_t total = nwork * vpr;
+  for (uint64_t idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t w = vpr_shift != 0xffffffffu ? idx >> vpr_shift : idx / vpr;
+    const uint32_t col = static_cast<uint32_t>(idx - w * vpr) * VE;
+    const SgdItem item = a.work[w];
+    T* dst = reinterpret_cast<T*>(item.dst);
+    const bool single = (item.q & kSgdSingleChunk) != 0;
+    V old{};
+    if (single && dst && !a.seg_out) old = *reinterpret_cast<const V*>(dst + col);  // in flight with the gradients
+    double acc[VE];
+#pragma unroll
+    for (int x = 0; x < VE; ++x) acc[x] = 0.0;
+    // software pipeline: the next batch's gradient-row pointers load while
+    // this batch's gradient vectors are in flight
+    const T* gp[kFlatBatch];
+#pragma unroll
+    for (int t = 0; t < kFlatBatch; ++t)
+      gp[t] = item.kb + t < item.ke ? (t == 0 && item.g0 ? reinterpret_cast<const T*>(item.g0) : a.gptr[item.kb + t])
+                                    : nullptr;
+    for (uint32_t k0 = item.kb; k0 < item.ke; k0 += kFlatBatch) {
+      V g[kFlatBatch];
+#pragma unroll
+      for (int t = 0; t < kFlatBatch; ++t)
+        if (k0 + t < item.ke) g[t] = *reinterpret_cast<const V*>(gp[t] + col);
+      const uint32_t k1 = k0 + kFlatBatch;
+#pragma unroll
+      for (int t = 0; t < kFlatBatch; ++t) gp[t] = k1 + t < item.ke ? a.gptr[k1 + t] : nullptr;
+#pragma unroll
+      for (int t = 0; t < kFlatBatch; ++t)
+        if (k0 + t < item.ke) {
+#pragma unroll
+          for (int x = 0; x < VE; ++x) acc[x] = __dadd_rn(acc[x], static_cast<double>(g[t].v[x]));
+        }
+    }
+    if (single) {
+      if (dst) sgd_store_vec<T, VE>(a, item.u, dst, col, acc, old);
+    } else {
+      double* p = a.partials + (static_cast<uint64_t>(a.part_base[item.u]) + item.q) * dim + col;
+#pragma unroll
+      for (int x = 0; x < VE; ++x) p[x] = acc[x];
     }
   }
 }

@@ -7,25 +7,28 @@
 namespace fsx {
 
 struct SgdScratch {
-  DevBuf<uint2> work;
+  DevBuf<SgdItem> work, singles;
+  DevBuf<const void*> gptr;  // gradient row per sorted occurrence
   DevBuf<uint32_t> multi, part_base;
   DevBuf<double> partials;
-  DevBuf<uint64_t> d_tot;  // [0] work items, [1] multi rows, [2] partial slots
+  DevBuf<uint64_t> d_tot;  // [0] singles, [1] work items, [2] multi rows, [3] partial slots
   ScanScratch scan;
-  uint64_t cap_rows = 0, cap_work = 0;
+  uint64_t cap_rows = 0, cap_work = 0, cap_occ = 0;
   uint32_t dim = 0;
   void reserve(uint64_t rows, uint64_t occ, uint32_t d, uint32_t chunk) {
     const uint64_t w = rows + (chunk ? occ / chunk + 1 : 0);
-    if (rows > cap_rows || w > cap_work || d != dim) {
+    if (rows > cap_rows || w > cap_work || d != dim || occ > cap_occ) {
+      cap_occ = occ > cap_occ ? occ : cap_occ;
       cap_rows = rows > cap_rows ? rows : cap_rows;
       cap_work = w > cap_work ? w : cap_work;
       dim = d;
-      work.alloc(cap_work); multi.alloc(cap_rows); part_base.alloc(cap_rows);
+      work.alloc(cap_work); singles.alloc(cap_rows); multi.alloc(cap_rows); part_base.alloc(cap_rows);
+      gptr.alloc(occ > rows ? occ : rows);
       // a row with k > 1 chunks has > (k-1)*chunk occurrences: slots <= 2*occ/chunk
       partials.alloc(chunk ? (2 * occ / chunk + 1) * d : 1);
     }
     if (!d_tot.p) d_tot.alloc(4);
-    scan.ensure(rows, 3);
+    scan.ensure(rows, 4);
   }
 };
 
@@ -55,22 +58,32 @@ void sgd_update_rows(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_ca
                      T* rows_out, cudaStream_t stream, char* const* seg_out = nullptr) {
   if (rows_cap == 0) return;
   s.reserve(rows_cap, occ_cap, t.g.dim, chunk);
-  SgdPlanOp plan{rs, chunk, s.work.p, s.multi.p, s.part_base.p};
+  const T** gptr = reinterpret_cast<const T**>(s.gptr.p);
+  FSX_LAUNCH(ctx, k_grad_ptrs<T>, grid_for(ctx, occ_cap, 256, 8), 256, 0, stream, gr, rs.perm, rs.seg_start,
+             rs.d_u, gptr);
+  SgdPlanOp plan{rs, chunk, s.singles.p, s.work.p, s.multi.p, s.part_base.p, static_cast<char*>(t.values),
+                 t.row_bytes(), t.g.local_rows, seg_out, reinterpret_cast<const char* const*>(gptr)};
   run_scan(ctx, plan, rows_cap, rs.d_u, s.scan, s.d_tot.p, stream);
-  SgdArgs<T> a{static_cast<T*>(t.values), t.g, t.lr, rs, gr, chunk, s.work.p, s.d_tot.p,
-               s.multi.p, s.d_tot.p + 1, s.part_base.p, s.partials.p, rows_out, ctx->d_err, seg_out};
+  SgdArgs<T> a{static_cast<T*>(t.values), t.g, t.lr, rs, gr, chunk, s.singles.p, s.d_tot.p, s.work.p,
+               s.d_tot.p + 1, s.multi.p, s.d_tot.p + 2, s.part_base.p, s.partials.p, rows_out, ctx->d_err,
+               seg_out, gptr};
   const uint64_t work_cap = rows_cap + (chunk ? occ_cap / chunk + 1 : 0);
   const unsigned g2 = grid_for(ctx, rows_cap, 1, 8);
   const uint32_t rb = t.row_bytes();
   constexpr int VE16 = static_cast<int>(16 / sizeof(T));
   const int ve = rb % 16 == 0 ? VE16 : 1;
-  const unsigned cols = 32u * static_cast<unsigned>(ve);  // NV = 1: one vector per lane per block
-  const unsigned ycols = (t.g.dim + cols - 1) / cols;
-  dim3 g1(grid_for(ctx, work_cap, 4, 16 / (ycols < 4 ? ycols : 4)), ycols);
-  if (ve == VE16)
-    FSX_LAUNCH(ctx, (k_sgd_chunks<T, VE16, 1>), g1, 128, 0, stream, a);
-  else
-    FSX_LAUNCH(ctx, (k_sgd_chunks<T, 1, 1>), g1, 128, 0, stream, a);
+  // one thread per (work item, vector); the grid streams over all of them
+  const unsigned vpr = t.g.dim / static_cast<unsigned>(ve);
+  const uint32_t shift = (vpr & (vpr - 1)) == 0 ? static_cast<uint32_t>(__builtin_ctz(vpr)) : 0xffffffffu;
+  const unsigned g0 = grid_for(ctx, rows_cap * vpr / 2, 256, 8);
+  const unsigned g1 = grid_for(ctx, work_cap * vpr, 256, 16);
+  if (ve == VE16) {
+    FSX_LAUNCH(ctx, (k_sgd_single<T, VE16>), g0, 256, 0, stream, a, shift);
+    FSX_LAUNCH(ctx, (k_sgd_flat<T, VE16>), g1, 256, 0, stream, a, shift);
+  } else {
+    FSX_LAUNCH(ctx, (k_sgd_single<T, 1>), g0, 256, 0, stream, a, shift);
+    FSX_LAUNCH(ctx, (k_sgd_flat<T, 1>), g1, 256, 0, stream, a, shift);
+  }
   if (chunk) {
     if (t.g.dim % 2 == 0)
       FSX_LAUNCH(ctx, (k_sgd_combine<T, 2>), g2, 128, 0, stream, a);

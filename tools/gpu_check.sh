@@ -1,0 +1,12 @@
+# full GPU check: tests, smoke, N=1 bench, launch list
+set -x
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -5
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_n1.json 2> gpurun_out/bench_n1.err; echo rc=$?
+python -c "
+import json; d=json.loads(open('gpurun_out/bench_n1.json').read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'], d['e2e'], d['roofline'], d['phases_ms_per_step'], d['cpu_baseline'])"
+if [ "${PROFILE:-0}" = 1 ]; then
+CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --profile-phases 0"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu1.log 2>&1; echo ncu rc=$?
+fi
