@@ -534,8 +534,13 @@ def main():
         # reads send_pos/dst/slot/flag/rank + the grad row, writes it
         "split": occ * (2 * rb + 14),
         "serve": occ * (4 * rb + 16),
-        "update": occ * (rb + 13) + uq * 2 * rb,
+        # gradient rows in (+ perm / source / rank / pointer indices), each
+        # unique row read and written once
+        "update": occ * (rb + 24) + uq * 2 * rb,
     }
+    if world == 1:
+        # one rank: the whole update runs as the collision-lane update
+        algo["co_update"] = algo["update"]
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(peaks_path):
         peaks = json.load(open(peaks_path))
@@ -544,15 +549,18 @@ def main():
         peak, peak_src = PEAKS_FALLBACK["hbm_gbs"], "fallback"
     roof = None
     if phases:
-        cand = [(k, phases[k][0], phases[k][1]) for k in ("merge", "split", "serve", "update")
-                if k in phases and phases[k][1] > 0]
+        cand = [(k, phases[k][0], phases[k][1]) for k in algo if k in phases and phases[k][1] > 0]
         if cand:
             name, tot_ms, spans = max(cand, key=lambda x: x[1])
             per_launch_ms = tot_ms / spans
             per_launch_bytes = algo[name] / spans
             achieved = per_launch_bytes / (per_launch_ms * 1e-3) / 1e9
+            traffic = None
+            tpath = os.path.join(ROOT, "profiles", "traffic.json")
+            if os.path.exists(tpath):
+                traffic = json.load(open(tpath)).get(f"n{world}", {}).get(name)
             roof = {"bound": "hbm", "kernel": name, "achieved": round(achieved, 1), "peak": peak,
-                    "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                    "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                     "peak_source": peak_src, "launch_ms": round(per_launch_ms, 4),
                     "algorithmic_bytes_per_launch": int(per_launch_bytes)}
 

@@ -137,8 +137,9 @@ template <class Map>
 void launch_copy_rows(Ctx* ctx, const Map& map, uint64_t n_cap, const uint64_t* d_n,
                       uint32_t row_bytes, cudaStream_t s) {
   if (n_cap == 0) return;
+  const int vb = vec_bytes_for(row_bytes);
   const unsigned grid = grid_for(ctx, n_cap, 8 * 32, 4);
-  switch (vec_bytes_for(row_bytes)) {
+  switch (vb) {
     case 16: FSX_LAUNCH(ctx, (k_copy_rows<Map, 16>), grid, 256, 0, s, map, n_cap, d_n, row_bytes); break;
     case 8: FSX_LAUNCH(ctx, (k_copy_rows<Map, 8>), grid, 256, 0, s, map, n_cap, d_n, row_bytes); break;
     default: FSX_LAUNCH(ctx, (k_copy_rows<Map, 4>), grid, 256, 0, s, map, n_cap, d_n, row_bytes); break;

@@ -144,3 +144,41 @@ def test_cfg2_full_size(P, cuda):
     for row, c2 in zip(z["cost"], (0.0, 1e-6)):
         got = CostModel(50.0, 0.01, c2).compute_times([lens[r * 8192:(r + 1) * 8192] for r in range(8)])
         assert np.array_equal(got.view(np.uint64), row.view(np.uint64))
+
+
+@pytest.mark.parametrize("partition,iters", [("fbs", 3), ("vbs", 1)])
+def test_balancer_gpu_partition_gloo_world2(cuda, oracle, tmp_path, partition, iters):
+    """The three-stage balancer at world size 2 (gloo plumbing) with the GPU
+    FBS / VBS partition: every rank's balanced batch equals the plan the C
+    oracle computes from the gathered lengths, applied to the global batch."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    from balancer_cases import make_raw
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    world, out = 2, str(tmp_path / "bal")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(os.path.dirname(os.path.abspath(__file__)), "balancer_worker.py"),
+           out, partition, str(iters), "1"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    for i in range(iters):
+        raws = [make_raw(i, rr, world) for rr in range(world)]
+        lens = np.asarray([x.uih.size for rr in range(world) for x in raws[rr].samples], np.uint64)
+        origin = np.repeat(np.arange(world), 6).astype(np.int32)
+        local = np.tile(np.arange(6), world).astype(np.int32)
+        if partition == "fbs":
+            _, order = oracle.fbs(lens, origin, local, world)
+        else:
+            _, order, _ = oracle.vbs(lens, origin, local, world, 1.0)
+        glob = [x for rr in range(world) for x in raws[rr].samples]
+        for rank in range(world):
+            got = json.load(open(f"{out}.rank{rank}.json"))["taken"][i]
+            want = [glob[int(g)] for g in order[rank]]
+            assert [g[0] for g in got] == [w.uih.tolist() for w in want]
+            assert [g[2] for g in got] == [w.label for w in want]

@@ -8,5 +8,5 @@ python -c "
 import json; d=json.loads(open('gpurun_out/bench_n1.json').read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'], d['e2e'], d['roofline'], d['phases_ms_per_step'], d['cpu_baseline'])"
 if [ "${PROFILE:-0}" = 1 ]; then
 CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --profile-phases 0"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu1.log 2>&1; echo ncu rc=$?
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches.csv $CMD > gpurun_out/ncu1.log 2>&1; echo ncu rc=$?
 fi
