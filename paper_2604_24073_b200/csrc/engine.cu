@@ -1108,8 +1108,9 @@ struct Engine {
     } else if (p == 1) {
       // single rank: nothing to hide behind a transfer, so the whole update
       // (collision rows first in row order is immaterial: rows are disjoint)
-      // runs at once on the caller's stream, reading the gradients in place
-      exposed_wait(c, {ev_mask});
+      // runs at once on the caller's stream, reading the gradients in place.
+      // It needs neither the masks nor the split plan (only the statistics
+      // do, on H below), so it does not wait for the side lane.
       update(oc, CH_GRADS, 0, nullptr, 0, false, c, FSX_PHASE_CO_UPDATE, grads, rc.send_pos.p);
       ev_chain_start = record(c);
       has_pending = false;
@@ -1168,9 +1169,11 @@ struct Engine {
         rn.cor_par = send_eco(on, hi);
       }
       cur_co_ready = record(hi);
+      if (p == 1) wait(hi, ev_mask);  // split counts for the statistics
       stats_backward(i, have_grads, true, rc, oc, on, rn.cor_par, hi);
     } else {
       cur_co_ready = nullptr;
+      if (p == 1 && i > 0) wait(hi, ev_mask);
       stats_backward(i, have_grads, false, rc, oc, oc, -1, i == 0 ? c : hi);
     }
     ev_hchain = have_grads || has_next ? record(hi) : nullptr;
