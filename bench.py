@@ -399,8 +399,10 @@ def main():
         with Clocks(local) as clk:
             barrier()
             ev0.record(stream)
+            th0 = time.perf_counter()
             for i in range(W, W + K):
                 step(i)
+            host_enqueue_ms = (time.perf_counter() - th0) * 1e3
             ev1.record(stream)
             barrier()
         ms_dev = ev0.elapsed_time(ev1)
@@ -602,6 +604,9 @@ def main():
                     "h2d_bytes_per_step": int(np.mean([b.size for b in timed])) * 8,
                     "d2h_bytes_per_step": 32},
             "gpu_launches": int(launches),
+            # host time to issue the K timed steps (python + C ABI + launches);
+            # close to ms_per_step means the step is host-bound
+            "host_enqueue_ms_per_step": round(host_enqueue_ms / K, 4),
             "roofline": roof,
             "phases_ms_per_step": {k: round(v[0] / K, 4) for k, v in phases.items() if v[1]},
             "cpu_baseline": cpu,

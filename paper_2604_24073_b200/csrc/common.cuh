@@ -95,6 +95,12 @@ struct Ctx {
   DevErr* h_err = nullptr;   // pinned host mirror
   std::atomic<uint64_t> launches{0};
   int num_sms = 148;
+  // grid caps (CTAs per SM) of the row movers and update kernels. The
+  // compute-stream kernels must leave register room on every SM for the
+  // side lanes' latency-bound kernels (dedup / collision of the next
+  // iteration), or those wait for a whole merge / update to drain.
+  // Overridable for tuning: FSX_COPY_PER_SM, FSX_SINGLE_PER_SM, FSX_FLAT_PER_SM.
+  unsigned copy_per_sm = 4, single_per_sm = 8, flat_per_sm = 16;
 
   void check_error(cudaStream_t s);  // D2H the word, sync `s`, throw if set
 };

@@ -115,6 +115,52 @@ __global__ void k_count_flags(const uint8_t* f, const uint64_t* d_n, unsigned lo
   if ((threadIdx.x & 31u) == 0 && c) atomicAdd(out, c);
 }
 
+// One rank: the owner partition of route_to_shard_major (embedding.cpp:194-212)
+// is the identity — every id goes to self in its original order. One pass
+// writes the IDS message, send_pos = j, send_dst = 0 and the counts
+// (tot[0] = n, send_off = {0, n}).
+__global__ void k_route_self(const uint64_t* __restrict__ ids, uint64_t n, uint64_t total_rows, Slots send,
+                             uint32_t* __restrict__ send_pos, uint8_t* __restrict__ send_dst,
+                             uint64_t* tot, DevErr* err) {
+  const uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i0 == 0) {
+    tot[0] = n;
+    tot[16] = 0;
+    tot[17] = n;
+    reinterpret_cast<uint64_t*>(send.p[0])[0] = n;
+    reinterpret_cast<uint64_t*>(send.p[0])[1] = 0;
+  }
+  uint64_t* msg = reinterpret_cast<uint64_t*>(send.p[0] + kHdr);
+  for (uint64_t i = i0; i < n; i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t id = ids[i];
+    if (id >= total_rows) report(err, kErrRowRange, id, total_rows);
+    msg[i] = id;
+    send_pos[i] = static_cast<uint32_t>(i);
+    send_dst[i] = 0;
+  }
+}
+
+// One rank: the split / occurrence-rank totals the statistics read
+// (k_blocking_bytes), without the per-occurrence plans nothing consumes —
+// [0] exclusive, [1] collision occurrences, for requester and owner alike.
+__global__ void k_co_occ_count(const uint32_t* __restrict__ inverse, const uint8_t* __restrict__ co,
+                               const uint64_t* d_n, unsigned long long* split_tot, unsigned long long* occ_tot) {
+  const uint64_t n = *d_n;
+  unsigned long long c = 0, e = 0;
+  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < n;
+       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    if (co && co[inverse[j]]) ++c; else ++e;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+    e += __shfl_xor_sync(0xffffffffu, e, o);
+  }
+  if ((threadIdx.x & 31u) == 0) {
+    if (e) { atomicAdd(split_tot, e); atomicAdd(occ_tot, e); }
+    if (c) { atomicAdd(split_tot + 1, c); atomicAdd(occ_tot + 1, c); }
+  }
+}
+
 // IterationStats.blocking_bytes (embedding.cpp:498-593) in the reference's
 // accounting (8-byte values): collision grads sent + received, E_co
 // messages sent + received.
@@ -177,6 +223,8 @@ struct OwnBatch {  // owner view: occurrences received for this shard
   DevBuf<uint32_t> partner;  // collision row -> its row in the next owner batch
   SortedIds srt;
   ScanScratch scan;
+  SgdScratch plan;               // one rank: the update's work lists, built on L
+  cudaEvent_t ev_plan = nullptr; // ahead of the backward that applies them
   std::vector<uint64_t> h_recv, h_pack, h_mask;
   bool has_co = false;
   uint64_t m_cap = 0;
@@ -602,6 +650,11 @@ struct Engine {
     const int par = next_par(CH_IDS);
     Slots send = send_slots(CH_IDS, par);
     FSX_CUDA(cudaMemsetAsync(r.tot.p, 0, 48 * 8, s));
+    if (p == 1) {
+      FSX_LAUNCH(ctx, k_route_self, grid_for(ctx, n ? n : 1, 256, 8), 256, 0, s, r.ids.p, n, t->g.total_rows, send,
+                 r.send_pos.p, r.send_dst.p, r.tot.p, ctx->d_err);
+      return par;
+    }
     if (p <= 8) {
       RouteOp<8> op{r.ids.p, t->g.total_rows, p, r.tot.p, send, r.send_pos.p, r.send_dst.p, cap, ctx->d_err};
       run_scan(ctx, op, n, nullptr, r.scan, r.tot.p, s);
@@ -655,6 +708,31 @@ struct Engine {
       GradRows<double> gr{recv_slot(ch, par, 0) + kHdr, ch_slot[ch], o.occ_src.p,
                           by_rank ? o.occ_rank.p : o.occ_idx.p, rb, sb, self_pos, sb ? me : -1};
       sgd_update_rows<double>(ctx, *t, rs, m, m, gr, cfg.reduce_chunk, sgd_for(s), nullptr, s);
+    }
+  }
+  // one rank: the whole update of an owner batch reads the caller's gradient
+  // array in occurrence order (row j of the array is occurrence j), so its
+  // work lists depend on the batch's row segments alone and are built on L a
+  // whole iteration early; the backward only runs the update kernels.
+  bool self_plan() const { return p == 1 && !presum(); }
+  void plan_self(OwnBatch& o, cudaStream_t s) {
+    RowSegments rs{o.srt.uniq.p, o.srt.seg_start.p, o.srt.perm, o.srt.d_u(), nullptr, 0};
+    if (t->dtype == FSX_F32)
+      sgd_plan<float>(ctx, *t, rs, o.m_cap, o.m_cap, nullptr, cfg.reduce_chunk, o.plan, s);
+    else
+      sgd_plan<double>(ctx, *t, rs, o.m_cap, o.m_cap, nullptr, cfg.reduce_chunk, o.plan, s);
+    o.ev_plan = record(s);
+  }
+  void apply_self(OwnBatch& o, const void* grads, cudaStream_t c) {
+    exposed_wait(c, {o.ev_plan});
+    Span sp(this, FSX_PHASE_CO_UPDATE, c);
+    RowSegments rs{o.srt.uniq.p, o.srt.seg_start.p, o.srt.perm, o.srt.d_u(), nullptr, 0};
+    if (t->dtype == FSX_F32) {
+      GradRows<float> gr{static_cast<const char*>(grads), 0, nullptr, nullptr, rb};
+      sgd_apply<float>(ctx, *t, rs, o.m_cap, o.m_cap, gr, cfg.reduce_chunk, o.plan, nullptr, c);
+    } else {
+      GradRows<double> gr{static_cast<const char*>(grads), 0, nullptr, nullptr, rb};
+      sgd_apply<double>(ctx, *t, rs, o.m_cap, o.m_cap, gr, cfg.reduce_chunk, o.plan, nullptr, c);
     }
   }
   SgdScratch sgd[3];  // one per lane that updates: ux, hi, compute
@@ -779,6 +857,17 @@ struct Engine {
   // (embedding.cpp:392-408, 524-536)
   void masks_and_split(OwnBatch& oc, ReqBatch& rc, bool with_co, cudaStream_t s) {
     Span sp(this, FSX_PHASE_MASKS, s);
+    if (p == 1 && !presum()) {
+      // one rank: the update needs no masks or split plan (it runs whole on
+      // the caller's stream); only the statistics need the totals
+      FSX_CUDA(cudaMemsetAsync(rc.split_tot.p, 0, 32 * 8, s));
+      FSX_CUDA(cudaMemsetAsync(oc.occ_tot(), 0, 32 * 8, s));
+      FSX_LAUNCH(ctx, k_co_occ_count, grid_for(ctx, oc.m_cap, 256, 4), 256, 0, s, oc.srt.inverse.p,
+                 with_co ? oc.co.p : nullptr, oc.srt.d_n(), reinterpret_cast<unsigned long long*>(rc.split_tot.p),
+                 reinterpret_cast<unsigned long long*>(oc.occ_tot()));
+      rc.has_flags = false;
+      return;
+    }
     if (with_co && presum()) {
       // GRP messages: each source's collision occurrences grouped by row
       const int par = next_par(CH_GRP);
@@ -1036,6 +1125,7 @@ struct Engine {
         receive(on, par, lo);
         rn.cor_par = -1;
         collide_and_prefetch(oc2, on, rn, lo);
+        if (self_plan()) plan_self(on, lo);
         ev_next_ready = record(lo);
         rn_ex_ready = ev_next_ready;
         if (!bootstrap) masks_and_split(oc2, rc2, true, lo);
@@ -1111,7 +1201,10 @@ struct Engine {
       // runs at once on the caller's stream, reading the gradients in place.
       // It needs neither the masks nor the split plan (only the statistics
       // do, on H below), so it does not wait for the side lane.
-      update(oc, CH_GRADS, 0, nullptr, 0, false, c, FSX_PHASE_CO_UPDATE, grads, rc.send_pos.p);
+      if (self_plan())
+        apply_self(oc, grads, c);
+      else
+        update(oc, CH_GRADS, 0, nullptr, 0, false, c, FSX_PHASE_CO_UPDATE, grads, rc.send_pos.p);
       ev_chain_start = record(c);
       has_pending = false;
       have_grads = true;
@@ -1335,6 +1428,8 @@ int fsx_engine_create(fsx_ctx* ctx, fsx_table* table, const fsx_engine_config* c
     e->ow[k].scan.ensure(m, 16);
   }
   for (auto& s : e->sgd) s.reserve(m, m, table->g.dim, cfg->reduce_chunk);
+  if (prio && e->self_plan())
+    for (int k = 0; k < 3; ++k) e->ow[k].plan.reserve(m, m, table->g.dim, cfg->reduce_chunk);
   e->stats_reserve(4 * Engine::kStatsChunk);
   FSX_CUDA(cudaDeviceSynchronize());
   *out = e.release();

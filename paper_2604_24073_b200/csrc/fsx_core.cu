@@ -1,6 +1,7 @@
 // libfsx core: context, error mapping, primitives (K1-K5, K8, K11) and the
 // table object behind the C ABI in include/fsx.h.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -149,6 +150,13 @@ int fsx_ctx_create(int device, int rank, int world, fsx_ctx** out) {
   c->rank = rank;
   c->world = world;
   FSX_CUDA(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+  auto env_u = [](const char* k, unsigned d) {
+    const char* v = std::getenv(k);
+    return v && std::atoi(v) > 0 ? static_cast<unsigned>(std::atoi(v)) : d;
+  };
+  c->copy_per_sm = env_u("FSX_COPY_PER_SM", c->copy_per_sm);
+  c->single_per_sm = env_u("FSX_SINGLE_PER_SM", c->single_per_sm);
+  c->flat_per_sm = env_u("FSX_FLAT_PER_SM", c->flat_per_sm);
   FSX_CUDA(cudaMalloc(&c->d_err, sizeof(DevErr)));
   FSX_CUDA(cudaMemset(c->d_err, 0, sizeof(DevErr)));
   FSX_CUDA(cudaMallocHost(&c->h_err, sizeof(DevErr)));

@@ -138,7 +138,7 @@ void launch_copy_rows(Ctx* ctx, const Map& map, uint64_t n_cap, const uint64_t* 
                       uint32_t row_bytes, cudaStream_t s) {
   if (n_cap == 0) return;
   const int vb = vec_bytes_for(row_bytes);
-  const unsigned grid = grid_for(ctx, n_cap, 8 * 32, 4);
+  const unsigned grid = grid_for(ctx, n_cap, 8 * 32, ctx->copy_per_sm);
   switch (vb) {
     case 16: FSX_LAUNCH(ctx, (k_copy_rows<Map, 16>), grid, 256, 0, s, map, n_cap, d_n, row_bytes); break;
     case 8: FSX_LAUNCH(ctx, (k_copy_rows<Map, 8>), grid, 256, 0, s, map, n_cap, d_n, row_bytes); break;
@@ -328,7 +328,9 @@ struct SgdPlanOp {
   uint32_t row_bytes;
   uint64_t local_rows;
   char* const* seg_out; // nullable: reduce-only destinations
-  const char* const* gptr;  // gradient row per sorted occurrence
+  const char* const* gptr;  // nullable: gradient row per sorted occurrence
+                            // (nullptr: items carry no gradient pointer; the
+                            // update kernels resolve rows from perm)
   __device__ uint32_t len(uint64_t u) const { return rs.seg_start[u + 1] - rs.seg_start[u]; }
   __device__ bool selected(uint64_t u) const { return !rs.select || rs.select[u] == rs.want; }
   // c0: singles, c1: work items, c2: multi-chunk rows, c3: partial slots
@@ -356,11 +358,11 @@ struct SgdPlanOp {
       }
     }
     if (c[0]) {
-      singles[ex[0]] = SgdItem{static_cast<uint32_t>(u), kSgdSingleChunk, s, e, dst, gptr[s]};
+      singles[ex[0]] = SgdItem{static_cast<uint32_t>(u), kSgdSingleChunk, s, e, dst, gptr ? gptr[s] : nullptr};
       return;
     }
     if (c[1] == 1) {
-      work[ex[1]] = SgdItem{static_cast<uint32_t>(u), kSgdSingleChunk, s, e, dst, gptr[s]};
+      work[ex[1]] = SgdItem{static_cast<uint32_t>(u), kSgdSingleChunk, s, e, dst, gptr ? gptr[s] : nullptr};
     } else {
       // chunks of a hot row: plain stores (no dependent loads in this loop)
       for (uint32_t q = 0; q < c[1]; ++q) {
@@ -407,7 +409,11 @@ struct SgdArgs {
   DevErr* err;
   char* const* seg_out;       // nullable: reduce-only mode — segment u's sum is
                               // written (as T) to seg_out[u] instead of updating
-  const T* const* gptr;       // gradient row per sorted occurrence (k_grad_ptrs)
+  const T* const* gptr;       // nullable: gradient row per sorted occurrence
+                              // (k_grad_ptrs); nullptr: gr.row(perm[k])
+  __device__ __forceinline__ const T* grad(uint32_t k) const {
+    return gptr ? gptr[k] : gr.row(rs.perm[k]);
+  }
 };
 
 // vector of VE elements of T moved as one 4/8/16-byte access
@@ -500,7 +506,8 @@ __global__ void __launch_bounds__(256) k_sgd_single(SgdArgs<T> a, uint32_t vpr_s
     for (int h = 0; h < 2; ++h) {
       ok[h] = ok[h] && it[h].dst != nullptr;
       if (ok[h]) {
-        g[h] = *reinterpret_cast<const V*>(reinterpret_cast<const T*>(it[h].g0) + col[h]);
+        const T* g0 = it[h].g0 ? reinterpret_cast<const T*>(it[h].g0) : a.grad(it[h].kb);
+        g[h] = *reinterpret_cast<const V*>(g0 + col[h]);
         if (!a.seg_out) old[h] = *reinterpret_cast<const V*>(reinterpret_cast<const T*>(it[h].dst) + col[h]);
       }
     }
@@ -543,7 +550,7 @@ __global__ void __launch_bounds__(256, 3) k_sgd_flat(SgdArgs<T> a, uint32_t vpr_
     const T* gp[kFlatBatch];
 #pragma unroll
     for (int t = 0; t < kFlatBatch; ++t)
-      gp[t] = item.kb + t < item.ke ? (t == 0 && item.g0 ? reinterpret_cast<const T*>(item.g0) : a.gptr[item.kb + t])
+      gp[t] = item.kb + t < item.ke ? (t == 0 && item.g0 ? reinterpret_cast<const T*>(item.g0) : a.grad(item.kb + t))
                                     : nullptr;
     for (uint32_t k0 = item.kb; k0 < item.ke; k0 += kFlatBatch) {
       V g[kFlatBatch];
@@ -552,7 +559,7 @@ __global__ void __launch_bounds__(256, 3) k_sgd_flat(SgdArgs<T> a, uint32_t vpr_
         if (k0 + t < item.ke) g[t] = *reinterpret_cast<const V*>(gp[t] + col);
       const uint32_t k1 = k0 + kFlatBatch;
 #pragma unroll
-      for (int t = 0; t < kFlatBatch; ++t) gp[t] = k1 + t < item.ke ? a.gptr[k1 + t] : nullptr;
+      for (int t = 0; t < kFlatBatch; ++t) gp[t] = k1 + t < item.ke ? a.grad(k1 + t) : nullptr;
 #pragma unroll
       for (int t = 0; t < kFlatBatch; ++t)
         if (k0 + t < item.ke) {

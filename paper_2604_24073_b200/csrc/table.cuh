@@ -14,6 +14,7 @@ struct SgdScratch {
   DevBuf<uint64_t> d_tot;  // [0] singles, [1] work items, [2] multi rows, [3] partial slots
   ScanScratch scan;
   uint64_t cap_rows = 0, cap_work = 0, cap_occ = 0;
+  bool resolved = false;  // the last plan stored gradient-row pointers
   uint32_t dim = 0;
   void reserve(uint64_t rows, uint64_t occ, uint32_t d, uint32_t chunk) {
     const uint64_t w = rows + (chunk ? occ / chunk + 1 : 0);
@@ -49,21 +50,40 @@ struct Table {
 };
 
 // Segmented deterministic SGD over the rows of `rs` (selected rows only),
-// gradients from `gr`. Issues plan scan + chunk kernel + combine kernel.
+// gradients from `gr`, in two halves:
+//  sgd_plan  — the work lists (plan scan). With resolve_grads the gradient row
+//              of every occurrence is resolved first (k_grad_ptrs) and stored
+//              in the items; without it the plan depends on the row segments
+//              alone, so it can be built ahead of time (before the gradients
+//              exist) and the update kernels resolve gr.row(perm[k]) — for a
+//              plain [M x dim] gradient array that is one multiply-add.
+//  sgd_apply — the chunk kernels + combine over a plan.
 // seg_out != nullptr: reduce only — each segment's gradient sum (same
 // chunked association) goes to seg_out[u]; the table is not touched.
 template <class T>
-void sgd_update_rows(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_cap,
-                     uint64_t occ_cap, const GradRows<T>& gr, uint32_t chunk, SgdScratch& s,
-                     T* rows_out, cudaStream_t stream, char* const* seg_out = nullptr) {
+void sgd_plan(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_cap, uint64_t occ_cap,
+              const GradRows<T>* resolve_grads, uint32_t chunk, SgdScratch& s, cudaStream_t stream,
+              char* const* seg_out = nullptr) {
   if (rows_cap == 0) return;
   s.reserve(rows_cap, occ_cap, t.g.dim, chunk);
-  const T** gptr = reinterpret_cast<const T**>(s.gptr.p);
-  FSX_LAUNCH(ctx, k_grad_ptrs<T>, grid_for(ctx, occ_cap, 256, 8), 256, 0, stream, gr, rs.perm, rs.seg_start,
-             rs.d_u, gptr);
+  const T** gptr = nullptr;
+  if (resolve_grads) {
+    gptr = reinterpret_cast<const T**>(s.gptr.p);
+    FSX_LAUNCH(ctx, k_grad_ptrs<T>, grid_for(ctx, occ_cap, 256, 8), 256, 0, stream, *resolve_grads, rs.perm,
+               rs.seg_start, rs.d_u, gptr);
+  }
+  s.resolved = gptr != nullptr;
   SgdPlanOp plan{rs, chunk, s.singles.p, s.work.p, s.multi.p, s.part_base.p, static_cast<char*>(t.values),
                  t.row_bytes(), t.g.local_rows, seg_out, reinterpret_cast<const char* const*>(gptr)};
   run_scan(ctx, plan, rows_cap, rs.d_u, s.scan, s.d_tot.p, stream);
+}
+
+template <class T>
+void sgd_apply(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_cap, uint64_t occ_cap,
+               const GradRows<T>& gr, uint32_t chunk, SgdScratch& s, T* rows_out, cudaStream_t stream,
+               char* const* seg_out = nullptr) {
+  if (rows_cap == 0) return;
+  const T** gptr = s.resolved ? reinterpret_cast<const T**>(s.gptr.p) : nullptr;
   SgdArgs<T> a{static_cast<T*>(t.values), t.g, t.lr, rs, gr, chunk, s.singles.p, s.d_tot.p, s.work.p,
                s.d_tot.p + 1, s.multi.p, s.d_tot.p + 2, s.part_base.p, s.partials.p, rows_out, ctx->d_err,
                seg_out, gptr};
@@ -75,8 +95,8 @@ void sgd_update_rows(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_ca
   // one thread per (work item, vector); the grid streams over all of them
   const unsigned vpr = t.g.dim / static_cast<unsigned>(ve);
   const uint32_t shift = (vpr & (vpr - 1)) == 0 ? static_cast<uint32_t>(__builtin_ctz(vpr)) : 0xffffffffu;
-  const unsigned g0 = grid_for(ctx, rows_cap * vpr / 2, 256, 8);
-  const unsigned g1 = grid_for(ctx, work_cap * vpr, 256, 16);
+  const unsigned g0 = grid_for(ctx, rows_cap * vpr / 2, 256, ctx->single_per_sm);
+  const unsigned g1 = grid_for(ctx, work_cap * vpr, 256, ctx->flat_per_sm);
   if (ve == VE16) {
     FSX_LAUNCH(ctx, (k_sgd_single<T, VE16>), g0, 256, 0, stream, a, shift);
     FSX_LAUNCH(ctx, (k_sgd_flat<T, VE16>), g1, 256, 0, stream, a, shift);
@@ -90,6 +110,14 @@ void sgd_update_rows(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_ca
     else
       FSX_LAUNCH(ctx, (k_sgd_combine<T, 1>), g2, 128, 0, stream, a);
   }
+}
+
+template <class T>
+void sgd_update_rows(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_cap,
+                     uint64_t occ_cap, const GradRows<T>& gr, uint32_t chunk, SgdScratch& s,
+                     T* rows_out, cudaStream_t stream, char* const* seg_out = nullptr) {
+  sgd_plan<T>(ctx, t, rs, rows_cap, occ_cap, &gr, chunk, s, stream, seg_out);
+  sgd_apply<T>(ctx, t, rs, rows_cap, occ_cap, gr, chunk, s, rows_out, stream, seg_out);
 }
 
 }  // namespace fsx
