@@ -329,17 +329,21 @@ struct SideLane {
       }
     });
   }
-  void post(std::function<void()> f) {
+  // returns a ticket: wait_for(ticket) returns once this job has run
+  uint64_t post(std::function<void()> f) {
+    uint64_t t;
     {
       std::lock_guard<std::mutex> lk(mu);
       q.push_back(std::move(f));
-      ++posted;
+      t = ++posted;
     }
     cv.notify_all();
+    return t;
   }
-  void drain() {
+  void drain() { wait_for(~uint64_t{0}); }
+  void wait_for(uint64_t ticket) {
     std::unique_lock<std::mutex> lk(mu);
-    cv.wait(lk, [&] { return done == posted; });
+    cv.wait(lk, [&] { return done >= (ticket < posted ? ticket : posted); });
     if (err) {
       auto e = err;
       err = nullptr;
@@ -639,7 +643,12 @@ struct Engine {
   int nc2() const { return p <= 4 ? 8 : 16; }  // counters for 2p classes
 
   // ---- requester: route a batch (embedding.cpp:185-212) ----------------------
-  int route(ReqBatch& r, const uint64_t* d_ids, uint64_t n, cudaStream_t s) {
+  // exact: fetch the per-owner counts (the blocking paths size their row
+  // messages by them). Otherwise the IDS copies are bounded by n — every
+  // owner's message has at most n ids — and no host round trip is taken,
+  // unless that bound is large (then the exact sizes are cheaper).
+  static constexpr uint64_t kBoundedCopyMax = 2ull << 20;
+  int route(ReqBatch& r, const uint64_t* d_ids, uint64_t n, cudaStream_t s, bool exact = true) {
     Span sp(this, FSX_PHASE_ROUTE, s);
     if (n > cap) raise(FSX_ERR_INVALID_ARGUMENT, "embedding: batch of " + std::to_string(n) +
                                                     " ids exceeds engine capacity " + std::to_string(cap));
@@ -665,16 +674,23 @@ struct Engine {
     FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, r.tot.p, 1, cap, ctx->d_err);
     FSX_LAUNCH(ctx, k_prefix, 1, 32, 0, s, r.tot.p, p, 1, r.tot.p + 16);
     if (p > 1) {
-      r.h_send = fetch(r.tot.p, p, s);
       std::vector<uint64_t> bytes(p);
-      for (int d = 0; d < p; ++d) bytes[d] = kHdr + 8 * r.h_send[d];
+      if (exact || 8 * n > kBoundedCopyMax) {
+        r.h_send = fetch(r.tot.p, p, s);
+        for (int d = 0; d < p; ++d) bytes[d] = kHdr + 8 * r.h_send[d];
+      } else {
+        r.h_send.clear();
+        for (int d = 0; d < p; ++d) bytes[d] = kHdr + 8 * n;
+      }
       a2a(CH_IDS, par, bytes, s);
     }
     return par;
   }
 
   // ---- owner: receive + dedup (embedding.cpp:214-229) -------------------------
-  void receive(OwnBatch& o, int ids_par, cudaStream_t s) {
+  // exact: fetch the per-source counts (blocking paths); the prioritized
+  // IDX / MASK messages are bounded by the capacity instead
+  void receive(OwnBatch& o, int ids_par, cudaStream_t s, bool exact = true) {
     Span sp(this, FSX_PHASE_DEDUP, s);
     o.reserve(static_cast<uint64_t>(p) * cap);
     o.has_co = false;
@@ -687,7 +703,14 @@ struct Engine {
     FSX_CUDA(cudaMemsetAsync(o.bits.p, 0, o.m_cap * 4, s));
     FSX_LAUNCH(ctx, k_src_bits, grid_for(ctx, o.m_cap, 256, 8), 256, 0, s, o.srt.inverse.p,
                o.occ_src.p, o.srt.d_n(), o.bits.p);
-    if (p > 1) o.h_recv = fetch(o.cnt.p + 2, p, s);
+    if (p > 1 && exact) o.h_recv = fetch(o.cnt.p + 2, p, s);
+    else o.h_recv.clear();
+  }
+  // bytes of a per-occurrence message of `elem` bytes to every source
+  std::vector<uint64_t> occ_msg_bytes(const OwnBatch& o, uint64_t elem) const {
+    std::vector<uint64_t> bytes(p);
+    for (int d = 0; d < p; ++d) bytes[d] = kHdr + elem * (o.h_recv.empty() ? cap : o.h_recv[d]);
+    return bytes;
   }
 
   // full-row deterministic update of an owner batch from a grads channel
@@ -789,7 +812,7 @@ struct Engine {
   // ---- prioritized building blocks ----------------------------------------------------
   // collision of (cur, next) owner batches + pack lists + EX prefetch of next
   // (embedding.cpp:360-390)
-  void collide_and_prefetch(OwnBatch& oc, OwnBatch& on, ReqBatch& rn, cudaStream_t s) {
+  void collide(OwnBatch& oc, OwnBatch& on, cudaStream_t s) {
     Span sp(this, FSX_PHASE_COLLIDE, s);
     FSX_CUDA(cudaMemsetAsync(on.co.p, 0, on.m_cap, s));
     FSX_CUDA(cudaMemsetAsync(oc.misc.p, 0, 8, s));
@@ -799,6 +822,11 @@ struct Engine {
                reinterpret_cast<unsigned long long*>(oc.misc.p));
     oc.has_co = true;
     on.has_co = false;
+  }
+  // pack lists + E_ex prefetch + IDX of the next batch (its collision flags
+  // come from collide)
+  void prefetch(OwnBatch& on, ReqBatch& rn, cudaStream_t s) {
+    Span sp(this, FSX_PHASE_COLLIDE, s);
     if (p == 1) {
       // single rank: every message would go to self, and self rows are
       // merged straight from the table — no pack lists, no copies. IDX still
@@ -845,11 +873,7 @@ struct Engine {
     FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, isend, p, on.cnt.p + 2, 1, cap, ctx->d_err);
     FSX_LAUNCH(ctx, k_idx_pack, grid_for(ctx, on.m_cap, 256, 8), 256, 0, s, on.srt.inverse.p, on.occ_src.p,
                on.occ_idx.p, on.srt.d_n(), on.rank_us.p, on.co.p, isend, me);
-    {
-      std::vector<uint64_t> bytes(p);
-      for (int d = 0; d < p; ++d) bytes[d] = kHdr + 4 * on.h_recv[d];
-      a2a(CH_IDX, ipar, bytes, s);
-    }
+    a2a(CH_IDX, ipar, occ_msg_bytes(on, 4), s);
     rn.idx_par = ipar;
   }
 
@@ -901,11 +925,7 @@ struct Engine {
       FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, oc.cnt.p + 2, 1, cap, ctx->d_err);
       FSX_LAUNCH(ctx, k_mask_pack, grid_for(ctx, oc.m_cap, 256, 8), 256, 0, s, oc.srt.inverse.p,
                  oc.occ_src.p, oc.occ_idx.p, oc.srt.d_n(), oc.co.p, send);
-      if (p > 1) {
-        std::vector<uint64_t> bytes(p);
-        for (int d = 0; d < p; ++d) bytes[d] = kHdr + oc.h_recv[d];
-        a2a(CH_MASK, par, bytes, s);
-      }
+      if (p > 1) a2a(CH_MASK, par, occ_msg_bytes(oc, 1), s);
       if (rc.n)
         FSX_LAUNCH(ctx, k_req_flags, grid_for(ctx, rc.n, 256, 8), 256, 0, s, recv_slots(CH_MASK, par),
                    rc.send_dst.p, rc.send_off(), rc.n, rc.flag.p, ctx->d_err);
@@ -1114,31 +1134,49 @@ struct Engine {
     }
     stats_reserve(i + 1);
     const bool with_next = ids_next != nullptr;
-    auto prep = [this, i, bootstrap, with_next, n_next]() {
+    // part 1 (what the backward of i waits for): route + dedup of i+1, the
+    // collision of (i, i+1), masks + split plan of i. Part 2 (needed only by
+    // the merge of i+1 and the E_co pack): pack lists, E_ex prefetch, IDX.
+    auto prep1 = [this, i, bootstrap, with_next, n_next]() {
       ReqBatch& rc2 = R(i);
       OwnBatch& oc2 = O(i);
       if (!bootstrap) apply_deferred();
       if (with_next) {
         ReqBatch& rn = R(i + 1);
         OwnBatch& on = O(i + 1);
-        const int par = route(rn, rn.ids.p, n_next, lo);
-        receive(on, par, lo);
+        const int par = route(rn, rn.ids.p, n_next, lo, false);
+        receive(on, par, lo, false);
         rn.cor_par = -1;
-        collide_and_prefetch(oc2, on, rn, lo);
-        if (self_plan()) plan_self(on, lo);
-        ev_next_ready = record(lo);
-        rn_ex_ready = ev_next_ready;
+        collide(oc2, on, lo);
         if (!bootstrap) masks_and_split(oc2, rc2, true, lo);
       } else {
         oc2.has_co = false;
-        ev_next_ready = nullptr;
         if (!bootstrap) masks_and_split(oc2, rc2, false, lo);
       }
       ev_mask = bootstrap ? nullptr : record(lo);
+    };
+    auto prep2 = [this, i, with_next]() {
+      if (with_next) {
+        ReqBatch& rn = R(i + 1);
+        OwnBatch& on = O(i + 1);
+        prefetch(on, rn, lo);
+        if (self_plan()) plan_self(on, lo);
+        ev_next_ready = record(lo);
+        rn_ex_ready = ev_next_ready;
+      } else {
+        ev_next_ready = nullptr;
+        rn_ex_ready = nullptr;
+      }
       stats_forward(i, with_next);
     };
     cudaEvent_t ex_ready_cur = cur_ex_ready;  // E_ex(i), recorded by the previous prep
-    if (side) side->post(prep); else prep();
+    if (side) {
+      ticket_mask = side->post(prep1);
+      ticket_next = side->post(prep2);
+    } else {
+      prep1();
+      prep2();
+    }
     // ---- compute stream C: serve iteration i ----
     if (bootstrap) {
       serve_blocking(rc, oc, out, c);
@@ -1155,6 +1193,10 @@ struct Engine {
     has_next = ids_next != nullptr;
   }
   cudaEvent_t cur_ex_ready = nullptr, cur_co_ready = nullptr, rn_ex_ready = nullptr;
+  uint64_t ticket_mask = 0, ticket_next = 0;  // side-lane jobs of the last forward
+  void wait_next_ready() {
+    if (side) side->wait_for(ticket_next);
+  }
   bool has_next = false;
 
   // deferred exclusive gradients of the previous iteration (embedding.cpp:314-339),
@@ -1183,8 +1225,7 @@ struct Engine {
 
   void prio_backward(const void* grads, cudaStream_t c) {
     if (!forward_done) raise(FSX_ERR_PROTOCOL, "embedding: backward before forward");
-    if (side) side->drain();  // masks + split counts of this iteration are issued
-    cur_ex_ready = rn_ex_ready;
+    if (side) side->wait_for(ticket_mask);  // masks + split counts of this iteration are issued
     const int i = iter;
     ReqBatch& rc = R(i);
     OwnBatch& oc = O(i);
@@ -1229,6 +1270,7 @@ struct Engine {
           }
           Span sp(this, FSX_PHASE_CO_UPDATE, hi);
           if (has_next && p > 1) {
+            wait_next_ready();
             wait(hi, ev_next_ready);
             fused_cor = next_par(CH_COR);
             co_apply(oc, cog, hi, &O(i + 1), fused_cor);
@@ -1246,6 +1288,8 @@ struct Engine {
         have_grads = true;
       }
     }
+    wait_next_ready();
+    cur_ex_ready = rn_ex_ready;
     if (has_next) {
       // E_co^{i+1}: fresh collision rows to the next iteration's requesters
       OwnBatch& on = O(i + 1);

@@ -157,6 +157,8 @@ int fsx_ctx_create(int device, int rank, int world, fsx_ctx** out) {
   c->copy_per_sm = env_u("FSX_COPY_PER_SM", c->copy_per_sm);
   c->single_per_sm = env_u("FSX_SINGLE_PER_SM", c->single_per_sm);
   c->flat_per_sm = env_u("FSX_FLAT_PER_SM", c->flat_per_sm);
+  c->warp_per_sm = env_u("FSX_WARP_PER_SM", c->warp_per_sm);
+  if (const char* v = std::getenv("FSX_SGD_WARP")) c->sgd_warp = std::atoi(v) != 0;
   FSX_CUDA(cudaMalloc(&c->d_err, sizeof(DevErr)));
   FSX_CUDA(cudaMemset(c->d_err, 0, sizeof(DevErr)));
   FSX_CUDA(cudaMallocHost(&c->h_err, sizeof(DevErr)));

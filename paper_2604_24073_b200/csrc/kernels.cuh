@@ -577,6 +577,127 @@ __global__ void __launch_bounds__(256, 3) k_sgd_flat(SgdArgs<T> a, uint32_t vpr_
   }
 }
 
+// k_sgd_warp: the work items of k_sgd_flat (rows of 2+ occurrences, chunks of
+// hot rows), one warp per item. Lane l resolves the gradient row of occurrence
+// kb + l (32 index chains in parallel instead of one per 16-byte vector), the
+// warp then streams the rows U at a time — lane l moves vectors l, l + 32, …
+// (VPL per lane) — so per gradient vector a lane issues one load, VE
+// conversions and VE adds. The next item and its row pointers load while the
+// current item's rows are in flight. A multi-chunk row's chunks leave f64
+// partials; the warp that completes the row's last chunk (arrival counter
+// `done[u]`, reset by that warp) adds them in chunk order — the association
+// k_sgd_combine uses — and applies the row: no separate combine pass.
+template <class T, int VE, int VPL, int U>
+__global__ void __launch_bounds__(256) k_sgd_warp(SgdArgs<T> a, uint32_t* __restrict__ done) {
+  using V = VecOf<T, VE>;
+  constexpr unsigned kFull = 0xffffffffu;
+  const uint64_t nwork = *a.d_work_n;
+  const uint32_t dim = a.g.dim;
+  const uint32_t vpr = dim / VE;
+  const unsigned lane = threadIdx.x & 31u;
+  const uint64_t nw = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
+  uint64_t w = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+  if (w >= nwork) return;
+  SgdItem it = a.work[w];
+  const T* myp = it.kb + lane < it.ke ? a.grad(it.kb + lane) : nullptr;
+  while (true) {
+    const uint64_t wn = w + nw;
+    SgdItem nx{};
+    if (wn < nwork) nx = a.work[wn];
+    const bool single = (it.q & kSgdSingleChunk) != 0;
+    T* dst = reinterpret_cast<T*>(it.dst);
+    V old[VPL];
+    if (single && dst && !a.seg_out) {
+#pragma unroll
+      for (int v = 0; v < VPL; ++v)
+        if (lane + 32u * v < vpr) old[v] = *reinterpret_cast<const V*>(dst + (lane + 32u * v) * VE);
+    }
+    double acc[VPL][VE];
+#pragma unroll
+    for (int v = 0; v < VPL; ++v)
+#pragma unroll
+      for (int x = 0; x < VE; ++x) acc[v][x] = 0.0;
+    const T* myp_nx = nullptr;
+    bool nx_resolved = false;
+    for (uint32_t k0 = it.kb; k0 < it.ke; k0 += 32) {
+      const uint32_t nk = min(32u, it.ke - k0);
+      if (k0 != it.kb) myp = k0 + lane < it.ke ? a.grad(k0 + lane) : nullptr;
+      for (uint32_t t0 = 0; t0 < nk; t0 += U) {
+        V g[U][VPL];
+#pragma unroll
+        for (int t = 0; t < U; ++t) {
+          const T* p = reinterpret_cast<const T*>(
+              __shfl_sync(kFull, reinterpret_cast<unsigned long long>(myp), t0 + t));
+          if (t0 + t < nk) {
+#pragma unroll
+            for (int v = 0; v < VPL; ++v)
+              if (lane + 32u * v < vpr) g[t][v] = *reinterpret_cast<const V*>(p + (lane + 32u * v) * VE);
+          }
+        }
+        if (!nx_resolved) {  // next item's pointers load behind this batch
+          nx_resolved = true;
+          if (wn < nwork && nx.kb + lane < nx.ke) myp_nx = a.grad(nx.kb + lane);
+        }
+#pragma unroll
+        for (int t = 0; t < U; ++t)
+          if (t0 + t < nk) {
+#pragma unroll
+            for (int v = 0; v < VPL; ++v)
+#pragma unroll
+              for (int x = 0; x < VE; ++x) acc[v][x] = __dadd_rn(acc[v][x], static_cast<double>(g[t][v].v[x]));
+          }
+      }
+    }
+    if (!nx_resolved && wn < nwork && nx.kb + lane < nx.ke) myp_nx = a.grad(nx.kb + lane);
+    if (single) {
+      if (dst) {
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+          if (lane + 32u * v < vpr) sgd_store_vec<T, VE>(a, it.u, dst, (lane + 32u * v) * VE, acc[v], old[v]);
+      }
+    } else {
+      const uint64_t base = a.part_base[it.u];
+      double* pp = a.partials + (base + it.q) * dim;
+#pragma unroll
+      for (int v = 0; v < VPL; ++v)
+        if (lane + 32u * v < vpr) {
+#pragma unroll
+          for (int x = 0; x < VE; ++x) pp[(lane + 32u * v) * VE + x] = acc[v][x];
+        }
+      __syncwarp();
+      unsigned arrived = 0;
+      if (lane == 0) {
+        __threadfence();
+        arrived = atomicAdd(done + it.u, 1u);
+      }
+      arrived = __shfl_sync(kFull, arrived, 0);
+      const uint32_t len = a.rs.seg_start[it.u + 1] - a.rs.seg_start[it.u];
+      const uint32_t nch = (len + a.chunk - 1) / a.chunk;
+      if (arrived == nch - 1) {  // last chunk of the row: combine in chunk order
+        __threadfence();
+        const double* pb = a.partials + base * dim;
+#pragma unroll
+        for (int v = 0; v < VPL; ++v)
+          if (lane + 32u * v < vpr) {
+            const uint32_t col = (lane + 32u * v) * VE;
+            double c[VE];
+#pragma unroll
+            for (int x = 0; x < VE; ++x) c[x] = 0.0;
+            for (uint32_t q = 0; q < nch; ++q)
+#pragma unroll
+              for (int x = 0; x < VE; ++x) c[x] = __dadd_rn(c[x], __ldcg(pb + static_cast<uint64_t>(q) * dim + col + x));
+            sgd_apply_vec<T, VE>(a, it.u, col, c);
+          }
+        if (lane == 0) done[it.u] = 0;
+      }
+    }
+    if (wn >= nwork) break;
+    w = wn;
+    it = nx;
+    myp = myp_nx;
+  }
+}
+
 // one CTA per multi-chunk row, each thread owning VE columns: the row's chunk
 // partials are summed in chunk order (8 loads in flight per thread)
 template <class T, int VE>

@@ -10,6 +10,7 @@ struct SgdScratch {
   DevBuf<SgdItem> work, singles;
   DevBuf<const void*> gptr;  // gradient row per sorted occurrence
   DevBuf<uint32_t> multi, part_base;
+  DevBuf<uint32_t> done;     // k_sgd_warp: chunks arrived per row (kept zeroed)
   DevBuf<double> partials;
   DevBuf<uint64_t> d_tot;  // [0] singles, [1] work items, [2] multi rows, [3] partial slots
   ScanScratch scan;
@@ -24,6 +25,8 @@ struct SgdScratch {
       cap_work = w > cap_work ? w : cap_work;
       dim = d;
       work.alloc(cap_work); singles.alloc(cap_rows); multi.alloc(cap_rows); part_base.alloc(cap_rows);
+      done.alloc(cap_rows);
+      FSX_CUDA(cudaMemset(done.p, 0, cap_rows * sizeof(uint32_t)));
       gptr.alloc(occ > rows ? occ : rows);
       // a row with k > 1 chunks has > (k-1)*chunk occurrences: slots <= 2*occ/chunk
       partials.alloc(chunk ? (2 * occ / chunk + 1) * d : 1);
@@ -97,6 +100,19 @@ void sgd_apply(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_cap, uin
   const uint32_t shift = (vpr & (vpr - 1)) == 0 ? static_cast<uint32_t>(__builtin_ctz(vpr)) : 0xffffffffu;
   const unsigned g0 = grid_for(ctx, rows_cap * vpr / 2, 256, ctx->single_per_sm);
   const unsigned g1 = grid_for(ctx, work_cap * vpr, 256, ctx->flat_per_sm);
+  const unsigned vpl = (vpr + 31) / 32;
+  if (ve == VE16 && ctx->sgd_warp && vpl <= 4 && vpl != 3) {
+    // warp per work item, combine fused (k_sgd_warp)
+    FSX_LAUNCH(ctx, (k_sgd_single<T, VE16>), g0, 256, 0, stream, a, shift);
+    const unsigned gw = grid_for(ctx, work_cap * 32, 256, ctx->warp_per_sm);
+    if (vpl == 1)
+      FSX_LAUNCH(ctx, (k_sgd_warp<T, VE16, 1, 4>), gw, 256, 0, stream, a, s.done.p);
+    else if (vpl == 2)
+      FSX_LAUNCH(ctx, (k_sgd_warp<T, VE16, 2, 4>), gw, 256, 0, stream, a, s.done.p);
+    else
+      FSX_LAUNCH(ctx, (k_sgd_warp<T, VE16, 4, 2>), gw, 256, 0, stream, a, s.done.p);
+    return;
+  }
   if (ve == VE16) {
     FSX_LAUNCH(ctx, (k_sgd_single<T, VE16>), g0, 256, 0, stream, a, shift);
     FSX_LAUNCH(ctx, (k_sgd_flat<T, VE16>), g1, 256, 0, stream, a, shift);
