@@ -202,6 +202,22 @@ struct ReqBatch {  // requester view of one iteration's ids
   DevBuf<char*> out_ptr;
   DevBuf<uint64_t> bases;  // k_grp_bases layout
   std::vector<uint64_t> h_slots;  // collision rows per owner (pre-summed message rows)
+  // split sizes arrive asynchronously: pinned mirror [2*16 split | 16 slots]
+  // written by a D2H copy on L; the first reader waits on ev_sizes
+  uint64_t* hp_sizes = nullptr;
+  cudaEvent_t ev_sizes = nullptr;
+  bool sizes_pending = false, sizes_slots = false;
+  void sizes(int p) {
+    if (!sizes_pending) return;
+    FSX_CUDA(cudaEventSynchronize(ev_sizes));
+    h_split.assign(hp_sizes, hp_sizes + 2 * p);
+    if (sizes_slots) h_slots.assign(hp_sizes + 32, hp_sizes + 32 + p);
+    sizes_pending = false;
+  }
+  ~ReqBatch() {
+    if (hp_sizes) cudaFreeHost(hp_sizes);
+    if (ev_sizes) cudaEventDestroy(ev_sizes);
+  }
   void reserve(uint64_t cap) {
     if (ids.n >= cap && ids.p) return;
     ids.alloc(cap); send_pos.alloc(cap); split_rank.alloc(cap); send_dst.alloc(cap); flag.alloc(cap);
@@ -825,6 +841,26 @@ struct Engine {
   }
   // pack lists + E_ex prefetch + IDX of the next batch (its collision flags
   // come from collide)
+  // (a) pack lists of the next batch + their sizes on the host: all the
+  // collision chain's E_co pack needs (ev_pack)
+  void prefetch_pack(OwnBatch& on, cudaStream_t s) {
+    ev_pack = nullptr;
+    if (p == 1) return;
+    Span sp(this, FSX_PHASE_COLLIDE, s);
+    FSX_CUDA(cudaMemsetAsync(on.pack_tot(), 0, 32 * 8, s));
+    if (nc2() == 8) {
+      OwnerPackOp<8> op{on.bits.p, on.co.p, p, on.pack_tot(), on.ex_list.p, on.co_list.p, on.rank_us.p};
+      run_scan(ctx, op, on.m_cap, on.srt.d_u(), on.scan, on.pack_tot(), s);
+    } else {
+      OwnerPackOp<16> op{on.bits.p, on.co.p, p, on.pack_tot(), on.ex_list.p, on.co_list.p, on.rank_us.p};
+      run_scan(ctx, op, on.m_cap, on.srt.d_u(), on.scan, on.pack_tot(), s);
+    }
+    FSX_LAUNCH(ctx, k_sum_pairs, 1, 32, 0, s, on.pack_tot(), p, on.misc.p + 2);
+    ev_pack = record(s);
+    on.h_pack = fetch(on.pack_tot(), 2 * p, s);
+  }
+  cudaEvent_t ev_pack = nullptr;
+  // (b) E_ex prefetch + IDX of the next batch
   void prefetch(OwnBatch& on, ReqBatch& rn, cudaStream_t s) {
     Span sp(this, FSX_PHASE_COLLIDE, s);
     if (p == 1) {
@@ -840,28 +876,17 @@ struct Engine {
       rn.idx_par = ipar;
       return;
     }
-    // pack lists over next's unique rows: ex -> E_ex now, co -> E_co later
-    FSX_CUDA(cudaMemsetAsync(on.pack_tot(), 0, 32 * 8, s));
-    if (nc2() == 8) {
-      OwnerPackOp<8> op{on.bits.p, on.co.p, p, on.pack_tot(), on.ex_list.p, on.co_list.p, on.rank_us.p};
-      run_scan(ctx, op, on.m_cap, on.srt.d_u(), on.scan, on.pack_tot(), s);
-    } else {
-      OwnerPackOp<16> op{on.bits.p, on.co.p, p, on.pack_tot(), on.ex_list.p, on.co_list.p, on.rank_us.p};
-      run_scan(ctx, op, on.m_cap, on.srt.d_u(), on.scan, on.pack_tot(), s);
-    }
     const int par = next_par(CH_EX);
     Slots send = send_slots(CH_EX, par);
     FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, send, p, on.pack_tot(), 2, cap, ctx->d_err);
     IdRowPackMap pm{static_cast<const char*>(t->values), on.srt.uniq.p, on.srt.uniq_g.p, on.ex_list.p,
                     send, on.pack_tot(), 0, rb, me};
-    FSX_LAUNCH(ctx, k_sum_pairs, 1, 32, 0, s, on.pack_tot(), p, on.misc.p + 2);
     wait(s, ev_ex_applied);  // rows of the previous exclusive set may be prefetched now
     {
       Span sp2(this, FSX_PHASE_PREFETCH, s);
       launch_copy_rows(ctx, pm, on.m_cap * static_cast<uint64_t>(p), on.misc.p + 2, rb, s);
     }
     {
-      on.h_pack = fetch(on.pack_tot(), 2 * p, s);
       std::vector<uint64_t> bytes(p);
       for (int d = 0; d < p; ++d) bytes[d] = idrows_rows_off(on.h_pack[2 * d]) + rb * on.h_pack[2 * d];
       a2a(CH_EX, par, bytes, s);
@@ -908,9 +933,12 @@ struct Engine {
       }
       FSX_LAUNCH(ctx, k_grp_headers, 1, 32, 0, s, send, p, oc.grp_tot());
       if (p > 1) {
-        const std::vector<uint64_t> g = fetch(oc.grp_tot(), 2 * p, s);
-        std::vector<uint64_t> bytes(p);
-        for (int d = 0; d < p; ++d) bytes[d] = grp_list_off(g[2 * d + 1]) + 4 * g[2 * d];
+        // bounded copies (the whole slot) when small: no host round trip
+        std::vector<uint64_t> bytes(p, ch_slot[CH_GRP]);
+        if (ch_slot[CH_GRP] > kBoundedCopyMax) {
+          const std::vector<uint64_t> g = fetch(oc.grp_tot(), 2 * p, s);
+          for (int d = 0; d < p; ++d) bytes[d] = grp_list_off(g[2 * d + 1]) + 4 * g[2 * d];
+        }
         a2a(CH_GRP, par, bytes, s);
       }
       FSX_CUDA(cudaMemsetAsync(rc.flag.p, 0, rc.n ? rc.n : 1, s));
@@ -950,15 +978,16 @@ struct Engine {
       OccRankOp<16> op{oc.occ_src.p, oc.srt.inverse.p, with_co ? oc.co.p : nullptr, oc.occ_rank.p};
       run_scan(ctx, op, oc.m_cap, oc.srt.d_n(), oc.scan, oc.occ_tot(), s);
     }
-    if (p > 1 && with_co && presum()) {
-      // split counts + collision rows per owner, one host round trip
-      rc.h_split.resize(2 * p);
-      rc.h_slots.resize(p);
-      FSX_CUDA(cudaMemcpyAsync(rc.h_split.data(), rc.split_tot.p, 16 * p, cudaMemcpyDeviceToHost, s));
-      FSX_CUDA(cudaMemcpyAsync(rc.h_slots.data(), rc.bases.p + 34, 8 * p, cudaMemcpyDeviceToHost, s));
-      FSX_CUDA(cudaStreamSynchronize(s));
-    } else if (p > 1) {
-      rc.h_split = fetch(rc.split_tot.p, 2 * p, s);
+    if (p > 1) {
+      // split counts (+ collision rows per owner) go to pinned memory without
+      // a host round trip here: only the gradient all-to-alls of the coming
+      // backward need them, and they read them through rc.sizes()
+      rc.sizes_slots = with_co && presum();
+      FSX_CUDA(cudaMemcpyAsync(rc.hp_sizes, rc.split_tot.p, 16 * p, cudaMemcpyDeviceToHost, s));
+      if (rc.sizes_slots)
+        FSX_CUDA(cudaMemcpyAsync(rc.hp_sizes + 32, rc.bases.p + 34, 8 * p, cudaMemcpyDeviceToHost, s));
+      FSX_CUDA(cudaEventRecord(rc.ev_sizes, s));
+      rc.sizes_pending = true;
     }
   }
   // the CO_G parity the coming backward will use (next_par is taken there)
@@ -1091,6 +1120,9 @@ struct Engine {
   void prio_forward(const uint64_t* ids_cur, uint64_t n_cur, const uint64_t* ids_next,
                     uint64_t n_next, void* out, cudaStream_t c) {
     if (forward_done) raise(FSX_ERR_PROTOCOL, "embedding: forward called twice in one iteration");
+    // E_ex of this batch: recorded by the previous forward's side-lane prep
+    wait_next_ready();
+    cur_ex_ready = rn_ex_ready;
     const int i = iter;
     ReqBatch& rc = R(i);
     OwnBatch& oc = O(i);
@@ -1140,7 +1172,6 @@ struct Engine {
     auto prep1 = [this, i, bootstrap, with_next, n_next]() {
       ReqBatch& rc2 = R(i);
       OwnBatch& oc2 = O(i);
-      if (!bootstrap) apply_deferred();
       if (with_next) {
         ReqBatch& rn = R(i + 1);
         OwnBatch& on = O(i + 1);
@@ -1154,6 +1185,16 @@ struct Engine {
         if (!bootstrap) masks_and_split(oc2, rc2, false, lo);
       }
       ev_mask = bootstrap ? nullptr : record(lo);
+      // (host zeroing of the row: before the backward's stats copy is issued)
+      stats_forward(i, with_next);
+    };
+    const Deferred dfr = take_deferred();
+    auto prep2a = [this, dfr, with_next, i]() {
+      // the deferred exclusive update of i-1 after the masks: it has a whole
+      // iteration of slack and would only slow the chain the backward waits on
+      apply_deferred(dfr);
+      if (with_next) prefetch_pack(O(i + 1), lo);
+      else ev_pack = nullptr;
     };
     auto prep2 = [this, i, with_next]() {
       if (with_next) {
@@ -1167,14 +1208,15 @@ struct Engine {
         ev_next_ready = nullptr;
         rn_ex_ready = nullptr;
       }
-      stats_forward(i, with_next);
     };
     cudaEvent_t ex_ready_cur = cur_ex_ready;  // E_ex(i), recorded by the previous prep
     if (side) {
       ticket_mask = side->post(prep1);
+      ticket_pack = side->post(prep2a);
       ticket_next = side->post(prep2);
     } else {
       prep1();
+      prep2a();
       prep2();
     }
     // ---- compute stream C: serve iteration i ----
@@ -1193,7 +1235,10 @@ struct Engine {
     has_next = ids_next != nullptr;
   }
   cudaEvent_t cur_ex_ready = nullptr, cur_co_ready = nullptr, rn_ex_ready = nullptr;
-  uint64_t ticket_mask = 0, ticket_next = 0;  // side-lane jobs of the last forward
+  uint64_t ticket_mask = 0, ticket_pack = 0, ticket_next = 0;  // side-lane jobs of the last forward
+  void wait_pack_ready() {
+    if (side) side->wait_for(ticket_pack);
+  }
   void wait_next_ready() {
     if (side) side->wait_for(ticket_next);
   }
@@ -1204,23 +1249,35 @@ struct Engine {
   // prefetch reads rows, so routing / dedup / collision overlap with them
   cudaEvent_t ev_ex_applied = nullptr;
   cudaEvent_t ev_hchain = nullptr;  // end of the last backward's collision chain
-  void apply_deferred() {
+  // The deferred state is taken by the caller's thread when the forward posts
+  // the side-lane job (the next backward overwrites it while that job waits).
+  struct Deferred {
+    bool pending = false;
+    int iter = -1, par = -1;
+    cudaEvent_t split = nullptr, hchain = nullptr;
+  };
+  Deferred take_deferred() {
+    Deferred d{has_pending, pending_iter, exg_par, ev_pending_split, ev_hchain};
+    has_pending = false;
+    return d;
+  }
+  void apply_deferred(const Deferred& d) {
     ev_ex_applied = nullptr;
-    if (!has_pending) return;
-    OwnBatch& op = O(pending_iter);
-    ReqBatch& rp = R(pending_iter);
-    wait(ux, ev_pending_split);
+    if (!d.pending) return;
+    OwnBatch& op = O(d.iter);
+    ReqBatch& rp = R(d.iter);
+    wait(ux, d.split);
     // the collision chain of that iteration has the links first: the
     // exclusive gradients have a whole iteration of slack
-    if (ev_hchain) wait(ux, ev_hchain);
+    if (d.hchain) wait(ux, d.hchain);
     if (p > 1) {
       std::vector<uint64_t> bytes(p);
-      for (int d = 0; d < p; ++d) bytes[d] = kHdr + rb * rp.h_split[2 * d];
-      a2a(CH_EXG, exg_par, bytes, ux);
+      rp.sizes(p);
+      for (int d2 = 0; d2 < p; ++d2) bytes[d2] = kHdr + rb * rp.h_split[2 * d2];
+      a2a(CH_EXG, d.par, bytes, ux);
     }
-    update(op, CH_EXG, exg_par, op.has_co ? op.co.p : nullptr, 0, true, ux, FSX_PHASE_EX_UPDATE);
+    update(op, CH_EXG, d.par, op.has_co ? op.co.p : nullptr, 0, true, ux, FSX_PHASE_EX_UPDATE);
     ev_ex_applied = record(ux);
-    has_pending = false;
   }
 
   void prio_backward(const void* grads, cudaStream_t c) {
@@ -1265,13 +1322,14 @@ struct Engine {
         if (presum()) {
           if (p > 1) {
             std::vector<uint64_t> bytes(p);
+            rc.sizes(p);
             for (int d = 0; d < p; ++d) bytes[d] = kHdr + rb * rc.h_slots[d];
             a2a(CH_COG, cog, bytes, hi);
           }
           Span sp(this, FSX_PHASE_CO_UPDATE, hi);
           if (has_next && p > 1) {
-            wait_next_ready();
-            wait(hi, ev_next_ready);
+            wait_pack_ready();
+            wait(hi, ev_pack);
             fused_cor = next_par(CH_COR);
             co_apply(oc, cog, hi, &O(i + 1), fused_cor);
           } else {
@@ -1280,6 +1338,7 @@ struct Engine {
         } else {
           if (p > 1) {
             std::vector<uint64_t> bytes(p);
+            rc.sizes(p);
             for (int d = 0; d < p; ++d) bytes[d] = kHdr + rb * rc.h_split[2 * d + 1];
             a2a(CH_COG, cog, bytes, hi);
           }
@@ -1288,14 +1347,13 @@ struct Engine {
         have_grads = true;
       }
     }
-    wait_next_ready();
-    cur_ex_ready = rn_ex_ready;
+    wait_pack_ready();
     if (has_next) {
       // E_co^{i+1}: fresh collision rows to the next iteration's requesters
       OwnBatch& on = O(i + 1);
       ReqBatch& rn = R(i + 1);
       wait(hi, ev_chain_start);
-      wait(hi, ev_next_ready);
+      if (ev_pack) wait(hi, ev_pack);
       if (fused_cor >= 0) {
         Span sp(this, FSX_PHASE_ECO, hi);
         std::vector<uint64_t> bytes(p);
@@ -1320,7 +1378,7 @@ struct Engine {
 
   void finalize(cudaStream_t c) {
     if (side) side->drain();
-    apply_deferred();
+    apply_deferred(take_deferred());
     wait(c, record(lo));
     wait(c, record(hi));
     wait(c, record(ux));
@@ -1466,6 +1524,8 @@ int fsx_engine_create(fsx_ctx* ctx, fsx_table* table, const fsx_engine_config* c
   e->d_stats.alloc(16);
   const uint64_t m = static_cast<uint64_t>(e->p) * cap;
   for (int k = 0; k < 3; ++k) {
+    FSX_CUDA(cudaHostAlloc(&e->rq[k].hp_sizes, 48 * 8, cudaHostAllocDefault));
+    FSX_CUDA(cudaEventCreateWithFlags(&e->rq[k].ev_sizes, cudaEventDisableTiming));
     e->rq[k].reserve(cap);
     e->rq[k].scan.ensure(cap, 16);
     e->ow[k].reserve(m);
