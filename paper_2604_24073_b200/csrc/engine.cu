@@ -202,6 +202,7 @@ struct ReqBatch {  // requester view of one iteration's ids
   DevBuf<char*> out_ptr;
   DevBuf<uint64_t> bases;  // k_grp_bases layout
   std::vector<uint64_t> h_slots;  // collision rows per owner (pre-summed message rows)
+  SgdScratch plan;  // PRESUM: work lists of the collision pre-sum, built on L
   // split sizes arrive asynchronously: pinned mirror [2*16 split | 16 slots]
   // written by a D2H copy on L; the first reader waits on ev_sizes
   uint64_t* hp_sizes = nullptr;
@@ -947,6 +948,13 @@ struct Engine {
       FSX_LAUNCH(ctx, k_grp_flatten, grid_for(ctx, static_cast<uint64_t>(p) * (cap + 1), 256, 8), 256, 0, s,
                  grp, p, cap, rc.bases.p, rc.send_off(), rc.send_pos.p, send_slots(CH_COG, cog_par_next()),
                  rb, rc.flag.p, rc.seg_flat.p, rc.perm_flat.p, rc.out_ptr.p);
+      // the pre-sum's work lists: the segments and the caller's gradient
+      // positions are known now, the gradients only at the backward
+      RowSegments prs{nullptr, rc.seg_flat.p, rc.perm_flat.p, rc.bases.p + 16, nullptr, 0};
+      if (t->dtype == FSX_F32)
+        sgd_plan<float>(ctx, *t, prs, rc.n, rc.n, nullptr, cfg.reduce_chunk, rc.plan, s, rc.out_ptr.p);
+      else
+        sgd_plan<double>(ctx, *t, prs, rc.n, rc.n, nullptr, cfg.reduce_chunk, rc.plan, s, rc.out_ptr.p);
     } else if (with_co) {
       const int par = next_par(CH_MASK);
       Slots send = send_slots(CH_MASK, par);
@@ -1045,12 +1053,13 @@ struct Engine {
     // the CO_G messages (same chunked reduce as the owner, reduce-only mode)
     RowSegments rs{nullptr, r.seg_flat.p, r.perm_flat.p, r.bases.p + 16, nullptr, 0};
     const uint64_t segs_cap = r.n;  // a segment holds >= 1 occurrence
+    // work lists planned on L (masks_and_split); gradient row j = occurrence j
     if (t->dtype == FSX_F32) {
       GradRows<float> gr{static_cast<const char*>(d_grads), 0, nullptr, nullptr, rb};
-      sgd_update_rows<float>(ctx, *t, rs, segs_cap, r.n, gr, cfg.reduce_chunk, sgd_for(s), nullptr, s, r.out_ptr.p);
+      sgd_apply<float>(ctx, *t, rs, segs_cap, r.n, gr, cfg.reduce_chunk, r.plan, nullptr, s, r.out_ptr.p);
     } else {
       GradRows<double> gr{static_cast<const char*>(d_grads), 0, nullptr, nullptr, rb};
-      sgd_update_rows<double>(ctx, *t, rs, segs_cap, r.n, gr, cfg.reduce_chunk, sgd_for(s), nullptr, s, r.out_ptr.p);
+      sgd_apply<double>(ctx, *t, rs, segs_cap, r.n, gr, cfg.reduce_chunk, r.plan, nullptr, s, r.out_ptr.p);
     }
     FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, co, p, r.bases.p + 34, 1, cap, ctx->d_err);
   }
@@ -1527,6 +1536,7 @@ int fsx_engine_create(fsx_ctx* ctx, fsx_table* table, const fsx_engine_config* c
     FSX_CUDA(cudaHostAlloc(&e->rq[k].hp_sizes, 48 * 8, cudaHostAllocDefault));
     FSX_CUDA(cudaEventCreateWithFlags(&e->rq[k].ev_sizes, cudaEventDisableTiming));
     e->rq[k].reserve(cap);
+    if (prio && (cfg->flags & FSX_ENGINE_PRESUM)) e->rq[k].plan.reserve(cap, cap, table->g.dim, cfg->reduce_chunk);
     e->rq[k].scan.ensure(cap, 16);
     e->ow[k].reserve(m);
     e->ow[k].scan.ensure(m, 16);
