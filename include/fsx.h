@@ -264,6 +264,18 @@ int fsx_a2a_ce(fsx_engine* e, const void* d_send, const uint64_t* h_send_offsets
                const uint64_t* h_send_bytes, void* d_recv, uint64_t slot_bytes,
                uint64_t* h_recv_bytes, void* stream);
 
+/* ---- copy-engine all-gather (comm.cpp:185-306 analogue) --------------------- */
+/* Collective: every rank contributes send_bytes bytes (<= max_bytes, the bound
+ * every rank passes identically); on return d_recv + d * slot_bytes holds rank
+ * d's bytes and h_recv_bytes[d] their size. ring = 0: direct copies to every
+ * peer (all_gather, comm.cpp:185-259 — on NVSwitch each peer link runs at full
+ * bandwidth); ring = 1: the reference's SmFree ring, p-1 forwarding stages
+ * (ring_all_gather, comm.cpp:214-236 / 261-306). 0 SMs: copy engines and stream
+ * memory operations only. CollectiveError if a chunk exceeds the bound or the
+ * engine's all-gather slot (max(8 * max_occurrences, 64 KiB) bytes). */
+int fsx_allgather_ce(fsx_engine* e, const void* d_send, uint64_t send_bytes, uint64_t max_bytes, void* d_recv,
+                     uint64_t slot_bytes, uint64_t* h_recv_bytes, int ring, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

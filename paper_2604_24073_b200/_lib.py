@@ -82,6 +82,7 @@ _SIGS = {
     "fsx_autotune_update": ([i32, vp, vp, P(dbl), i32, dbl, dbl, vp], i32),
     "fsx_engine_slot_bytes": ([vp], u64),
     "fsx_a2a_ce": ([vp, vp, vp, vp, vp, u64, vp, vp], i32),
+    "fsx_allgather_ce": ([vp, vp, u64, u64, vp, u64, vp, i32, vp], i32),
 }
 
 EXPORTED = sorted(_SIGS)

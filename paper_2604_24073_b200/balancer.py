@@ -27,6 +27,8 @@ from typing import Callable, Optional
 
 import numpy as np
 
+from . import _lib
+
 from . import partition as P
 from .errors import ConfigError, ProtocolError
 
@@ -158,6 +160,67 @@ class LocalComm:
 
     def all_to_all_u64(self, parts):
         return [np.asarray(parts[0], np.uint64).copy()]
+
+
+class CeComm:
+    """The balancer's collectives on the copy engines (0 SMs), over an
+    embedding engine's receive windows: all_gather (comm.cpp:185-306; the
+    direct schedule, or ring=True for the reference's SmFree ring
+    comm.cpp:214-236) through fsx_allgather_ce, all_to_all (comm.cpp:308-365)
+    through fsx_a2a_ce. Variable sizes go in a first round (like
+    TorchComm); every call synchronizes the engine's device."""
+
+    def __init__(self, engine, ring: bool = False):
+        import torch
+        self.torch, self.e, self.ring = torch, engine, bool(ring)
+        self.dev = engine.shard.ctx.torch_device
+
+    def rank(self) -> int:
+        return self.e.comm.rank()
+
+    def world_size(self) -> int:
+        return self.e.comm.world_size()
+
+    def _stream(self):
+        return self.torch.cuda.current_stream(self.dev).cuda_stream
+
+    def _gather(self, a: np.ndarray, bound: int) -> list:
+        import ctypes as C
+        torch, w = self.torch, self.world_size()
+        a = np.ascontiguousarray(a, np.uint64)
+        slot = max(int(bound), 8)
+        send = torch.from_numpy(a.view(np.int64).copy()).to(self.dev) if a.size else \
+            torch.zeros(1, dtype=torch.int64, device=self.dev)
+        recv = torch.zeros(w * slot // 8, dtype=torch.int64, device=self.dev)
+        got = (C.c_uint64 * w)()
+        _lib.call("fsx_allgather_ce", self.e.h, C.c_void_p(send.data_ptr()), a.nbytes, slot,
+                  C.c_void_p(recv.data_ptr()), slot, got, int(self.ring), C.c_void_p(self._stream()))
+        host = recv.cpu().numpy().view(np.uint64)
+        return [host[d * slot // 8: d * slot // 8 + got[d] // 8].copy() for d in range(w)]
+
+    def all_gather_u64(self, a: np.ndarray) -> list:
+        sizes = [int(x[0]) for x in self._gather(np.array([np.asarray(a).size], np.uint64), 8)]
+        return self._gather(a, 8 * max(sizes + [1]))
+
+    def all_to_all_u64(self, parts: list) -> list:
+        import ctypes as C
+        torch, w = self.torch, self.world_size()
+        parts = [np.ascontiguousarray(p, np.uint64) for p in parts]
+        # size round: every rank's row of the send matrix
+        mat = self.all_gather_u64(np.array([p.size for p in parts], np.uint64))
+        # one slot size on every rank (the sender checks its payloads against it)
+        slot = 8 * max([int(x) for row in mat for x in row] + [1])
+        flat = np.concatenate(parts) if parts else np.zeros(0, np.uint64)
+        send = torch.from_numpy(flat.view(np.int64).copy()).to(self.dev) if flat.size else \
+            torch.zeros(1, dtype=torch.int64, device=self.dev)
+        offs = (C.c_uint64 * w)(*np.concatenate([[0], np.cumsum([8 * p.size for p in parts])[:-1]]).astype(int))
+        nbytes = (C.c_uint64 * w)(*[8 * p.size for p in parts])
+        recv = torch.zeros(w * slot // 8, dtype=torch.int64, device=self.dev)
+        got = (C.c_uint64 * w)()
+        _lib.call("fsx_a2a_ce", self.e.h, C.c_void_p(send.data_ptr()), offs, nbytes, C.c_void_p(recv.data_ptr()),
+                  slot, got, C.c_void_p(self._stream()))
+        host = recv.cpu().numpy().view(np.uint64)
+        return [host[d * slot // 8: d * slot // 8 + got[d] // 8].copy() for d in range(w)]
 
 
 # ---- balancer ---------------------------------------------------------------------------

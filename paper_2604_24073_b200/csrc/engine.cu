@@ -39,7 +39,7 @@
 
 namespace fsx {
 
-enum Channel : int { CH_IDS, CH_ROWS, CH_GRADS, CH_EX, CH_MASK, CH_COG, CH_EXG, CH_COR, CH_IDX, CH_GRP, NCH };
+enum Channel : int { CH_IDS, CH_ROWS, CH_GRADS, CH_EX, CH_MASK, CH_COG, CH_EXG, CH_COR, CH_IDX, CH_GRP, CH_AG, NCH };
 
 // ---- NCCL, loaded at run time (baseline transport only) ----------------------
 struct NcclApi {
@@ -655,6 +655,76 @@ struct Engine {
                                    CU_STREAM_WAIT_VALUE_GEQ));
       }
     }
+  }
+
+  // ---- copy-engine all-gather (comm.cpp:185-306 analogue) -------------------
+  // Every rank's chunk (16-byte header + payload) sits in its own receive slot
+  // `me` of channel CH_AG (parity par); afterwards slot d holds rank d's chunk
+  // on every rank. ring == false: each rank copies its chunk straight to every
+  // peer (NVSwitch: full bandwidth to each). ring == true: the reference's
+  // SmFree schedule (comm.cpp:214-236) — p-1 stages, at stage st rank r
+  // forwards chunk (r - st) mod p to r + 1, each stage gated on the previous
+  // stage's arrival from r - 1. Flag values: one sequence number per stage.
+  uint32_t ag_calls = 0;
+  void all_gather_ce(int par, uint64_t bytes, bool ring, cudaStream_t s) {
+    if (p == 1) return;
+    Span sp(this, FSX_PHASE_A2A, s);
+    const int ch = CH_AG;
+    auto peer_slot = [&](int d, int chunk) {
+      return peer[d].base + ch_off[ch] + (static_cast<size_t>(par) * p + chunk) * ch_slot[ch];
+    };
+    auto send = [&](cudaStream_t cs, int d, int chunk, uint64_t n, uint32_t v) {
+      const PeerView& pv = peer[d];
+      if (!pv.base) raise(FSX_ERR_COLLECTIVE, "all_gather: peer " + std::to_string(d) + " not connected");
+      if (n) FSX_CUDA(cudaMemcpyAsync(peer_slot(d, chunk), recv_slot(ch, par, chunk), n, cudaMemcpyDefault, cs));
+      if (pv.local) {
+        cudaEvent_t ev;
+        FSX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        FSX_CUDA(cudaEventRecord(ev, cs));
+        Hub::get().post(pv.local, ch, v, me, ev);
+      } else {
+        FSX_CU(drv::write_value32()(reinterpret_cast<CUstream>(cs),
+                                    reinterpret_cast<CUdeviceptr>(pv.flags + ch * kMaxRanks + me), v,
+                                    CU_STREAM_WRITE_VALUE_DEFAULT));
+      }
+    };
+    auto recv_wait = [&](cudaStream_t ws, int src, uint32_t v) {
+      if (peer[src].local) {
+        cudaEvent_t ev = Hub::get().take(this, ch, v, src);
+        FSX_CUDA(cudaStreamWaitEvent(ws, ev, 0));
+        FSX_CUDA(cudaEventDestroy(ev));
+      } else {
+        FSX_CU(drv::wait_value32()(reinterpret_cast<CUstream>(ws),
+                                   reinterpret_cast<CUdeviceptr>(flags + ch * kMaxRanks + src), v,
+                                   CU_STREAM_WAIT_VALUE_GEQ));
+      }
+    };
+    cudaEvent_t fork = record(s);
+    if (!ring) {
+      const uint32_t v = ++seq[ch];
+      for (int k = 1; k < p; ++k) {
+        const int d = (me + k) % p;
+        cudaStream_t cs = cstream[lane_of(s)][d];
+        wait(cs, fork);
+        send(cs, d, me, kHdr + bytes, v);
+        wait(s, record(cs));
+      }
+      for (int k = 1; k < p; ++k) recv_wait(s, (me + p - k) % p, v);
+      return;
+    }
+    // ring: chunk sizes differ per rank, so every stage moves the whole slot
+    // prefix the largest chunk can occupy (bytes is the caller's bound)
+    const int right = (me + 1) % p, left = (me + p - 1) % p;
+    cudaStream_t cs = cstream[lane_of(s)][right];
+    wait(cs, fork);
+    const uint32_t v0 = seq[ch];
+    for (int st = 0; st < p - 1; ++st) {
+      if (st > 0) recv_wait(cs, left, v0 + st);  // chunk (me - st) arrived at stage st - 1
+      send(cs, right, ((me - st) % p + p) % p, kHdr + bytes, v0 + st + 1);
+    }
+    seq[ch] = v0 + p - 1;
+    recv_wait(s, left, v0 + p - 1);
+    wait(s, record(cs));
   }
 
   int nc2() const { return p <= 4 ? 8 : 16; }  // counters for 2p classes
@@ -1491,6 +1561,7 @@ int fsx_engine_create(fsx_ctx* ctx, fsx_table* table, const fsx_engine_config* c
   slot[CH_IDS] = kHdr + cap * 8;
   slot[CH_ROWS] = kHdr + cap * rb;
   slot[CH_GRADS] = kHdr + cap * rb;
+  slot[CH_AG] = kHdr + std::max<uint64_t>(cap * 8, 1u << 16);  // fsx_allgather_ce chunks
   if (prio) {
     slot[CH_EX] = idrows_rows_off(cap) + cap * rb;
     slot[CH_MASK] = kHdr + align16(cap);
@@ -1761,6 +1832,42 @@ uint64_t fsx_engine_slot_bytes(const fsx_engine* e) { return e ? e->ch_slot[CH_G
 
 // Byte all-to-all over the engine's GRADS channel (comm.cpp:308-365 shape:
 // size round, then payloads); collective, between iterations only.
+int fsx_allgather_ce(fsx_engine* e, const void* d_send, uint64_t send_bytes, uint64_t max_bytes, void* d_recv,
+                     uint64_t slot_bytes, uint64_t* h_recv_bytes, int ring, void* stream) {
+  FSX_API_BEGIN
+  DeviceGuard dg(e->ctx->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint64_t cap = e->ch_slot[CH_AG] - kHdr;
+  if (max_bytes < send_bytes) max_bytes = send_bytes;
+  if (max_bytes > cap || max_bytes > slot_bytes)
+    raise(FSX_ERR_COLLECTIVE, "all_gather: payload of " + std::to_string(max_bytes) +
+                                  " bytes exceeds the slot capacity");
+  if (e->side) e->side->drain();
+  const int p = e->p, me = e->me;
+  const int par = static_cast<int>(++e->ag_calls & 1u);
+  char* mine = e->recv_slot(CH_AG, par, me);
+  const uint64_t hdr[2] = {send_bytes, 0};
+  FSX_CUDA(cudaMemcpyAsync(mine, hdr, kHdr, cudaMemcpyHostToDevice, s));
+  if (send_bytes) FSX_CUDA(cudaMemcpyAsync(mine + kHdr, d_send, send_bytes, cudaMemcpyDeviceToDevice, s));
+  FSX_CUDA(cudaStreamSynchronize(s));  // the host header above is stack memory
+  e->all_gather_ce(par, max_bytes, ring != 0, s);
+  std::vector<uint64_t> h(2 * p);
+  for (int d = 0; d < p; ++d)
+    FSX_CUDA(cudaMemcpyAsync(&h[2 * d], e->recv_slot(CH_AG, par, d), kHdr, cudaMemcpyDeviceToHost, s));
+  FSX_CUDA(cudaStreamSynchronize(s));
+  for (int d = 0; d < p; ++d) {
+    if (h[2 * d] > max_bytes)
+      raise(FSX_ERR_COLLECTIVE, "all_gather: rank " + std::to_string(d) + " sent " + std::to_string(h[2 * d]) +
+                                    " bytes, above the agreed bound " + std::to_string(max_bytes));
+    h_recv_bytes[d] = h[2 * d];
+    if (h[2 * d])
+      FSX_CUDA(cudaMemcpyAsync(static_cast<char*>(d_recv) + d * slot_bytes, e->recv_slot(CH_AG, par, d) + kHdr,
+                               h[2 * d], cudaMemcpyDeviceToDevice, s));
+  }
+  FSX_CUDA(cudaStreamSynchronize(s));
+  FSX_API_END
+}
+
 int fsx_a2a_ce(fsx_engine* e, const void* d_send, const uint64_t* h_send_offsets,
                const uint64_t* h_send_bytes, void* d_recv, uint64_t slot_bytes, uint64_t* h_recv_bytes,
                void* stream) {

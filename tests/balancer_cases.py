@@ -35,3 +35,18 @@ def sorted_round_robin(metas, n):
         a[g] = k % n
         ro[k % n].append(g)
     return P.PartitionPlan(n, a, [np.asarray(o, np.uint64) for o in ro])
+
+
+def expected_batches(iters, world, partition):
+    """The reference's assemble semantics (balancer.cpp:224-252): rank r's
+    balanced batch = the global samples in plan.receive_order[r]."""
+    exp = []
+    for i in range(iters):
+        raws = [make_raw(i, r, world) for r in range(world)]
+        metas = [P.GlobalSampleMeta(r, k, int(s.uih.size), len(s.candidates))
+                 for r in range(world) for k, s in enumerate(raws[r].samples)]
+        glob = [s for r in range(world) for s in raws[r].samples]
+        plan = (P.identity_partition(metas, world) if partition == "none"
+                else sorted_round_robin(metas, world))
+        exp.append([[glob[int(g)] for g in plan.receive_order[r]] for r in range(world)])
+    return exp

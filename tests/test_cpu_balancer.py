@@ -12,7 +12,7 @@ import sys
 import numpy as np
 import pytest
 
-from balancer_cases import make_raw, sorted_round_robin
+from balancer_cases import expected_batches, make_raw
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 
@@ -26,17 +26,7 @@ def _port():
 
 
 def _expected(iters, world, partition):
-    from paper_2604_24073_b200 import partition as P
-    exp = []
-    for i in range(iters):
-        raws = [make_raw(i, r, world) for r in range(world)]
-        metas = [P.GlobalSampleMeta(r, k, int(s.uih.size), len(s.candidates))
-                 for r in range(world) for k, s in enumerate(raws[r].samples)]
-        glob = [s for r in range(world) for s in raws[r].samples]
-        plan = (P.identity_partition(metas, world) if partition == "none"
-                else sorted_round_robin(metas, world))
-        exp.append([[glob[int(g)] for g in plan.receive_order[r]] for r in range(world)])
-    return exp
+    return expected_batches(iters, world, partition)
 
 
 @pytest.mark.parametrize("partition,lead", [("none", 1), ("custom:sorted_rr", 1), ("custom:sorted_rr", 2)])
