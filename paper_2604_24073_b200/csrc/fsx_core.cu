@@ -159,6 +159,11 @@ int fsx_ctx_create(int device, int rank, int world, fsx_ctx** out) {
   c->flat_per_sm = env_u("FSX_FLAT_PER_SM", c->flat_per_sm);
   c->warp_per_sm = env_u("FSX_WARP_PER_SM", c->warp_per_sm);
   if (const char* v = std::getenv("FSX_SGD_WARP")) c->sgd_warp = std::atoi(v) != 0;
+  // measured (bench, B200): at one rank the look-back CTAs' spinning costs the
+  // concurrent update more than the saved launches give the side lane; with
+  // peers the side lane's sort is on the critical path and onesweep wins
+  c->onesweep = world > 1;
+  if (const char* v = std::getenv("FSX_ONESWEEP")) c->onesweep = std::atoi(v) != 0;
   FSX_CUDA(cudaMalloc(&c->d_err, sizeof(DevErr)));
   FSX_CUDA(cudaMemset(c->d_err, 0, sizeof(DevErr)));
   FSX_CUDA(cudaMallocHost(&c->h_err, sizeof(DevErr)));

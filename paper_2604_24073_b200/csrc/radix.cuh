@@ -167,8 +167,158 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(
   }
 }
 
+// ---- onesweep variant (FSX_ONESWEEP, default on) ------------------------------
+// One launch computes every pass's global digit histogram (one read of the
+// keys); each pass is then ONE launch: CTAs take tiles in order from a
+// counter, rank keys inside the tile exactly as k_radix_scatter does, publish
+// the tile's per-digit count, and find the count of all earlier tiles by
+// decoupled look-back over those published words (aggregate / inclusive
+// flags) instead of a separate per-tile histogram + scan. 1 + passes launches
+// instead of 3 * passes; same stable order.
+constexpr int kOsMaxPasses = 8;
+constexpr uint32_t kOsAgg = 1u << 30, kOsIncl = 2u << 30, kOsCount = (1u << 30) - 1u;
+
+template <class K>
+__global__ void __launch_bounds__(kRadixThreads) k_os_hist(const K* __restrict__ keys, uint64_t n_cap,
+                                                           const uint64_t* d_n, int passes, int dbits,
+                                                           uint32_t* __restrict__ hist) {
+  __shared__ uint32_t h[kOsMaxPasses][kRadixBins];
+  for (int i = threadIdx.x; i < kOsMaxPasses * kRadixBins; i += blockDim.x) (&h[0][0])[i] = 0;
+  __syncthreads();
+  const uint64_t n = scan_n(n_cap, d_n);
+  const unsigned mask = (1u << dbits) - 1u;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t n_round = (n + 31) & ~uint64_t{31};  // whole warps through match_any
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n_round; i += stride) {
+    const bool valid = i < n;
+    const K k = valid ? keys[i] : K(0);
+    for (int ps = 0; ps < passes; ++ps) {
+      const unsigned d = valid ? static_cast<unsigned>((k >> (ps * dbits)) & mask) : 0xffffu;
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      if (valid && (peers & lanemask_lt()) == 0) atomicAdd(&h[ps][d], __popc(peers));
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < passes * kRadixBins; i += blockDim.x) {
+    const uint32_t c = (&h[0][0])[i];
+    if (c) atomicAdd(hist + i, c);
+  }
+}
+
+template <class K>
+__global__ void __launch_bounds__(kRadixThreads) k_os_scatter(
+    const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
+    uint32_t* __restrict__ vout, uint64_t n_cap, const uint64_t* d_n, int shift, unsigned mask,
+    const uint32_t* __restrict__ digit_total, uint32_t* status, uint32_t* tile_ctr) {
+  __shared__ uint32_t wcount[kRadixWarps][kRadixBins];
+  __shared__ uint32_t tile_off[kRadixBins];
+  __shared__ uint32_t wsum[kRadixWarps];
+  __shared__ uint32_t s_tile;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1u);
+  for (int w = 0; w < kRadixWarps; ++w)
+    for (int b = 0; b < kBinsPerThread; ++b) wcount[w][threadIdx.x + b * kRadixThreads] = 0;
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t n = scan_n(n_cap, d_n);
+  const uint64_t tile_base = static_cast<uint64_t>(tile) * kRadixTile;
+  if (tile_base >= n) return;
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  const unsigned bins = mask + 1;
+  // digit base = exclusive scan of the pass's global digit totals (each
+  // thread owns kBinsPerThread consecutive digits)
+  {
+    uint32_t tot[kBinsPerThread], own = 0;
+    for (int b = 0; b < kBinsPerThread; ++b) {
+      const unsigned d = threadIdx.x * kBinsPerThread + b;
+      tot[b] = d < bins ? digit_total[d] : 0u;
+      own += tot[b];
+    }
+    uint32_t x = own;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= static_cast<unsigned>(o)) x += y;
+    }
+    if (lane == 31) wsum[warp] = x;
+    __syncthreads();
+    uint32_t run = x - own;
+    for (unsigned w = 0; w < warp; ++w) run += wsum[w];
+    for (int b = 0; b < kBinsPerThread; ++b) {
+      const unsigned d = threadIdx.x * kBinsPerThread + b;
+      if (d < bins) tile_off[d] = run;
+      run += tot[b];
+    }
+  }
+  const uint64_t base = tile_base + warp * kRadixWarpItems;
+  K k[kRadixRounds];
+  uint32_t v[kRadixRounds], rk[kRadixRounds];
+  unsigned dg[kRadixRounds];
+#pragma unroll
+  for (int r = 0; r < kRadixRounds; ++r) {
+    const uint64_t i = base + r * 32 + lane;
+    const bool valid = i < n;
+    k[r] = valid ? kin[i] : K(0);
+    v[r] = valid ? (vin ? vin[i] : static_cast<uint32_t>(i)) : 0u;
+    dg[r] = valid ? static_cast<unsigned>((k[r] >> shift) & mask) : 0xffffu;
+  }
+#pragma unroll
+  for (int r = 0; r < kRadixRounds; ++r) {
+    const unsigned d = dg[r];
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const unsigned before = __popc(peers & lanemask_lt());
+    uint32_t run = d <= mask ? wcount[warp][d] : 0u;
+    rk[r] = run + before;
+    __syncwarp();
+    if (d <= mask && before == 0) wcount[warp][d] = run + __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  // per digit: warps' exclusive offsets, the tile's count, then look-back
+  uint32_t* my = status + static_cast<uint64_t>(tile) * kRadixBins;
+  for (int b = 0; b < kBinsPerThread; ++b) {
+    const unsigned d = threadIdx.x + b * kRadixThreads;
+    uint32_t run = 0;
+    for (int w = 0; w < kRadixWarps; ++w) {
+      const uint32_t x = wcount[w][d];
+      wcount[w][d] = run;
+      run += x;
+    }
+    if (d >= bins) continue;
+    if (tile == 0) {
+      *reinterpret_cast<volatile uint32_t*>(my + d) = kOsIncl | run;
+      continue;
+    }
+    *reinterpret_cast<volatile uint32_t*>(my + d) = kOsAgg | run;
+    uint32_t acc = 0;
+    for (int64_t t = static_cast<int64_t>(tile) - 1; t >= 0;) {
+      const uint32_t st = *reinterpret_cast<volatile const uint32_t*>(status + static_cast<uint64_t>(t) * kRadixBins + d);
+      if ((st & ~kOsCount) == 0) continue;  // not published yet: spin
+      acc += st & kOsCount;
+      if (st & kOsIncl) break;
+      --t;
+    }
+    *reinterpret_cast<volatile uint32_t*>(my + d) = kOsIncl | (acc + run);
+    tile_off[d] += acc;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kRadixRounds; ++r) {
+    const unsigned d = dg[r];
+    if (d <= mask) {
+      const uint32_t pos = tile_off[d] + wcount[warp][d] + rk[r];
+      kout[pos] = k[r];
+      vout[pos] = v[r];
+    }
+  }
+}
+
 struct RadixScratch {
   DevBuf<uint32_t> counts;
+  DevBuf<uint32_t> os;  // onesweep: [passes][tiles][bins] status | [passes][bins] hist | [passes] tile counters
+  void ensure_onesweep(uint64_t n_cap, int passes) {
+    const uint64_t tiles = ceil_div(n_cap > 0 ? n_cap : 1, kRadixTile);
+    os.ensure(static_cast<size_t>(passes) * (tiles + 1) * kRadixBins + 32);
+  }
 };
 
 // Sorts (keys, vals) by bits [0, nbits) stably. `vals` may be null: payload
@@ -194,6 +344,33 @@ void radix_sort_pairs(Ctx* ctx, K* k0, uint32_t* v0, K* k1, uint32_t* v1, uint64
   if (n_cap == 0) {
     *k_out = k0;
     *v_out = v0;
+    return;
+  }
+  if (ctx->onesweep && passes <= kOsMaxPasses) {
+    const unsigned tiles_os = tiles;
+    s.ensure_onesweep(n_cap, passes);
+    uint32_t* status = s.os.p;
+    uint32_t* hist = status + static_cast<size_t>(passes) * tiles_os * kRadixBins;
+    uint32_t* ctr = hist + static_cast<size_t>(passes) * kRadixBins;
+    FSX_CUDA(cudaMemsetAsync(s.os.p, 0,
+                             (static_cast<size_t>(passes) * (tiles_os + 1) * kRadixBins + 32) * sizeof(uint32_t),
+                             stream));
+    FSX_LAUNCH(ctx, k_os_hist<K>, grid_for(ctx, n_cap, kRadixThreads, 2), kRadixThreads, 0, stream, kin, n_cap,
+               d_n, passes, dbits, hist);
+    for (int p = 0; p < passes; ++p) {
+      FSX_LAUNCH(ctx, k_os_scatter<K>, tiles_os, kRadixThreads, 0, stream, kin, vin, kout, vout, n_cap, d_n,
+                 dbits * p, mask, hist + static_cast<size_t>(p) * kRadixBins,
+                 status + static_cast<size_t>(p) * tiles_os * kRadixBins, ctr + p);
+      K* kt = kin;
+      kin = kout;
+      kout = kt;
+      vin = vout;
+      uint32_t* vt = vbuf_in;
+      vbuf_in = vout;
+      vout = vt;
+    }
+    *k_out = kin;
+    *v_out = vbuf_in;
     return;
   }
   for (int p = 0; p < passes; ++p) {

@@ -53,6 +53,7 @@ struct SortedIds {
     // every scratch buffer is sized up front: a lazy cudaMalloc/cudaFree in
     // the middle of a multi-rank iteration can serialize the device
     radix.counts.ensure(static_cast<size_t>(ceil_div(cap, kRadixTile)) * kRadixBins + kRadixBins);
+    radix.ensure_onesweep(cap, 4);
     scan.ensure(cap, 1);
   }
   void reserve64() {
