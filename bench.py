@@ -301,11 +301,11 @@ def main():
 
     W, K = max(args.warmup, 3), args.steps
     cfg5 = args.cfg5 if args.cfg5 >= 0 else int(world > 1)
-    iters = W + 2 * K + min(K, 5) + 2 + (2 * K + 4 if cfg5 else 0)
+    iters = W + 3 * K + 4 + (2 * K + 4 if cfg5 else 0)
     t_gen = time.time()
     batches, blens = batches_for(args, rank, world, iters, with_lens=True)
     ctx = E.Context(local, rank, world)
-    cfg5_first = W + 2 * K + min(K, 5)
+    cfg5_first = W + 3 * K + 2
     if cfg5 and world > 1 and args.mode == "prio":
         bi, bl = balance_batches(args, world, rank, iters, cfg5_first, ctx)
         for i in bi:
@@ -389,9 +389,6 @@ def main():
         for i in range(W):
             step(i)
         barrier()
-        if args.profile_phases and hasattr(eng, "set_profiling"):
-            eng.set_profiling(True)
-            eng.phase_ms()  # reset
         launches0 = ctx.launches()
         if args.mode == "prio":
             eng.exposed_ms()  # reset the accumulator
@@ -408,17 +405,27 @@ def main():
         ms_dev = ev0.elapsed_time(ev1)
         launches = ctx.launches() - launches0
         exp_timed = eng.exposed_ms() / K
-        phases = eng.phase_ms() if args.profile_phases and hasattr(eng, "set_profiling") else {}
-        if hasattr(eng, "set_profiling"):
-            eng.set_profiling(False)
-        # a few untimed steps between the sections
-        for i in range(W + K, W + K + min(K, 5)):
+        # phase timing (CUDA events around every phase, on the stream each
+        # runs on) in a separate section of K steps, so the event overhead is
+        # not inside the timed region above
+        prof_lo = W + K
+        phases = {}
+        if args.profile_phases and hasattr(eng, "set_profiling"):
+            eng.set_profiling(True)
+            eng.phase_ms()  # reset
+        for i in range(prof_lo, prof_lo + K):
             step(i)
         barrier()
+        if args.profile_phases and hasattr(eng, "set_profiling"):
+            phases = eng.phase_ms()
+            eng.set_profiling(False)
         eng.exposed_ms()
-        # end-to-end: host ids -> device each step, stats read back
+        # end-to-end: host ids -> device each step, stats read back (two
+        # untimed steps first: the switch from resident to host ids)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        first_e2e = W + K + min(K, 5)
+        for i in range(W + 2 * K, W + 2 * K + 2):
+            step(i, e2e=True)
+        first_e2e = W + 2 * K + 2
         barrier()
         e0.record(stream)
         n_e2e = 0
@@ -525,11 +532,13 @@ def main():
     exposed_ms = max_over_ranks(exp_timed)
     exposed_sum = sum_over_ranks(exp_timed)
 
-    # roofline of the dominant row-moving phase (rank 0's view)
+    # roofline of the dominant row-moving phase (rank 0's view), over the
+    # profiled section's batches
     rb = args.dim * 4
     timed = batches[W:W + K]
-    occ = sum(b.size for b in timed)
-    uq = sum(np.unique(b).size for b in timed)
+    profiled = batches[prof_lo:prof_lo + K]
+    occ = sum(b.size for b in profiled)
+    uq = sum(np.unique(b).size for b in profiled)
     algo = {
         # reads occ_slot + row pointer + the row, writes the row
         "merge": occ * (2 * rb + 12),

@@ -158,6 +158,7 @@ int fsx_ctx_create(int device, int rank, int world, fsx_ctx** out) {
   c->single_per_sm = env_u("FSX_SINGLE_PER_SM", c->single_per_sm);
   c->flat_per_sm = env_u("FSX_FLAT_PER_SM", c->flat_per_sm);
   c->warp_per_sm = env_u("FSX_WARP_PER_SM", c->warp_per_sm);
+  c->warp_variant = env_u("FSX_WARP_VARIANT", c->warp_variant);
   if (const char* v = std::getenv("FSX_SGD_WARP")) c->sgd_warp = std::atoi(v) != 0;
   // measured (bench, B200): at one rank the look-back CTAs' spinning costs the
   // concurrent update more than the saved launches give the side lane; with

@@ -357,12 +357,16 @@ struct SgdPlanOp {
         dst = l < local_rows ? table + l * row_bytes : nullptr;  // never outside the shard
       }
     }
+    // first gradient row: a pointer (resolved plans), or, for plans built
+    // ahead of the gradients, the occurrence index tagged in bit 0 — the
+    // update kernels then skip the perm load
+    const char* g0 = gptr ? gptr[s] : reinterpret_cast<const char*>((static_cast<uintptr_t>(rs.perm[s]) << 1) | 1u);
     if (c[0]) {
-      singles[ex[0]] = SgdItem{static_cast<uint32_t>(u), kSgdSingleChunk, s, e, dst, gptr ? gptr[s] : nullptr};
+      singles[ex[0]] = SgdItem{static_cast<uint32_t>(u), kSgdSingleChunk, s, e, dst, g0};
       return;
     }
     if (c[1] == 1) {
-      work[ex[1]] = SgdItem{static_cast<uint32_t>(u), kSgdSingleChunk, s, e, dst, gptr ? gptr[s] : nullptr};
+      work[ex[1]] = SgdItem{static_cast<uint32_t>(u), kSgdSingleChunk, s, e, dst, g0};
     } else {
       // chunks of a hot row: plain stores (no dependent loads in this loop)
       for (uint32_t q = 0; q < c[1]; ++q) {
@@ -413,6 +417,13 @@ struct SgdArgs {
                               // (k_grad_ptrs); nullptr: gr.row(perm[k])
   __device__ __forceinline__ const T* grad(uint32_t k) const {
     return gptr ? gptr[k] : gr.row(rs.perm[k]);
+  }
+  // gradient row of an item's first occurrence (SgdItem::g0: pointer,
+  // tagged occurrence index, or nullptr)
+  __device__ __forceinline__ const T* first_grad(const SgdItem& it) const {
+    const uintptr_t g = reinterpret_cast<uintptr_t>(it.g0);
+    if (g & 1u) return gr.row(static_cast<uint32_t>(g >> 1));
+    return g ? reinterpret_cast<const T*>(g) : grad(it.kb);
   }
 };
 
@@ -506,7 +517,7 @@ __global__ void __launch_bounds__(256) k_sgd_single(SgdArgs<T> a, uint32_t vpr_s
     for (int h = 0; h < 2; ++h) {
       ok[h] = ok[h] && it[h].dst != nullptr;
       if (ok[h]) {
-        const T* g0 = it[h].g0 ? reinterpret_cast<const T*>(it[h].g0) : a.grad(it[h].kb);
+        const T* g0 = a.first_grad(it[h]);
         g[h] = *reinterpret_cast<const V*>(g0 + col[h]);
         if (!a.seg_out) old[h] = *reinterpret_cast<const V*>(reinterpret_cast<const T*>(it[h].dst) + col[h]);
       }
@@ -550,8 +561,7 @@ __global__ void __launch_bounds__(256, 3) k_sgd_flat(SgdArgs<T> a, uint32_t vpr_
     const T* gp[kFlatBatch];
 #pragma unroll
     for (int t = 0; t < kFlatBatch; ++t)
-      gp[t] = item.kb + t < item.ke ? (t == 0 && item.g0 ? reinterpret_cast<const T*>(item.g0) : a.grad(item.kb + t))
-                                    : nullptr;
+      gp[t] = item.kb + t < item.ke ? (t == 0 ? a.first_grad(item) : a.grad(item.kb + t)) : nullptr;
     for (uint32_t k0 = item.kb; k0 < item.ke; k0 += kFlatBatch) {
       V g[kFlatBatch];
 #pragma unroll
@@ -587,8 +597,8 @@ __global__ void __launch_bounds__(256, 3) k_sgd_flat(SgdArgs<T> a, uint32_t vpr_
 // partials; the warp that completes the row's last chunk (arrival counter
 // `done[u]`, reset by that warp) adds them in chunk order — the association
 // k_sgd_combine uses — and applies the row: no separate combine pass.
-template <class T, int VE, int VPL, int U>
-__global__ void __launch_bounds__(256) k_sgd_warp(SgdArgs<T> a, uint32_t* __restrict__ done) {
+template <class T, int VE, int VPL, int U, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_sgd_warp(SgdArgs<T> a, uint32_t* __restrict__ done) {
   using V = VecOf<T, VE>;
   constexpr unsigned kFull = 0xffffffffu;
   const uint64_t nwork = *a.d_work_n;

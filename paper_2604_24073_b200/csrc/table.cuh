@@ -107,6 +107,12 @@ void sgd_apply(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_cap, uin
     const unsigned gw = grid_for(ctx, work_cap * 32, 256, ctx->warp_per_sm);
     if (vpl == 1)
       FSX_LAUNCH(ctx, (k_sgd_warp<T, VE16, 1, 4>), gw, 256, 0, stream, a, s.done.p);
+    else if (vpl == 2 && ctx->warp_variant == 1)
+      FSX_LAUNCH(ctx, (k_sgd_warp<T, VE16, 2, 2, 3>), gw, 256, 0, stream, a, s.done.p);
+    else if (vpl == 2 && ctx->warp_variant == 2)
+      FSX_LAUNCH(ctx, (k_sgd_warp<T, VE16, 2, 4, 3>), gw, 256, 0, stream, a, s.done.p);
+    else if (vpl == 2 && ctx->warp_variant == 3)
+      FSX_LAUNCH(ctx, (k_sgd_warp<T, VE16, 2, 2, 4>), gw, 256, 0, stream, a, s.done.p);
     else if (vpl == 2)
       FSX_LAUNCH(ctx, (k_sgd_warp<T, VE16, 2, 4>), gw, 256, 0, stream, a, s.done.p);
     else

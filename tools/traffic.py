@@ -10,7 +10,7 @@ import csv
 import json
 import sys
 
-UPDATE = ("k_grad_ptrs", "SgdPlanOp", "k_sgd_single", "k_sgd_flat", "k_sgd_combine")
+UPDATE = ("k_grad_ptrs", "k_sgd_single", "k_sgd_flat", "k_sgd_warp", "k_sgd_combine")  # the plan scan runs on L (one rank)
 
 
 def load(path):
