@@ -413,7 +413,12 @@ struct Engine {
   // traffic issued earlier on the same peer)
   static constexpr int kLanes = 4;  // L, H, ux, caller
   cudaStream_t cstream[kLanes][kMaxRanks] = {};
-  int lane_of(cudaStream_t s) const { return s == lo ? 0 : s == hi ? 1 : s == ux ? 2 : 3; }
+  // copy-stream set of a lane: the prioritized engine's caller stream runs no
+  // all-to-all of its own (raw fsx_a2a_ce / all-gather calls borrow H's set),
+  // the blocking engine uses only the caller's — fewer streams keep every
+  // used stream on its own hardware queue at 8 ranks (CUDA_DEVICE_MAX_CONNECTIONS)
+  int lane_map[kLanes] = {0, 1, 2, 3};
+  int lane_of(cudaStream_t s) const { return lane_map[s == lo ? 0 : s == hi ? 1 : s == ux ? 2 : 3]; }
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_next = 0;
   // exposed-wait timing on the compute stream
@@ -1594,9 +1599,12 @@ int fsx_engine_create(fsx_ctx* ctx, fsx_table* table, const fsx_engine_config* c
   FSX_CUDA(cudaStreamCreateWithPriority(&e->ux, cudaStreamNonBlocking, least));
   // one copy stream per peer: outgoing copies of an all-to-all run on
   // several copy engines at once instead of queueing on one
-  for (int l = 0; l < Engine::kLanes; ++l)
+  for (int l = 0; l < Engine::kLanes; ++l) e->lane_map[l] = prio ? (l == 3 ? 1 : l) : 3;
+  for (int l = 0; l < Engine::kLanes; ++l) {
+    if (prio ? l == 3 : l != 3) continue;
     for (int d = 0; d < e->p; ++d)
       if (d != e->me) FSX_CUDA(cudaStreamCreateWithPriority(&e->cstream[l][d], cudaStreamNonBlocking, greatest));
+  }
   if (e->p > 1) {
     e->side = std::make_unique<SideLane>();
     e->side->start(ctx->device);
