@@ -264,6 +264,25 @@ int fsx_a2a_ce(fsx_engine* e, const void* d_send, const uint64_t* h_send_offsets
                const uint64_t* h_send_bytes, void* d_recv, uint64_t slot_bytes,
                uint64_t* h_recv_bytes, void* stream);
 
+/* ---- jagged reshuffle (jagged.hpp:89-248) ------------------- */
+/* Device layout: values = elem_bytes-sized elements back to back, offsets =
+ * u64 [n+1] exclusive prefix of the lengths. */
+/* offsets of a length array (the JaggedTensor constructor's prefix, jagged.hpp:23-34) */
+int fsx_jagged_offsets(fsx_ctx* ctx, const uint64_t* d_lengths, uint64_t n, uint64_t* d_offsets,
+                       uint64_t* h_total, void* stream);
+/* indexed_permute (jagged.hpp:89-111): output segment j = input segment
+ * perm[j] (repetition allowed). Writes out lengths/offsets, *h_out_total; with
+ * d_out_values == NULL only sizes. FSX_ERR_OUT_OF_RANGE ("indexed_permute:
+ * segment index K out of range (have N)") before anything moves. */
+int fsx_jagged_permute(fsx_ctx* ctx, const void* d_values, uint32_t elem_bytes, const uint64_t* d_offsets,
+                       uint64_t n_segs, const uint64_t* d_perm, uint64_t n_perm, void* d_out_values,
+                       uint64_t out_capacity, uint64_t* d_out_lengths, uint64_t* d_out_offsets,
+                       uint64_t* h_out_total, void* stream);
+/* keyed_transpose's permutation (jagged.hpp:227-248): feature_major != 0 maps
+ * (f, s) at f*S+s to s*F+f, else the inverse */
+int fsx_keyed_transpose_perm(fsx_ctx* ctx, uint64_t num_keys, uint64_t num_samples, int feature_major,
+                             uint64_t* d_perm, void* stream);
+
 /* ---- copy-engine all-gather (comm.cpp:185-306 analogue) --------------------- */
 /* Collective: every rank contributes send_bytes bytes (<= max_bytes, the bound
  * every rank passes identically); on return d_recv + d * slot_bytes holds rank

@@ -83,6 +83,9 @@ _SIGS = {
     "fsx_engine_slot_bytes": ([vp], u64),
     "fsx_a2a_ce": ([vp, vp, vp, vp, vp, u64, vp, vp], i32),
     "fsx_allgather_ce": ([vp, vp, u64, u64, vp, u64, vp, i32, vp], i32),
+    "fsx_jagged_offsets": ([vp, vp, u64, vp, P(u64), vp], i32),
+    "fsx_jagged_permute": ([vp, vp, u32, vp, u64, vp, u64, vp, u64, vp, vp, P(u64), vp], i32),
+    "fsx_keyed_transpose_perm": ([vp, u64, u64, i32, vp, vp], i32),
 }
 
 EXPORTED = sorted(_SIGS)

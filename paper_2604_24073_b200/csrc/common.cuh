@@ -68,6 +68,7 @@ enum DevErrKind : int {
   kErrCapacity = 6,     // a = needed, b = capacity      -> CollectiveError
   kErrMissingCoRow = 7, // a = id                        -> ProtocolError
   kErrMaskOverlap = 8,  //                               -> ProtocolError
+  kErrSegIndex = 9,     // a = index, b = segments       -> out_of_range
 };
 
 struct DevErr {

@@ -39,6 +39,9 @@ std::string describe(const DevErr& e, int* code) {
     case kErrMaskOverlap:
       *code = FSX_ERR_PROTOCOL;
       return "embedding: a row appears in both collision and exclusive masks";
+    case kErrSegIndex:  // jagged.hpp:93-96
+      *code = FSX_ERR_OUT_OF_RANGE;
+      return "indexed_permute: segment index " + u(e.a) + " out of range (have " + u(e.b) + ")";
     default:
       *code = FSX_ERR_CUDA;
       return "fsx: unknown device error " + std::to_string(e.kind);
