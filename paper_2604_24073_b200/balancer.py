@@ -146,6 +146,28 @@ class TorchComm:
         return res
 
 
+def _ce_all_to_all_jagged(comm, parts: list) -> list:
+    """Jagged all-to-all on the copy engines: every part's lengths (host, a
+    small size round) and its 8-byte values device to device (fsx_a2a_ce)."""
+    import ctypes as C
+    import torch
+    from . import jagged as J
+    w, dev = comm.world_size(), comm.dev
+    lens = comm.all_to_all_u64([p.lengths() for p in parts])
+    nbytes = [8 * p.total_values() for p in parts]
+    mat = comm.all_gather_u64(np.asarray(nbytes, np.uint64))
+    slot = max([int(x) for row in mat for x in row] + [8])
+    vals = [p.values().view(torch.int64) for p in parts]
+    send = torch.cat(vals) if any(v.numel() for v in vals) else torch.zeros(1, dtype=torch.int64, device=dev)
+    offs = (C.c_uint64 * w)(*np.concatenate([[0], np.cumsum(nbytes)[:-1]]).astype(int))
+    recv = torch.empty(w * slot // 8, dtype=torch.int64, device=dev)
+    got = (C.c_uint64 * w)()
+    _lib.call("fsx_a2a_ce", comm.e.h, C.c_void_p(send.data_ptr()), offs, (C.c_uint64 * w)(*nbytes),
+              C.c_void_p(recv.data_ptr()), slot, got, C.c_void_p(comm._stream()))
+    return [J.JaggedTensor(recv[d * slot // 8: d * slot // 8 + got[d] // 8].clone(), lens[d], device=dev)
+            for d in range(w)]
+
+
 class LocalComm:
     """world of one (comm.cpp:194-198: every exchange is a local hand-off)."""
 
@@ -221,6 +243,9 @@ class CeComm:
                   slot, got, C.c_void_p(self._stream()))
         host = recv.cpu().numpy().view(np.uint64)
         return [host[d * slot // 8: d * slot // 8 + got[d] // 8].copy() for d in range(w)]
+
+
+CeComm.all_to_all_jagged = _ce_all_to_all_jagged
 
 
 # ---- balancer ---------------------------------------------------------------------------
@@ -436,15 +461,64 @@ class Balancer:
             raise ProtocolError("balancer: stage 3 before stage 2")
         lists = p.plan.exchange_lists(p.metas)
         mine = lists[self.comm.rank()]
-        msgs = [encode_jagged([p.raw.samples[int(l)] for l in mine[dst]])
-                for dst in range(self.comm.world_size())]
-        p.shuffled = self.comm.all_to_all_u64(msgs)
+        if hasattr(self.comm, "all_to_all_jagged"):
+            p.shuffled = self._stage3_jagged(p, mine)
+        else:
+            msgs = [encode_jagged([p.raw.samples[int(l)] for l in mine[dst]])
+                    for dst in range(self.comm.world_size())]
+            p.shuffled = self.comm.all_to_all_u64(msgs)
         p.stage = Stage.Shuffled
+
+    def _stage3_jagged(self, p: _Pending, mine: list) -> list:
+        """Stage 3 as jagged device ops instead of per-sample
+        record serialization: the UIH and candidate segments go to the device
+        once, indexed_permute groups them by destination in exchange order,
+        ranged_dispatch cuts one part per destination, and the parts travel by
+        copy-engine all-to-all; candidate counts and labels ride a small u64
+        message."""
+        from . import jagged as J
+        dev = self.comm.dev
+        samples = p.raw.samples
+        w = self.comm.world_size()
+        uih = J.IdJagged.from_segments([s.uih for s in samples], device=dev)
+        nc = np.asarray([len(s.candidates) for s in samples], np.int64)
+        cstart = np.concatenate([[0], np.cumsum(nc)]).astype(np.int64)
+        cand = J.IdJagged.from_segments([c for s in samples for c in s.candidates], device=dev)
+        order = [int(k) for dst in range(w) for k in mine[dst]]
+        counts = [len(mine[dst]) for dst in range(w)]
+        ccounts = [int(sum(nc[int(k)] for k in mine[dst])) for dst in range(w)]
+        cperm = [int(cstart[k]) + j for k in order for j in range(int(nc[k]))]
+        starts = np.concatenate([[0], np.cumsum(counts)]).astype(int)
+        cstarts = np.concatenate([[0], np.cumsum(ccounts)]).astype(int)
+        uih_parts = J.ranged_dispatch(J.indexed_permute(uih, order), [(starts[d], counts[d]) for d in range(w)])
+        cand_parts = J.ranged_dispatch(J.indexed_permute(cand, cperm), [(cstarts[d], ccounts[d]) for d in range(w)])
+        meta = [np.concatenate([nc[[int(k) for k in mine[dst]]].astype(np.uint64),
+                                np.asarray([_f64_bits(samples[int(k)].label) for k in mine[dst]], np.uint64)])
+                for dst in range(w)]
+        r_uih = self.comm.all_to_all_jagged(uih_parts)
+        r_cand = self.comm.all_to_all_jagged(cand_parts)
+        r_meta = self.comm.all_to_all_u64(meta)
+        out = []
+        for src in range(w):
+            segs = r_uih[src].to_segments()
+            n = len(segs)
+            if r_meta[src].size != 2 * n:
+                raise ProtocolError("balancer: stage-3 payload shorter than the plan")
+            ncs = r_meta[src][:n].astype(np.int64)
+            csegs = r_cand[src].to_segments()
+            at, samp = 0, []
+            for k in range(n):
+                cs = [np.asarray(c, np.uint64) for c in csegs[at:at + int(ncs[k])]]
+                at += int(ncs[k])
+                samp.append(Sample(np.asarray(segs[k], np.uint64), cs, _bits_f64(r_meta[src][n + k])))
+            out.append(samp)
+        return out
 
     # -- consumption (balancer.cpp:224-277)
     def _assemble(self, p: _Pending) -> Batch:
         me = self.comm.rank()
-        per_src = [decode_jagged(m) for m in p.shuffled]
+        per_src = ([decode_jagged(m) for m in p.shuffled] if p.shuffled and isinstance(p.shuffled[0], np.ndarray)
+                   else p.shuffled)
         cursor = [0] * len(per_src)
         out = Batch(rank=me)
         for g in p.plan.receive_order[me]:

@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import threading
 
 import numpy as np
 import torch
@@ -25,15 +26,20 @@ def _stream(device) -> int:
 
 
 def _ctx(device: torch.device):
+    """One libfsx context per device for the jagged ops, created once under a
+    lock (a context that lost a creation race would be destroyed while a
+    caller still holds its handle)."""
     from .embedding import Context
     idx = device.index if device.index is not None else torch.cuda.current_device()
-    c = _CTX.get(idx)
-    if c is None:
-        c = _CTX[idx] = Context(idx, 0, 1)
+    with _CTX_LOCK:
+        c = _CTX.get(idx)
+        if c is None:
+            c = _CTX[idx] = Context(idx, 0, 1)
     return c
 
 
 _CTX: dict = {}
+_CTX_LOCK = threading.Lock()
 
 
 class JaggedTensor:
