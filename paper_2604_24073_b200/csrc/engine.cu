@@ -105,15 +105,6 @@ __global__ void k_sum_pairs(const uint64_t* t, int p, uint64_t* out) {
   }
 }
 
-__global__ void k_count_flags(const uint8_t* f, const uint64_t* d_n, unsigned long long* out) {
-  const uint64_t n = *d_n;
-  unsigned long long c = 0;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    c += f[i] ? 1 : 0;
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if ((threadIdx.x & 31u) == 0 && c) atomicAdd(out, c);
-}
 
 // One rank: the owner partition of route_to_shard_major (embedding.cpp:194-212)
 // is the identity — every id goes to self in its original order. One pass
@@ -140,24 +131,80 @@ __global__ void k_route_self(const uint64_t* __restrict__ ids, uint64_t n, uint6
   }
 }
 
-// One rank: the split / occurrence-rank totals the statistics read
-// (k_blocking_bytes), without the per-occurrence plans nothing consumes —
-// [0] exclusive, [1] collision occurrences, for requester and owner alike.
-__global__ void k_co_occ_count(const uint32_t* __restrict__ inverse, const uint8_t* __restrict__ co,
-                               const uint64_t* d_n, unsigned long long* split_tot, unsigned long long* occ_tot) {
-  const uint64_t n = *d_n;
-  unsigned long long c = 0, e = 0;
-  for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < n;
-       j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    if (co && co[inverse[j]]) ++c; else ++e;
+// compute_collision (embedding.cpp:82-93) on the owner's sorted unique rows:
+// co[u] for rows of a also in b (b's flag and a's partner row set alongside),
+// plus the counts the statistics need — collision rows (misc[0]) and the
+// occurrences of a on them (misc[1]) — warp-aggregated.
+__global__ void k_collide_count(const uint64_t* __restrict__ a, const uint64_t* d_na,
+                                const uint64_t* __restrict__ b, const uint64_t* d_nb,
+                                const uint32_t* __restrict__ seg_a, uint8_t* __restrict__ flag_a,
+                                uint8_t* __restrict__ flag_b, uint32_t* __restrict__ partner_a,
+                                unsigned long long* misc) {
+  const uint64_t na = *d_na, nb = *d_nb;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  const uint64_t n_round = (na + 31) & ~uint64_t{31};
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n_round; i += stride) {
+    bool hit = false;
+    unsigned long long occ = 0;
+    if (i < na) {
+      const uint64_t x = a[i];
+      uint64_t lo = 0, hi = nb;
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (b[mid] < x) lo = mid + 1; else hi = mid;
+      }
+      hit = lo < nb && b[lo] == x;
+      flag_a[i] = hit ? 1 : 0;
+      if (hit) {
+        flag_b[lo] = 1;
+        partner_a[i] = static_cast<uint32_t>(lo);
+        occ = seg_a[i + 1] - seg_a[i];
+      }
+    }
+    const unsigned ballot = __ballot_sync(0xffffffffu, hit);
+    for (int o = 16; o > 0; o >>= 1) occ += __shfl_xor_sync(0xffffffffu, occ, o);
+    if ((threadIdx.x & 31u) == 0 && ballot) {
+      atomicAdd(misc, static_cast<unsigned long long>(__popc(ballot)));
+      atomicAdd(misc + 1, occ);
+    }
   }
-  for (int o = 16; o > 0; o >>= 1) {
-    c += __shfl_xor_sync(0xffffffffu, c, o);
-    e += __shfl_xor_sync(0xffffffffu, e, o);
+}
+
+// one rank: the split / occurrence-rank totals of the statistics from the
+// collision counts ([0] exclusive, [1] collision occurrences)
+__global__ void k_self_split_totals(const uint64_t* d_n, const uint64_t* misc, int with_co, uint64_t* split_tot,
+                                    uint64_t* occ_tot) {
+  if (threadIdx.x == 0) {
+    const uint64_t n = *d_n, c = with_co ? misc[1] : 0;
+    split_tot[0] = occ_tot[0] = n - c;
+    split_tot[1] = occ_tot[1] = c;
   }
-  if ((threadIdx.x & 31u) == 0) {
-    if (e) { atomicAdd(split_tot, e); atomicAdd(occ_tot, e); }
-    if (c) { atomicAdd(split_tot + 1, c); atomicAdd(occ_tot + 1, c); }
+}
+
+// one rank: receive = the own IDS message as the owner batch — occurrence j
+// is id j from source 0 — and its 32-bit sort keys (local row = id), in one
+// pass (k_recv_prefix + k_flatten_recv + k_make_keys at p > 1)
+__global__ void k_self_receive(const char* __restrict__ slot, uint64_t cap, uint64_t* __restrict__ cnt,
+                               uint64_t* __restrict__ d_n, uint64_t* __restrict__ ids,
+                               uint8_t* __restrict__ occ_src, uint32_t* __restrict__ occ_idx,
+                               uint32_t* __restrict__ keys, DevErr* err) {
+  const uint64_t n_msg = reinterpret_cast<const uint64_t*>(slot)[0];
+  const uint64_t n = n_msg <= cap ? n_msg : cap;
+  const uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i0 == 0) {
+    if (n_msg > cap) report(err, kErrCapacity, n_msg, cap);
+    cnt[0] = n;
+    cnt[2] = n;
+    cnt[2 + kMaxRanks] = 0;
+    *d_n = n;
+  }
+  const uint64_t* msg = reinterpret_cast<const uint64_t*>(slot + kHdr);
+  for (uint64_t j = i0; j < n; j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t id = msg[j];
+    ids[j] = id;
+    occ_src[j] = 0;
+    occ_idx[j] = static_cast<uint32_t>(j);
+    keys[j] = static_cast<uint32_t>(id);
   }
 }
 
@@ -787,14 +834,23 @@ struct Engine {
     o.reserve(static_cast<uint64_t>(p) * cap);
     o.has_co = false;
     CSlots slots = recv_slots(CH_IDS, ids_par);
-    FSX_LAUNCH(ctx, k_recv_prefix, 1, 32, 0, s, slots, p, cap, o.cnt.p, ctx->d_err);
-    FSX_CUDA(cudaMemcpyAsync(o.srt.d_n(), o.cnt.p, 8, cudaMemcpyDeviceToDevice, s));
-    FSX_LAUNCH(ctx, k_flatten_recv, grid_for(ctx, static_cast<uint64_t>(p) * cap, 256, 8), 256, 0, s,
-               slots, p, cap, o.cnt.p, t->g, o.ids.p, o.occ_src.p, o.occ_idx.p, ctx->d_err);
-    o.srt.run(ctx, o.ids.p, o.m_cap, t->g, true, false, t->key_bits(), s);
-    FSX_CUDA(cudaMemsetAsync(o.bits.p, 0, o.m_cap * 4, s));
-    FSX_LAUNCH(ctx, k_src_bits, grid_for(ctx, o.m_cap, 256, 8), 256, 0, s, o.srt.inverse.p,
-               o.occ_src.p, o.srt.d_n(), o.bits.p);
+    if (p == 1 && t->key_bits() <= 32) {
+      o.srt.reserve(o.m_cap);
+      FSX_LAUNCH(ctx, k_self_receive, grid_for(ctx, cap, 256, 8), 256, 0, s, slots.p[0], cap, o.cnt.p, o.srt.d_n(),
+                 o.ids.p, o.occ_src.p, o.occ_idx.p, o.srt.k32a.p, ctx->d_err);
+      o.srt.run(ctx, o.ids.p, o.m_cap, t->g, true, false, t->key_bits(), s, /*keys_ready=*/true);
+    } else {
+      FSX_LAUNCH(ctx, k_recv_prefix, 1, 32, 0, s, slots, p, cap, o.cnt.p, ctx->d_err);
+      FSX_CUDA(cudaMemcpyAsync(o.srt.d_n(), o.cnt.p, 8, cudaMemcpyDeviceToDevice, s));
+      FSX_LAUNCH(ctx, k_flatten_recv, grid_for(ctx, static_cast<uint64_t>(p) * cap, 256, 8), 256, 0, s,
+                 slots, p, cap, o.cnt.p, t->g, o.ids.p, o.occ_src.p, o.occ_idx.p, ctx->d_err);
+      o.srt.run(ctx, o.ids.p, o.m_cap, t->g, true, false, t->key_bits(), s);
+    }
+    if (p > 1 || presum()) {  // requester bits per row: one source at p = 1
+      FSX_CUDA(cudaMemsetAsync(o.bits.p, 0, o.m_cap * 4, s));
+      FSX_LAUNCH(ctx, k_src_bits, grid_for(ctx, o.m_cap, 256, 8), 256, 0, s, o.srt.inverse.p,
+                 o.occ_src.p, o.srt.d_n(), o.bits.p);
+    }
     if (p > 1 && exact) o.h_recv = fetch(o.cnt.p + 2, p, s);
     else o.h_recv.clear();
   }
@@ -907,10 +963,9 @@ struct Engine {
   void collide(OwnBatch& oc, OwnBatch& on, cudaStream_t s) {
     Span sp(this, FSX_PHASE_COLLIDE, s);
     FSX_CUDA(cudaMemsetAsync(on.co.p, 0, on.m_cap, s));
-    FSX_CUDA(cudaMemsetAsync(oc.misc.p, 0, 8, s));
-    FSX_LAUNCH(ctx, k_intersect_flags, grid_for(ctx, oc.m_cap, 256, 8), 256, 0, s, oc.srt.uniq_g.p,
-               oc.srt.d_u(), on.srt.uniq_g.p, on.srt.d_u(), oc.co.p, on.co.p, oc.partner.p);
-    FSX_LAUNCH(ctx, k_count_flags, grid_for(ctx, oc.m_cap, 256, 4), 256, 0, s, oc.co.p, oc.srt.d_u(),
+    FSX_CUDA(cudaMemsetAsync(oc.misc.p, 0, 16, s));
+    FSX_LAUNCH(ctx, k_collide_count, grid_for(ctx, oc.m_cap, 256, 8), 256, 0, s, oc.srt.uniq_g.p,
+               oc.srt.d_u(), on.srt.uniq_g.p, on.srt.d_u(), oc.srt.seg_start.p, oc.co.p, on.co.p, oc.partner.p,
                reinterpret_cast<unsigned long long*>(oc.misc.p));
     oc.has_co = true;
     on.has_co = false;
@@ -985,11 +1040,9 @@ struct Engine {
     if (p == 1 && !presum()) {
       // one rank: the update needs no masks or split plan (it runs whole on
       // the caller's stream); only the statistics need the totals
-      FSX_CUDA(cudaMemsetAsync(rc.split_tot.p, 0, 32 * 8, s));
-      FSX_CUDA(cudaMemsetAsync(oc.occ_tot(), 0, 32 * 8, s));
-      FSX_LAUNCH(ctx, k_co_occ_count, grid_for(ctx, oc.m_cap, 256, 4), 256, 0, s, oc.srt.inverse.p,
-                 with_co ? oc.co.p : nullptr, oc.srt.d_n(), reinterpret_cast<unsigned long long*>(rc.split_tot.p),
-                 reinterpret_cast<unsigned long long*>(oc.occ_tot()));
+      // (collision occurrences counted by k_collide_count)
+      FSX_LAUNCH(ctx, k_self_split_totals, 1, 32, 0, s, oc.srt.d_n(), oc.misc.p, with_co ? 1 : 0, rc.split_tot.p,
+                 oc.occ_tot());
       rc.has_flags = false;
       return;
     }

@@ -65,14 +65,16 @@ struct SortedIds {
 
   // ids: n_cap-capacity input, live count at *d_n() (caller fills it, or
   // pass host n via set_n). nbits: significant key bits.
+  // keys_ready: k32a already holds the 32-bit keys (the caller's fused pass)
   void run(Ctx* ctx, const uint64_t* ids, uint64_t n_cap, const ShardGeom& g, bool local,
-           bool validate, int nbits, cudaStream_t s) {
+           bool validate, int nbits, cudaStream_t s, bool keys_ready = false) {
     reserve(n_cap);
     const unsigned grid = grid_for(ctx, n_cap, 256, 8);
     uint64_t* totals = d_counts.p + 1;  // scan total -> U
     if (nbits <= 32) {
-      FSX_LAUNCH(ctx, k_make_keys<uint32_t>, grid, 256, 0, s, ids, n_cap, d_n(), g, local ? 1 : 0,
-                 validate ? 1 : 0, k32a.p, ctx->d_err);
+      if (!keys_ready)
+        FSX_LAUNCH(ctx, k_make_keys<uint32_t>, grid, 256, 0, s, ids, n_cap, d_n(), g, local ? 1 : 0,
+                   validate ? 1 : 0, k32a.p, ctx->d_err);
       uint32_t* ko;
       radix_sort_pairs<uint32_t>(ctx, k32a.p, va.p, k32b.p, vb.p, n_cap, d_n(), nbits, radix, s,
                                  &ko, &perm);
