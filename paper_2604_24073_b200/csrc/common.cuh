@@ -101,10 +101,10 @@ struct Ctx {
   // side lanes' latency-bound kernels (dedup / collision of the next
   // iteration), or those wait for a whole merge / update to drain.
   // Overridable for tuning: FSX_COPY_PER_SM, FSX_SINGLE_PER_SM, FSX_FLAT_PER_SM.
-  unsigned copy_per_sm = 4, single_per_sm = 8, flat_per_sm = 16, warp_per_sm = 3;
-  bool sgd_warp = true;
+  unsigned copy_per_sm = 3, single_per_sm = 8, flat_per_sm = 16, warp_per_sm = 3;
+  bool sgd_warp = true;  // FSX_SGD_WARP=0: the thread-per-vector k_sgd_flat + k_sgd_combine
   unsigned warp_variant = 0;  // FSX_WARP_VARIANT (tuning): k_sgd_warp unroll / min CTAs per SM
-  bool onesweep = true;  // decoupled look-back radix passes (default: world > 1; FSX_ONESWEEP)  // FSX_SGD_WARP=0: the thread-per-vector k_sgd_flat + k_sgd_combine
+  bool onesweep = true;  // decoupled look-back radix passes (FSX_ONESWEEP=0: 3 launches per pass)
 
   void check_error(cudaStream_t s);  // D2H the word, sync `s`, throw if set
 };

@@ -163,10 +163,9 @@ int fsx_ctx_create(int device, int rank, int world, fsx_ctx** out) {
   c->warp_per_sm = env_u("FSX_WARP_PER_SM", c->warp_per_sm);
   c->warp_variant = env_u("FSX_WARP_VARIANT", c->warp_variant);
   if (const char* v = std::getenv("FSX_SGD_WARP")) c->sgd_warp = std::atoi(v) != 0;
-  // measured (bench, B200): at one rank the look-back CTAs' spinning costs the
-  // concurrent update more than the saved launches give the side lane; with
-  // peers the side lane's sort is on the critical path and onesweep wins
-  c->onesweep = world > 1;
+  // onesweep radix passes: on (bench A/B on B200, after the one-rank side
+  // lane was slimmed: 0.274 -> 0.259 ms at N = 1; on at N = 4 as well)
+  c->onesweep = true;
   if (const char* v = std::getenv("FSX_ONESWEEP")) c->onesweep = std::atoi(v) != 0;
   FSX_CUDA(cudaMalloc(&c->d_err, sizeof(DevErr)));
   FSX_CUDA(cudaMemset(c->d_err, 0, sizeof(DevErr)));
