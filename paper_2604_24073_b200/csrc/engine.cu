@@ -1131,13 +1131,58 @@ struct Engine {
 
   // owner, PRESUM: collision rows from the sources' pre-summed rows; with
   // `on` the E_co messages of the next iteration are packed in the same pass
+  // E_co written by the collision update straight into the requesters'
+  // receive windows (their slot `me`, over NVLink) instead of local staging +
+  // a copy-engine all-to-all: the transfer rides the update's own stores and
+  // leaves the chain; signal_direct then only raises the flags.
+  bool eco_direct = true;  // FSX_ECO_DIRECT=0: stage + copy-engine all-to-all
+  Slots remote_slots(int ch, int par) const {
+    Slots r{};
+    for (int d = 0; d < p; ++d)
+      r.p[d] = d == me ? recv_slot(ch, par, me)
+                       : peer[d].base + ch_off[ch] + (static_cast<size_t>(par) * p + me) * ch_slot[ch];
+    return r;
+  }
+  // flags of a channel whose payload the sender's kernels already stored into
+  // the peers' windows (ordered by `s`), then wait for every peer's
+  void signal_direct(int ch, cudaStream_t s) {
+    Span sp(this, FSX_PHASE_A2A, s);
+    const uint32_t v = seq[ch];
+    for (int k = 1; k < p; ++k) {
+      const int d = (me + k) % p;
+      const PeerView& pv = peer[d];
+      if (pv.local) {
+        cudaEvent_t ev;  // one per receiver: the Hub hands it over and the receiver destroys it
+        FSX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        FSX_CUDA(cudaEventRecord(ev, s));
+        Hub::get().post(pv.local, ch, v, me, ev);
+      } else {
+        FSX_CU(drv::write_value32()(reinterpret_cast<CUstream>(s),
+                                    reinterpret_cast<CUdeviceptr>(pv.flags + ch * kMaxRanks + me), v,
+                                    CU_STREAM_WRITE_VALUE_DEFAULT));
+      }
+    }
+    for (int k = 1; k < p; ++k) {
+      const int src = (me + p - k) % p;
+      if (peer[src].local) {
+        cudaEvent_t ev = Hub::get().take(this, ch, v, src);
+        FSX_CUDA(cudaStreamWaitEvent(s, ev, 0));
+        FSX_CUDA(cudaEventDestroy(ev));
+      } else {
+        FSX_CU(drv::wait_value32()(reinterpret_cast<CUstream>(s),
+                                   reinterpret_cast<CUdeviceptr>(flags + ch * kMaxRanks + src), v,
+                                   CU_STREAM_WAIT_VALUE_GEQ));
+      }
+    }
+  }
+
   void co_apply(OwnBatch& oc, int cog_par, cudaStream_t s, OwnBatch* on = nullptr, int cor_par = -1) {
     CSlots cog = recv_slots(CH_COG, cog_par);
     EcoOut eco{};
     eco.self = me;
     if (on) {
       eco = EcoOut{oc.partner.p, on->bits.p, on->rank_us.p, on->pack_tot(), on->srt.uniq_g.p,
-                   send_slots(CH_COR, cor_par), me};
+                   eco_direct ? remote_slots(CH_COR, cor_par) : send_slots(CH_COR, cor_par), me};
       FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, eco.send, p, on->pack_tot() + 1, 2, cap, ctx->d_err);
     }
     const unsigned grid = grid_for(ctx, oc.m_cap, 4, 16);
@@ -1493,9 +1538,13 @@ struct Engine {
       if (ev_pack) wait(hi, ev_pack);
       if (fused_cor >= 0) {
         Span sp(this, FSX_PHASE_ECO, hi);
-        std::vector<uint64_t> bytes(p);
-        for (int d = 0; d < p; ++d) bytes[d] = idrows_rows_off(on.h_pack[2 * d + 1]) + rb * on.h_pack[2 * d + 1];
-        a2a(CH_COR, fused_cor, bytes, hi);
+        if (eco_direct) {
+          signal_direct(CH_COR, hi);
+        } else {
+          std::vector<uint64_t> bytes(p);
+          for (int d = 0; d < p; ++d) bytes[d] = idrows_rows_off(on.h_pack[2 * d + 1]) + rb * on.h_pack[2 * d + 1];
+          a2a(CH_COR, fused_cor, bytes, hi);
+        }
         rn.cor_par = fused_cor;
       } else {
         rn.cor_par = send_eco(on, hi);
@@ -1612,6 +1661,7 @@ int fsx_engine_create(fsx_ctx* ctx, fsx_table* table, const fsx_engine_config* c
   e->me = ctx->rank;
   e->cap = std::max<uint64_t>(cfg->max_occurrences, 1);
   e->rb = table->row_bytes();
+  if (const char* v = std::getenv("FSX_ECO_DIRECT")) e->eco_direct = std::atoi(v) != 0;
   const bool prio = cfg->mode == FSX_MODE_PRIO;
   const uint64_t cap = e->cap, rb = e->rb;
   auto round256 = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };

@@ -625,6 +625,9 @@ __global__ void __launch_bounds__(128) k_co_apply(T* __restrict__ table, ShardGe
                                 static_cast<uint64_t>(pos[s]) * rb + col * sizeof(T)) = r;
     }
   }
+  // E_co may have gone straight to peer windows: visible system-wide before
+  // the stream's flag write that follows this kernel
+  if (eco.partner) __threadfence_system();
 }
 
 }  // namespace fsx
