@@ -508,6 +508,9 @@ def main():
             "exposed_reduction_pct": round(100.0 * (1 - exp_p / exp_b), 2) if exp_b > 0 else None,
             "step_ms": {b_key: round(step_b, 4), "prio_ce": round(step_p, 4)},
             "victim_alone_ms": round(max_over_ranks(victim_alone), 4),
+            # straggler share of the exposed wait: the slowest rank's victim
+            # holds every peer's collision chain (both engines pay it)
+            "victim_alone_ms_min_over_ranks": round(-max_over_ranks(-victim_alone), 4),
             "comm_sms": {b_key: "NCCL kernels" if base_tr == "nccl" else 0, "prio_ce": 0},
         }
 
