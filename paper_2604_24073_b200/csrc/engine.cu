@@ -208,6 +208,47 @@ __global__ void k_self_receive(const char* __restrict__ slot, uint64_t cap, uint
   }
 }
 
+// receive (embedding.cpp:214-229) at p > 1 in one pass: each thread finds its
+// source's offset from the p headers itself (k_recv_prefix), flattens the id
+// (k_flatten_recv) and writes its 32-bit sort key (k_make_keys, local row)
+__global__ void k_receive_keys(CSlots slots, int p, uint64_t cap, ShardGeom g, uint64_t* __restrict__ cnt,
+                               uint64_t* __restrict__ d_n, uint64_t* __restrict__ ids,
+                               uint8_t* __restrict__ occ_src, uint32_t* __restrict__ occ_idx,
+                               uint32_t* __restrict__ keys, DevErr* err) {
+  const uint64_t total = static_cast<uint64_t>(p) * cap;
+  const uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i0 == 0) {
+    uint64_t off = 0;
+    for (int s = 0; s < p; ++s) {
+      const uint64_t n = slot_n(slots.p[s]);
+      if (n > cap) report(err, kErrCapacity, n, cap);
+      cnt[2 + s] = n;
+      cnt[2 + kMaxRanks + s] = off;
+      off += n <= cap ? n : cap;
+    }
+    cnt[0] = off;
+    *d_n = off;
+  }
+  for (uint64_t i = i0; i < total; i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const int s = static_cast<int>(i / cap);
+    const uint64_t idx = i - static_cast<uint64_t>(s) * cap;
+    const uint64_t ns = slot_n(slots.p[s]);
+    if (idx >= ns || idx >= cap) continue;
+    uint64_t base = 0;
+    for (int q = 0; q < s; ++q) {
+      const uint64_t nq = slot_n(slots.p[q]);
+      base += nq <= cap ? nq : cap;
+    }
+    const uint64_t id = reinterpret_cast<const uint64_t*>(slots.p[s] + kHdr)[idx];
+    if (!g.owns(id)) report(err, kErrRecvNotOwned, id, g.shard);
+    const uint64_t j = base + idx;
+    ids[j] = id;
+    occ_src[j] = static_cast<uint8_t>(s);
+    occ_idx[j] = static_cast<uint32_t>(idx);
+    keys[j] = static_cast<uint32_t>(id / static_cast<uint64_t>(g.p));
+  }
+}
+
 // IterationStats.blocking_bytes (embedding.cpp:498-593) in the reference's
 // accounting (8-byte values): collision grads sent + received, E_co
 // messages sent + received.
@@ -838,6 +879,11 @@ struct Engine {
       o.srt.reserve(o.m_cap);
       FSX_LAUNCH(ctx, k_self_receive, grid_for(ctx, cap, 256, 8), 256, 0, s, slots.p[0], cap, o.cnt.p, o.srt.d_n(),
                  o.ids.p, o.occ_src.p, o.occ_idx.p, o.srt.k32a.p, ctx->d_err);
+      o.srt.run(ctx, o.ids.p, o.m_cap, t->g, true, false, t->key_bits(), s, /*keys_ready=*/true);
+    } else if (t->key_bits() <= 32) {
+      o.srt.reserve(o.m_cap);
+      FSX_LAUNCH(ctx, k_receive_keys, grid_for(ctx, static_cast<uint64_t>(p) * cap, 256, 8), 256, 0, s, slots, p,
+                 cap, t->g, o.cnt.p, o.srt.d_n(), o.ids.p, o.occ_src.p, o.occ_idx.p, o.srt.k32a.p, ctx->d_err);
       o.srt.run(ctx, o.ids.p, o.m_cap, t->g, true, false, t->key_bits(), s, /*keys_ready=*/true);
     } else {
       FSX_LAUNCH(ctx, k_recv_prefix, 1, 32, 0, s, slots, p, cap, o.cnt.p, ctx->d_err);
