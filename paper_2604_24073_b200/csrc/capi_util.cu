@@ -5,7 +5,7 @@ namespace fsx {
 namespace {
 thread_local std::string g_last_error;
 
-__global__ void k_max_u64(const uint64_t* __restrict__ k, uint64_t n, unsigned long long* out) {
+__global__ void k_max_u64(const uint64_t* __restrict__ k, uint64_t n, unsigned long long* out) { FSX_PDL_ENTER();
   unsigned long long m = 0;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)

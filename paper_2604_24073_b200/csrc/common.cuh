@@ -104,6 +104,7 @@ struct Ctx {
   unsigned copy_per_sm = 3, single_per_sm = 8, flat_per_sm = 16, warp_per_sm = 3;
   bool sgd_warp = true;  // FSX_SGD_WARP=0: the thread-per-vector k_sgd_flat + k_sgd_combine
   unsigned warp_variant = 0;  // FSX_WARP_VARIANT (tuning): k_sgd_warp unroll / min CTAs per SM
+  bool pdl = true;       // programmatic dependent launches (FSX_PDL=0: plain launches)
   bool onesweep = true;  // decoupled look-back radix passes (FSX_ONESWEEP=0: 3 launches per pass)
 
   void check_error(cudaStream_t s);  // D2H the word, sync `s`, throw if set
@@ -122,11 +123,38 @@ struct DeviceGuard {
 };
 
 // Launch helper: counts launches and checks the launch error.
-#define FSX_LAUNCH(ctx, kernel, grid, block, smem, stream, ...)             \
-  do {                                                                      \
-    kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);             \
-    FSX_CUDA(cudaGetLastError());                                           \
-    (ctx)->launches.fetch_add(1, std::memory_order_relaxed);                \
+// Every kernel is a programmatic dependent launch (PDL) when ctx->pdl: the
+// next kernel on a stream is scheduled while the previous one drains, and
+// waits for its completion (and memory) at its first statement — the
+// FSX_PDL_ENTER() that opens every __global__ function. Each kernel then
+// releases its own dependent as soon as all of its CTAs are resident, so a
+// chain of short latency-bound kernels (the side lanes' sort / scan / flag
+// kernels) overlaps launch latency with the predecessor's tail.
+#define FSX_PDL_ENTER()                                  \
+  do {                                                   \
+    asm volatile("griddepcontrol.wait;" ::: "memory");   \
+    asm volatile("griddepcontrol.launch_dependents;" ::); \
+  } while (0)
+
+#define FSX_LAUNCH(ctx_, kern_, grid_, block_, smem_, strm_, ...)                       \
+  do {                                                                                \
+    if ((ctx_)->pdl) {                                                                 \
+      cudaLaunchConfig_t cfg_{};                                                      \
+      cfg_.gridDim = dim3(grid_);                                                      \
+      cfg_.blockDim = dim3(block_);                                                    \
+      cfg_.dynamicSmemBytes = (smem_);                                                 \
+      cfg_.stream = (strm_);                                                         \
+      cudaLaunchAttribute at_[1];                                                     \
+      at_[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;                 \
+      at_[0].val.programmaticStreamSerializationAllowed = 1;                          \
+      cfg_.attrs = at_;                                                               \
+      cfg_.numAttrs = 1;                                                              \
+      FSX_CUDA(cudaLaunchKernelEx(&cfg_, kern_, __VA_ARGS__));                       \
+    } else {                                                                          \
+      kern_<<<(grid_), (block_), (smem_), (strm_)>>>(__VA_ARGS__);                     \
+      FSX_CUDA(cudaGetLastError());                                                   \
+    }                                                                                 \
+    (ctx_)->launches.fetch_add(1, std::memory_order_relaxed);                          \
   } while (0)
 
 // ---- device buffers ----------------------------------------------------------

@@ -81,7 +81,7 @@ inline void nccl_check(ncclResult_t r, const char* what) {
 
 namespace {
 
-__global__ void k_prefix(const uint64_t* cnt, int p, int stride, uint64_t* off) {
+__global__ void k_prefix(const uint64_t* cnt, int p, int stride, uint64_t* off) { FSX_PDL_ENTER();
   if (threadIdx.x == 0) {
     uint64_t s = 0;
     for (int d = 0; d < p; ++d) {
@@ -93,7 +93,7 @@ __global__ void k_prefix(const uint64_t* cnt, int p, int stride, uint64_t* off) 
 }
 
 // out[0] = sum of even entries, out[1] = sum of odd entries of t[0..2p)
-__global__ void k_sum_pairs(const uint64_t* t, int p, uint64_t* out) {
+__global__ void k_sum_pairs(const uint64_t* t, int p, uint64_t* out) { FSX_PDL_ENTER();
   if (threadIdx.x == 0) {
     uint64_t a = 0, b = 0;
     for (int d = 0; d < p; ++d) {
@@ -112,7 +112,7 @@ __global__ void k_sum_pairs(const uint64_t* t, int p, uint64_t* out) {
 // (tot[0] = n, send_off = {0, n}).
 __global__ void k_route_self(const uint64_t* __restrict__ ids, uint64_t n, uint64_t total_rows, Slots send,
                              uint32_t* __restrict__ send_pos, uint8_t* __restrict__ send_dst,
-                             uint64_t* tot, DevErr* err) {
+                             uint64_t* tot, DevErr* err) { FSX_PDL_ENTER();
   const uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (i0 == 0) {
     tot[0] = n;
@@ -139,7 +139,7 @@ __global__ void k_collide_count(const uint64_t* __restrict__ a, const uint64_t* 
                                 const uint64_t* __restrict__ b, const uint64_t* d_nb,
                                 const uint32_t* __restrict__ seg_a, uint8_t* __restrict__ flag_a,
                                 uint8_t* __restrict__ flag_b, uint32_t* __restrict__ partner_a,
-                                unsigned long long* misc) {
+                                unsigned long long* misc) { FSX_PDL_ENTER();
   const uint64_t na = *d_na, nb = *d_nb;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   const uint64_t n_round = (na + 31) & ~uint64_t{31};
@@ -173,7 +173,7 @@ __global__ void k_collide_count(const uint64_t* __restrict__ a, const uint64_t* 
 // one rank: the split / occurrence-rank totals of the statistics from the
 // collision counts ([0] exclusive, [1] collision occurrences)
 __global__ void k_self_split_totals(const uint64_t* d_n, const uint64_t* misc, int with_co, uint64_t* split_tot,
-                                    uint64_t* occ_tot) {
+                                    uint64_t* occ_tot) { FSX_PDL_ENTER();
   if (threadIdx.x == 0) {
     const uint64_t n = *d_n, c = with_co ? misc[1] : 0;
     split_tot[0] = occ_tot[0] = n - c;
@@ -187,7 +187,7 @@ __global__ void k_self_split_totals(const uint64_t* d_n, const uint64_t* misc, i
 __global__ void k_self_receive(const char* __restrict__ slot, uint64_t cap, uint64_t* __restrict__ cnt,
                                uint64_t* __restrict__ d_n, uint64_t* __restrict__ ids,
                                uint8_t* __restrict__ occ_src, uint32_t* __restrict__ occ_idx,
-                               uint32_t* __restrict__ keys, DevErr* err) {
+                               uint32_t* __restrict__ keys, DevErr* err) { FSX_PDL_ENTER();
   const uint64_t n_msg = reinterpret_cast<const uint64_t*>(slot)[0];
   const uint64_t n = n_msg <= cap ? n_msg : cap;
   const uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -214,7 +214,7 @@ __global__ void k_self_receive(const char* __restrict__ slot, uint64_t cap, uint
 __global__ void k_receive_keys(CSlots slots, int p, uint64_t cap, ShardGeom g, uint64_t* __restrict__ cnt,
                                uint64_t* __restrict__ d_n, uint64_t* __restrict__ ids,
                                uint8_t* __restrict__ occ_src, uint32_t* __restrict__ occ_idx,
-                               uint32_t* __restrict__ keys, DevErr* err) {
+                               uint32_t* __restrict__ keys, DevErr* err) { FSX_PDL_ENTER();
   const uint64_t total = static_cast<uint64_t>(p) * cap;
   const uint64_t i0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (i0 == 0) {
@@ -255,7 +255,7 @@ __global__ void k_receive_keys(CSlots slots, int p, uint64_t cap, ShardGeom g, u
 // (single rank: E_co is a message to self carrying every collision row)
 __global__ void k_blocking_bytes(int p, uint64_t rb8, const uint64_t* split_tot,
                                  const uint64_t* occ_tot, const uint64_t* pack_tot, CSlots cor_recv,
-                                 const uint64_t* co_count, int have_grads, int have_eco, uint64_t* out) {
+                                 const uint64_t* co_count, int have_grads, int have_eco, uint64_t* out) { FSX_PDL_ENTER();
   if (threadIdx.x != 0) return;
   uint64_t b = 0;
   if (have_grads)

@@ -34,7 +34,7 @@ __device__ __forceinline__ uint64_t slot_n(const char* s) { return *reinterpret_
 // ---- headers ---------------------------------------------------------------
 // n of destination d = counts[d * stride] (device); one thread per slot.
 static __global__ void k_write_headers(Slots dst, int p, const uint64_t* counts, int stride,
-                                uint64_t cap, DevErr* err) {
+                                uint64_t cap, DevErr* err) { FSX_PDL_ENTER();
   const int d = threadIdx.x;
   if (d < p) {
     const uint64_t n = counts[d * stride];
@@ -90,7 +90,7 @@ struct RouteOp {
 
 // ---- owner: flatten received ids (embedding.cpp:214-229) ----------------------
 // cnt[0] = M, cnt[2+s] = n_s, off[s] prefix (cnt[2+p+s])
-static __global__ void k_recv_prefix(CSlots slots, int p, uint64_t cap, uint64_t* cnt, DevErr* err) {
+static __global__ void k_recv_prefix(CSlots slots, int p, uint64_t cap, uint64_t* cnt, DevErr* err) { FSX_PDL_ENTER();
   if (threadIdx.x == 0) {
     uint64_t off = 0;
     for (int s = 0; s < p; ++s) {
@@ -106,7 +106,7 @@ static __global__ void k_recv_prefix(CSlots slots, int p, uint64_t cap, uint64_t
 
 static __global__ void k_flatten_recv(CSlots slots, int p, uint64_t cap, const uint64_t* cnt, ShardGeom g,
                                uint64_t* __restrict__ ids, uint8_t* __restrict__ occ_src,
-                               uint32_t* __restrict__ occ_idx, DevErr* err) {
+                               uint32_t* __restrict__ occ_idx, DevErr* err) { FSX_PDL_ENTER();
   const uint64_t total = static_cast<uint64_t>(p) * cap;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -124,7 +124,7 @@ static __global__ void k_flatten_recv(CSlots slots, int p, uint64_t cap, const u
 
 // src bitmask per unique row: bit s set iff source s requested it
 static __global__ void k_src_bits(const uint32_t* __restrict__ inverse, const uint8_t* __restrict__ occ_src,
-                           const uint64_t* d_m, uint32_t* __restrict__ bits) {
+                           const uint64_t* d_m, uint32_t* __restrict__ bits) { FSX_PDL_ENTER();
   const uint64_t m = *d_m;
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < m;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x)
@@ -193,7 +193,7 @@ static __global__ void k_idx_pack(const uint32_t* __restrict__ inverse,
                                   const uint8_t* __restrict__ occ_src,
                                   const uint32_t* __restrict__ occ_idx, const uint64_t* d_m,
                                   const uint32_t* __restrict__ rank_us,
-                                  const uint8_t* __restrict__ co, Slots send, int self) {
+                                  const uint8_t* __restrict__ co, Slots send, int self) { FSX_PDL_ENTER();
   const uint64_t m = *d_m;
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < m;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -209,7 +209,7 @@ static __global__ void k_idx_pack(const uint32_t* __restrict__ inverse,
 static __global__ void k_mask_pack(const uint32_t* __restrict__ inverse,
                                    const uint8_t* __restrict__ occ_src,
                                    const uint32_t* __restrict__ occ_idx, const uint64_t* d_m,
-                                   const uint8_t* __restrict__ co, Slots send) {
+                                   const uint8_t* __restrict__ co, Slots send) { FSX_PDL_ENTER();
   const uint64_t m = *d_m;
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < m;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x)
@@ -246,7 +246,7 @@ struct OccRankOp {
 // ---- requester: collision flag of every sent occurrence (MASK messages) ----
 static __global__ void k_req_flags(CSlots mask, const uint8_t* __restrict__ send_dst,
                                    const uint64_t* __restrict__ send_off, uint64_t n,
-                                   uint8_t* __restrict__ flag, DevErr* err) {
+                                   uint8_t* __restrict__ flag, DevErr* err) { FSX_PDL_ENTER();
   for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n;
        k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const int d = send_dst[k];
@@ -477,7 +477,7 @@ struct GroupOp {
 };
 
 // headers + closing seg entry: tot[2s] = n_occ, tot[2s+1] = n_slots
-static __global__ void k_grp_headers(Slots send, int p, const uint64_t* tot) {
+static __global__ void k_grp_headers(Slots send, int p, const uint64_t* tot) { FSX_PDL_ENTER();
   const int s = threadIdx.x;
   if (s < p) {
     const uint64_t n_occ = tot[2 * s], n_slots = tot[2 * s + 1];
@@ -489,7 +489,7 @@ static __global__ void k_grp_headers(Slots send, int p, const uint64_t* tot) {
 
 // requester: per-owner bases of the received GRP messages.
 // bases[0..p] slot prefix, bases[17..17+p] occurrence prefix, bases[34+d] = n_slots_d
-static __global__ void k_grp_bases(CSlots grp, int p, uint64_t* bases) {
+static __global__ void k_grp_bases(CSlots grp, int p, uint64_t* bases) { FSX_PDL_ENTER();
   if (threadIdx.x == 0) {
     uint64_t s = 0, o = 0;
     for (int d = 0; d < p; ++d) {
@@ -513,7 +513,7 @@ static __global__ void k_grp_bases(CSlots grp, int p, uint64_t* bases) {
 static __global__ void k_grp_flatten(CSlots grp, int p, uint64_t cap, const uint64_t* bases,
                                      const uint64_t* send_off, const uint32_t* send_pos, Slots cog,
                                      uint32_t row_bytes, uint8_t* flag, uint32_t* seg_flat,
-                                     uint32_t* perm_flat, char** out_ptr) {
+                                     uint32_t* perm_flat, char** out_ptr) { FSX_PDL_ENTER();
   const uint64_t total = static_cast<uint64_t>(p) * (cap + 1);
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -558,7 +558,7 @@ __global__ void __launch_bounds__(128) k_co_apply(T* __restrict__ table, ShardGe
                                                    const uint64_t* d_u, const uint8_t* __restrict__ co,
                                                    const uint32_t* __restrict__ bits,
                                                    const uint32_t* __restrict__ slot_us, CSlots cog,
-                                                   int p, EcoOut eco, DevErr* err) {
+                                                   int p, EcoOut eco, DevErr* err) { FSX_PDL_ENTER();
   using V = VecOf<T, VE>;
   const uint64_t U = *d_u;
   const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);

@@ -65,7 +65,7 @@ void Ctx::check_error(cudaStream_t s) {
 __global__ void k_intersect_flags(const uint64_t* __restrict__ a, const uint64_t* d_na,
                                   const uint64_t* __restrict__ b, const uint64_t* d_nb,
                                   uint8_t* __restrict__ flag_a, uint8_t* __restrict__ flag_b,
-                                  uint32_t* __restrict__ partner_a) {
+                                  uint32_t* __restrict__ partner_a) { FSX_PDL_ENTER();
   const uint64_t na = *d_na, nb = *d_nb;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < na;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -167,6 +167,7 @@ int fsx_ctx_create(int device, int rank, int world, fsx_ctx** out) {
   // lane was slimmed: 0.274 -> 0.259 ms at N = 1; on at N = 4 as well)
   c->onesweep = true;
   if (const char* v = std::getenv("FSX_ONESWEEP")) c->onesweep = std::atoi(v) != 0;
+  if (const char* v = std::getenv("FSX_PDL")) c->pdl = std::atoi(v) != 0;
   FSX_CUDA(cudaMalloc(&c->d_err, sizeof(DevErr)));
   FSX_CUDA(cudaMemset(c->d_err, 0, sizeof(DevErr)));
   FSX_CUDA(cudaMallocHost(&c->h_err, sizeof(DevErr)));
@@ -248,7 +249,7 @@ int fsx_collision_split(fsx_ctx* ctx, const uint64_t* d_cur, uint64_t n_cur,
   DevBuf<uint8_t> fa(na ? na : 1), fb(nb ? nb : 1);
   FSX_CUDA(cudaMemsetAsync(fb.p, 0, nb ? nb : 1, s));
   FSX_LAUNCH(ctx, k_intersect_flags, grid_for(ctx, na, 256, 8), 256, 0, s, ua.p, cnt.p, ub.p,
-             cnt.p + 1, fa.p, fb.p);
+             cnt.p + 1, fa.p, fb.p, nullptr);
   ScanScratch sc;
   SplitByFlagOp opa{ua.p, fa.p, d_co, d_ex_cur};
   run_scan(ctx, opa, na, cnt.p, sc, cnt.p + 2, s);

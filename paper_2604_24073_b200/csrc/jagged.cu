@@ -22,7 +22,7 @@ constexpr int kJagTile = 2048;  // segments per scan tile
 // counted as empty so the scan stays defined
 __global__ void k_perm_lengths(const uint64_t* __restrict__ offs, uint64_t n_segs,
                                const uint64_t* __restrict__ perm, uint64_t n_perm,
-                               uint64_t* __restrict__ out_len, DevErr* err) {
+                               uint64_t* __restrict__ out_len, DevErr* err) { FSX_PDL_ENTER();
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < n_perm;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t k = perm[j];
@@ -38,7 +38,7 @@ __global__ void k_perm_lengths(const uint64_t* __restrict__ offs, uint64_t n_seg
 // exclusive scan of u64 lengths, three launches: tile sums, scan of the tile
 // sums (one CTA), tile-local scan + carry
 __global__ void __launch_bounds__(kJagThreads) k_tile_sums(const uint64_t* __restrict__ len, uint64_t n,
-                                                           uint64_t* __restrict__ sums) {
+                                                           uint64_t* __restrict__ sums) { FSX_PDL_ENTER();
   __shared__ uint64_t ws[kJagThreads / 32];
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kJagTile;
   uint64_t s = 0;
@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(kJagThreads) k_tile_sums(const uint64_t* __res
   }
 }
 
-__global__ void k_scan_sums(uint64_t* sums, uint64_t tiles, uint64_t* total) {
+__global__ void k_scan_sums(uint64_t* sums, uint64_t tiles, uint64_t* total) { FSX_PDL_ENTER();
   // one warp: sequential carry over 32-wide chunks
   const unsigned lane = threadIdx.x & 31u;
   uint64_t carry = 0;
@@ -75,7 +75,7 @@ __global__ void k_scan_sums(uint64_t* sums, uint64_t tiles, uint64_t* total) {
 __global__ void __launch_bounds__(kJagThreads) k_tile_scan(const uint64_t* __restrict__ len, uint64_t n,
                                                            const uint64_t* __restrict__ sums,
                                                            const uint64_t* __restrict__ total,
-                                                           uint64_t* __restrict__ offs) {
+                                                           uint64_t* __restrict__ offs) { FSX_PDL_ENTER();
   // each thread owns kJagTile / kJagThreads consecutive segments
   constexpr int kPer = kJagTile / kJagThreads;
   __shared__ uint64_t ws[kJagThreads / 32];
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kJagThreads) k_perm_values(const char* __restr
                                                              const uint64_t* __restrict__ offs, uint64_t n_segs,
                                                              const uint64_t* __restrict__ perm,
                                                              const uint64_t* __restrict__ out_offs, uint64_t n_perm,
-                                                             uint32_t elem_bytes, char* __restrict__ out) {
+                                                             uint32_t elem_bytes, char* __restrict__ out) { FSX_PDL_ENTER();
   const unsigned lane = threadIdx.x & 31u;
   const uint64_t warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
   const uint32_t upe = elem_bytes / sizeof(U);  // units per element
@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kJagThreads) k_perm_values(const char* __restr
 }
 
 // keyed_transpose permutation (jagged.hpp:232-241): target position of (f, s)
-__global__ void k_transpose_perm(uint64_t keys, uint64_t samples, int feature_major, uint64_t* __restrict__ perm) {
+__global__ void k_transpose_perm(uint64_t keys, uint64_t samples, int feature_major, uint64_t* __restrict__ perm) { FSX_PDL_ENTER();
   const uint64_t n = keys * samples;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {

@@ -43,7 +43,7 @@ __device__ __forceinline__ double initial_value_dev(uint64_t seed, uint64_t row,
 }
 
 template <class T>
-__global__ void k_init_table(T* __restrict__ vals, ShardGeom g, uint64_t seed) {
+__global__ void k_init_table(T* __restrict__ vals, ShardGeom g, uint64_t seed) { FSX_PDL_ENTER();
   const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
   const uint64_t wid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const unsigned lane = threadIdx.x & 31u;
@@ -86,7 +86,7 @@ constexpr int kRowsPerWarp = 8;
 
 template <class Map, int VB>
 __global__ void __launch_bounds__(256, 4) k_copy_rows(Map map, uint64_t n_cap, const uint64_t* d_n,
-                                                   uint32_t row_bytes) {
+                                                   uint32_t row_bytes) { FSX_PDL_ENTER();
   using V = typename VecT<VB>::type;
   const uint64_t n = scan_n(n_cap, d_n);
   const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
@@ -386,7 +386,7 @@ struct SgdPlanOp {
 template <class T>
 __global__ void k_grad_ptrs(GradRows<T> gr, const uint32_t* __restrict__ perm,
                             const uint32_t* __restrict__ seg_start, const uint64_t* d_u,
-                            const T** __restrict__ gptr) {
+                            const T** __restrict__ gptr) { FSX_PDL_ENTER();
   const uint64_t n = seg_start[*d_u];
   for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n;
        k += static_cast<uint64_t>(gridDim.x) * blockDim.x)
@@ -493,7 +493,7 @@ __device__ __forceinline__ void sgd_store_vec(const SgdArgs<T>& a, uint32_t u, T
 //
 // k_sgd_single: one-occurrence rows, two items per thread in flight.
 template <class T, int VE>
-__global__ void __launch_bounds__(256) k_sgd_single(SgdArgs<T> a, uint32_t vpr_shift) {
+__global__ void __launch_bounds__(256) k_sgd_single(SgdArgs<T> a, uint32_t vpr_shift) { FSX_PDL_ENTER();
   using V = VecOf<T, VE>;
   const uint64_t n = *a.d_single_n;
   const uint32_t dim = a.g.dim;
@@ -538,7 +538,7 @@ __global__ void __launch_bounds__(256) k_sgd_single(SgdArgs<T> a, uint32_t vpr_s
 // partials for k_sgd_combine.
 constexpr int kFlatBatch = 8;
 template <class T, int VE>
-__global__ void __launch_bounds__(256, 3) k_sgd_flat(SgdArgs<T> a, uint32_t vpr_shift) {
+__global__ void __launch_bounds__(256, 3) k_sgd_flat(SgdArgs<T> a, uint32_t vpr_shift) { FSX_PDL_ENTER();
   using V = VecOf<T, VE>;
   const uint64_t nwork = *a.d_work_n;
   const uint32_t dim = a.g.dim;
@@ -598,7 +598,7 @@ __global__ void __launch_bounds__(256, 3) k_sgd_flat(SgdArgs<T> a, uint32_t vpr_
 // `done[u]`, reset by that warp) adds them in chunk order — the association
 // k_sgd_combine uses — and applies the row: no separate combine pass.
 template <class T, int VE, int VPL, int U, int MINB = 1>
-__global__ void __launch_bounds__(256, MINB) k_sgd_warp(SgdArgs<T> a, uint32_t* __restrict__ done) {
+__global__ void __launch_bounds__(256, MINB) k_sgd_warp(SgdArgs<T> a, uint32_t* __restrict__ done) { FSX_PDL_ENTER();
   using V = VecOf<T, VE>;
   constexpr unsigned kFull = 0xffffffffu;
   const uint64_t nwork = *a.d_work_n;
@@ -711,7 +711,7 @@ __global__ void __launch_bounds__(256, MINB) k_sgd_warp(SgdArgs<T> a, uint32_t* 
 // one CTA per multi-chunk row, each thread owning VE columns: the row's chunk
 // partials are summed in chunk order (8 loads in flight per thread)
 template <class T, int VE>
-__global__ void __launch_bounds__(128) k_sgd_combine(SgdArgs<T> a) {
+__global__ void __launch_bounds__(128) k_sgd_combine(SgdArgs<T> a) { FSX_PDL_ENTER();
   const uint64_t nm = *a.d_multi_n;
   const uint32_t dim = a.g.dim;
   for (uint64_t m = blockIdx.x; m < nm; m += gridDim.x) {

@@ -19,7 +19,7 @@ namespace {
 // the integer sum) while every L < 2^26 and the total stays below 2^53 — the
 // CTA checks both and otherwise its thread 0 redoes the f64 sum sequentially.
 __global__ void k_cost(const uint64_t* __restrict__ lens, const uint64_t* __restrict__ offsets,
-                       double c0, double c1, double c2, double* __restrict__ out) {
+                       double c0, double c1, double c2, double* __restrict__ out) { FSX_PDL_ENTER();
   __shared__ unsigned long long s_tok, s_sq, s_big;
   const uint64_t lo = offsets[blockIdx.x], hi = offsets[blockIdx.x + 1];
   if (threadIdx.x == 0) { s_tok = 0; s_sq = 0; s_big = 0; }
@@ -56,7 +56,7 @@ __global__ void k_cost(const uint64_t* __restrict__ lens, const uint64_t* __rest
 // descending length, then origin, then local index.
 __global__ void k_partition_keys(const uint64_t* __restrict__ lens, const int32_t* __restrict__ origin,
                                  const int32_t* __restrict__ local, uint64_t m, uint64_t maxlen, int bo,
-                                 int bl, uint64_t* __restrict__ keys) {
+                                 int bl, uint64_t* __restrict__ keys) { FSX_PDL_ENTER();
   for (uint64_t g = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; g < m;
        g += static_cast<uint64_t>(gridDim.x) * blockDim.x)
     keys[g] = ((maxlen - lens[g]) << (bo + bl)) | (static_cast<uint64_t>(origin[g]) << bl) |
@@ -65,7 +65,7 @@ __global__ void k_partition_keys(const uint64_t* __restrict__ lens, const int32_
 
 // snake deal (partition.cpp:169-174): sorted position k -> rank
 __global__ void k_fbs_assign(const uint32_t* __restrict__ sorted, uint64_t m, int n,
-                             int32_t* __restrict__ assignment, uint64_t* __restrict__ order) {
+                             int32_t* __restrict__ assignment, uint64_t* __restrict__ order) { FSX_PDL_ENTER();
   const uint64_t per = m / static_cast<uint64_t>(n);
   for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < m;
        k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
@@ -82,7 +82,7 @@ __global__ void k_fbs_assign(const uint32_t* __restrict__ sorted, uint64_t m, in
 // L < 2^26 (std::pow returns the exact product then); prefix sums are exact
 // integers below 2^53. Both are checked; otherwise the host supplies weights.
 __global__ void k_vbs_weights(const uint64_t* __restrict__ lens, const uint32_t* __restrict__ sorted,
-                              uint64_t m, int alpha2, uint64_t* __restrict__ wint) {
+                              uint64_t m, int alpha2, uint64_t* __restrict__ wint) { FSX_PDL_ENTER();
   for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < m;
        k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     const uint64_t l = lens[sorted[k]];
@@ -92,7 +92,7 @@ __global__ void k_vbs_weights(const uint64_t* __restrict__ lens, const uint32_t*
 
 // sequential f64 prefix (prefix[i+1] = prefix[i] + w[i], partition.cpp:58-59)
 // for weights that are not exact integers: one thread, reference order
-__global__ void k_prefix_seq(const double* __restrict__ w, uint64_t m, double* __restrict__ prefix) {
+__global__ void k_prefix_seq(const double* __restrict__ w, uint64_t m, double* __restrict__ prefix) { FSX_PDL_ENTER();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     double s = 0.0;
     prefix[0] = 0.0;
@@ -105,7 +105,7 @@ __global__ void k_prefix_seq(const double* __restrict__ w, uint64_t m, double* _
 
 // u64 inclusive scan: one CTA of 1024 threads, contiguous chunks (m <= ~1M)
 __global__ void __launch_bounds__(1024) k_prefix_u64(const uint64_t* __restrict__ w, uint64_t m,
-                                                     double* __restrict__ prefix) {
+                                                     double* __restrict__ prefix) { FSX_PDL_ENTER();
   __shared__ unsigned long long part[1024];
   const uint64_t per = (m + blockDim.x - 1) / blockDim.x;
   const uint64_t lo = threadIdx.x * per, hi = lo + per < m ? lo + per : m;
@@ -130,14 +130,14 @@ __global__ void __launch_bounds__(1024) k_prefix_u64(const uint64_t* __restrict_
   }
 }
 
-__global__ void k_fill_inf(double* __restrict__ dp, uint64_t n) {
+__global__ void k_fill_inf(double* __restrict__ dp, uint64_t n) { FSX_PDL_ENTER();
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
     dp[i] = __longlong_as_double(0x7ff0000000000000ll);
 }
 
 // dp layer k=1: dp[1][j] = prefix[j]
-__global__ void k_dp_first(const double* __restrict__ prefix, uint64_t m, double* __restrict__ dp1) {
+__global__ void k_dp_first(const double* __restrict__ prefix, uint64_t m, double* __restrict__ dp1) { FSX_PDL_ENTER();
   for (uint64_t j = 1 + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j <= m;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x)
     dp1[j] = prefix[j];
@@ -147,7 +147,7 @@ __global__ void k_dp_first(const double* __restrict__ prefix, uint64_t m, double
 // strict `<` keeps the largest x attaining the minimum, and the scan stops
 // once the trailing segment alone reaches the best cost (partition.cpp:66-81).
 __global__ void k_dp_layer(const double* __restrict__ prefix, const double* __restrict__ prev,
-                           uint64_t m, int k, double* __restrict__ cur, uint32_t* __restrict__ cut) {
+                           uint64_t m, int k, double* __restrict__ cur, uint32_t* __restrict__ cut) { FSX_PDL_ENTER();
   for (uint64_t j = static_cast<uint64_t>(k) + blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
        j <= m; j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     double best = __longlong_as_double(0x7ff0000000000000ll);
@@ -170,7 +170,7 @@ __global__ void k_dp_layer(const double* __restrict__ prefix, const double* __re
 }
 
 // backtrack (partition.cpp:84-90): sizes of the n segments
-__global__ void k_dp_backtrack(const uint32_t* __restrict__ cut, uint64_t m, int n, int32_t* __restrict__ sizes) {
+__global__ void k_dp_backtrack(const uint32_t* __restrict__ cut, uint64_t m, int n, int32_t* __restrict__ sizes) { FSX_PDL_ENTER();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     uint64_t j = m;
     for (int k = n; k >= 1; --k) {
@@ -183,7 +183,7 @@ __global__ void k_dp_backtrack(const uint32_t* __restrict__ cut, uint64_t m, int
 
 // contiguous segments of the sorted order: sorted position k -> rank
 __global__ void k_vbs_assign(const uint32_t* __restrict__ sorted, uint64_t m, const int32_t* __restrict__ sizes,
-                             int n, int32_t* __restrict__ assignment, uint64_t* __restrict__ order) {
+                             int n, int32_t* __restrict__ assignment, uint64_t* __restrict__ order) { FSX_PDL_ENTER();
   for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < m;
        k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     uint64_t start = 0;

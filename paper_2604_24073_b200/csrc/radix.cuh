@@ -36,7 +36,7 @@ template <class K>
 __global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const K* __restrict__ keys,
                                                               uint64_t n_cap, const uint64_t* d_n,
                                                               int shift, unsigned mask, uint32_t* counts,
-                                                              unsigned tiles) {
+                                                              unsigned tiles) { FSX_PDL_ENTER();
   __shared__ uint32_t hist[kRadixBins];
   const uint64_t n = scan_n(n_cap, d_n);
   for (int b = 0; b < kBinsPerThread; ++b) hist[threadIdx.x + b * kRadixThreads] = 0;
@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(kRadixThreads) k_radix_hist(const K* __restric
 // one warp per digit: exclusive scan of counts[d][0..tiles) in place, total[d]
 static __global__ void __launch_bounds__(256) k_radix_rows(uint32_t* __restrict__ counts,
                                                            unsigned tiles, unsigned bins,
-                                                           uint32_t* __restrict__ total) {
+                                                           uint32_t* __restrict__ total) { FSX_PDL_ENTER();
   const unsigned lane = threadIdx.x & 31u;
   const unsigned d = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (d >= bins) return;
@@ -85,7 +85,7 @@ template <class K>
 __global__ void __launch_bounds__(kRadixThreads) k_radix_scatter(
     const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
     uint32_t* __restrict__ vout, uint64_t n_cap, const uint64_t* d_n, int shift, unsigned mask,
-    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ digit_total, unsigned tiles) {
+    const uint32_t* __restrict__ offsets, const uint32_t* __restrict__ digit_total, unsigned tiles) { FSX_PDL_ENTER();
   __shared__ uint32_t wcount[kRadixWarps][kRadixBins];
   __shared__ uint32_t tile_off[kRadixBins];
   __shared__ uint32_t wsum[kRadixWarps];
@@ -181,7 +181,7 @@ constexpr uint32_t kOsAgg = 1u << 30, kOsIncl = 2u << 30, kOsCount = (1u << 30) 
 template <class K>
 __global__ void __launch_bounds__(kRadixThreads) k_os_hist(const K* __restrict__ keys, uint64_t n_cap,
                                                            const uint64_t* d_n, int passes, int dbits,
-                                                           uint32_t* __restrict__ hist) {
+                                                           uint32_t* __restrict__ hist) { FSX_PDL_ENTER();
   __shared__ uint32_t h[kOsMaxPasses][kRadixBins];
   for (int i = threadIdx.x; i < kOsMaxPasses * kRadixBins; i += blockDim.x) (&h[0][0])[i] = 0;
   __syncthreads();
@@ -209,7 +209,7 @@ template <class K>
 __global__ void __launch_bounds__(kRadixThreads) k_os_scatter(
     const K* __restrict__ kin, const uint32_t* __restrict__ vin, K* __restrict__ kout,
     uint32_t* __restrict__ vout, uint64_t n_cap, const uint64_t* d_n, int shift, unsigned mask,
-    const uint32_t* __restrict__ digit_total, uint32_t* status, uint32_t* tile_ctr) {
+    const uint32_t* __restrict__ digit_total, uint32_t* status, uint32_t* tile_ctr) { FSX_PDL_ENTER();
   __shared__ uint32_t wcount[kRadixWarps][kRadixBins];
   __shared__ uint32_t tile_off[kRadixBins];
   __shared__ uint32_t wsum[kRadixWarps];

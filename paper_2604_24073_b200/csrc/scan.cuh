@@ -70,7 +70,7 @@ __device__ __forceinline__ void block_exclusive_scan(uint32_t (&v)[NC], uint32_t
 template <class Op>
 static __global__ void __launch_bounds__(kScanThreads) k_tile_reduce(Op op, uint64_t n_cap,
                                                               const uint64_t* d_n,
-                                                              uint32_t* tile_sums) {
+                                                              uint32_t* tile_sums) { FSX_PDL_ENTER();
   constexpr int NC = Op::NC;
   const uint64_t n = scan_n(n_cap, d_n);
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile;
@@ -102,7 +102,7 @@ static __global__ void __launch_bounds__(kScanThreads) k_tile_reduce(Op op, uint
 // (in place, all counters in one block pass), grand totals to `totals`.
 template <int NC>
 static __global__ void __launch_bounds__(1024) k_scan_tiles(uint32_t* tile_sums, unsigned tiles,
-                                                            uint64_t* totals) {
+                                                            uint64_t* totals) { FSX_PDL_ENTER();
   __shared__ uint32_t wt[32][NC];
   const unsigned per = (tiles + blockDim.x - 1) / blockDim.x;
   const unsigned lo = threadIdx.x * per;
@@ -150,7 +150,7 @@ static __global__ void __launch_bounds__(kScanThreads) k_tile_emit(Op op, uint64
                                                                    const uint64_t* d_n,
                                                                    const uint32_t* tile_sums,
                                                                    unsigned tiles,
-                                                                   uint64_t* d_totals) {
+                                                                   uint64_t* d_totals) { FSX_PDL_ENTER();
   constexpr int NC = Op::NC;
   __shared__ uint32_t s_pre[NC], s_tot[NC];
   const uint64_t n = scan_n(n_cap, d_n);

@@ -15,7 +15,7 @@ namespace fsx {
 template <class K>
 __global__ void k_make_keys(const uint64_t* __restrict__ ids, uint64_t n_cap, const uint64_t* d_n,
                             ShardGeom g, int local, int validate, K* __restrict__ keys,
-                            DevErr* err) {
+                            DevErr* err) { FSX_PDL_ENTER();
   const uint64_t n = scan_n(n_cap, d_n);
   for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < n;
        j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
