@@ -41,6 +41,7 @@ extern "C" {
 #define FSX_ERR_CONFIG (-6)           /* freescale::ConfigError          */
 #define FSX_ERR_CUDA (-7)             /* CUDA runtime/driver failure     */
 #define FSX_ERR_NOMEM (-8)            /* device allocation failed        */
+#define FSX_ERR_IO (-9)               /* freescale::IoError              */
 
 /* element type of table values, rows and gradients */
 #define FSX_F32 0
@@ -294,6 +295,29 @@ int fsx_keyed_transpose_perm(fsx_ctx* ctx, uint64_t num_keys, uint64_t num_sampl
  * engine's all-gather slot (max(8 * max_occurrences, 64 KiB) bytes). */
 int fsx_allgather_ce(fsx_engine* e, const void* d_send, uint64_t send_bytes, uint64_t max_bytes, void* d_recv,
                      uint64_t slot_bytes, uint64_t* h_recv_bytes, int ring, void* stream);
+
+/* ---- workload-file replay ----------------------------------- */
+/* Replaces workload::Reader::next_iteration (workload.hpp:131-140,
+ * workload.cpp:500-549) for the engine's input. Host part: walk the length
+ * prefixes of one iteration's bytes (h_bytes = the file from the iteration's
+ * first byte): h_rank_samples[num_ranks] = samples per rank, h_rec_off[k] =
+ * byte offset of record k's body (capacity cap; NULL only counts),
+ * *h_consumed = the iteration's size. FSX_ERR_IO with the reference's text
+ * ("workload: file truncated; last complete record is iteration I, rank R,
+ * sample S") on a short file. No device work. */
+int fsx_workload_scan(const uint8_t* h_bytes, uint64_t nbytes, int num_ranks, int iteration,
+                      uint64_t* h_rank_samples, uint64_t* h_rec_off, uint64_t cap, uint64_t* h_n_records,
+                      uint64_t* h_consumed);
+/* Device part: d_bytes = the same iteration's bytes in HBM, d_rec_off = the
+ * scan's offsets. Per record: d_uih_len[n], d_labels[n] (may be NULL); batch-major
+ * d_offsets[n + 1] (u64 exclusive prefix) and d_values (uih ids, capacity cap;
+ * NULL only sizes, *h_total = id count). FSX_ERR_IO "workload: record has
+ * trailing bytes at iteration I, rank R, sample S" (decode_sample consumed less
+ * than the record) or "workload: record truncated". Synchronizes `stream`. */
+int fsx_workload_decode(fsx_ctx* ctx, const uint8_t* d_bytes, uint64_t nbytes, const uint64_t* d_rec_off,
+                        uint64_t n, int iteration, const uint64_t* h_rank_samples, int num_ranks,
+                        uint64_t* d_uih_len, uint64_t* d_offsets, double* d_labels, uint64_t* d_values,
+                        uint64_t cap, uint64_t* h_total, void* stream);
 
 #ifdef __cplusplus
 }

@@ -300,6 +300,28 @@ class Reference(_Lib):
                       grad_scale, grad_shift, table, stats))
         return table[:total_rows * dim].reshape(total_rows, dim), stats[:3 * iters].reshape(iters, 3)
 
+    def save_workload_uniform(self, path, world, batch, max_uih, lo, hi, table_rows, seed, iters):
+        """workload::save_workload of generate_all (workload.cpp:551-557)."""
+        f = self._fn("save_workload_uniform", [C.c_char_p, C.c_int, C.c_int, C.c_uint64, C.c_uint64,
+                                               C.c_uint64, C.c_uint64, C.c_uint64, C.c_int])
+        self._check(f(path.encode(), world, batch, max_uih, lo, hi, table_rows, seed, iters))
+
+    def load_workload(self, path):
+        """workload::load_workload (workload.cpp:559-564), flattened: dict of
+        ids, lens / labels per sample, counts per (iteration, rank), ranks, iterations."""
+        f = self._fn("load_workload", [C.c_char_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                       C.POINTER(C.c_uint64), C.POINTER(C.c_uint64), C.POINTER(C.c_int)])
+        ni, ns, dims = C.c_uint64(), C.c_uint64(), (C.c_int * 2)()
+        self._check(f(path.encode(), None, None, None, None, C.byref(ni), C.byref(ns), dims))
+        ids = np.zeros(max(ni.value, 1), np.uint64)
+        lens = np.zeros(max(ns.value, 1), np.uint64)
+        labels = np.zeros(max(ns.value, 1), np.float64)
+        counts = np.zeros(max(dims[0] * dims[1], 1), np.uint64)
+        self._check(f(path.encode(), ids.ctypes.data, lens.ctypes.data, labels.ctypes.data, counts.ctypes.data,
+                      C.byref(ni), C.byref(ns), dims))
+        return {"ids": ids[:ni.value], "lens": lens[:ns.value], "labels": labels[:ns.value],
+                "counts": counts[:dims[0] * dims[1]], "ranks": dims[0], "iterations": dims[1]}
+
     def generate_uniform(self, world, batch, max_uih, lo, hi, table_rows, target_collision, seed,
                          iters):
         cap = iters * world * batch * max(max_uih, 1)

@@ -402,4 +402,55 @@ int fsref_bench_engine(int prioritized, int world, int iters, const std::uint64_
   SHIM_CATCH
 }
 
+// workload::save_workload (workload.cpp:551-557) of generate_all's output for a
+// uniform-length spec: a file written by the reference's own Writer, for the
+// workload-file replay parity tests.
+int fsref_save_workload_uniform(const char* path, int world, int batch, std::uint64_t max_uih,
+                                std::uint64_t lo, std::uint64_t hi, std::uint64_t table_rows,
+                                std::uint64_t seed, int iters) {
+  SHIM_TRY
+  workload::WorkloadSpec spec;
+  spec.num_ranks = world;
+  spec.batch_size = batch;
+  spec.max_uih = max_uih;
+  spec.dist = workload::DistSpec::uniform(lo, hi);
+  spec.table_rows = table_rows;
+  spec.seed = seed;
+  spec.num_iterations = iters;
+  workload::save_workload(path, spec, workload::generate_all(spec));
+  SHIM_CATCH
+}
+
+// workload::load_workload (workload.cpp:559-564) flattened [iter][rank][sample]:
+// counts_out[iter*ranks + rank] = samples, lens_out / labels_out per sample,
+// ids_out = uih ids in order. Sizing: with ids_out == nullptr only the totals
+// (n_ids, n_samples, dims[0] = ranks, dims[1] = iterations) are written.
+int fsref_load_workload(const char* path, std::uint64_t* ids_out, std::uint64_t* lens_out,
+                        double* labels_out, std::uint64_t* counts_out, std::uint64_t* n_ids,
+                        std::uint64_t* n_samples, int* dims) {
+  SHIM_TRY
+  auto [spec, its] = workload::load_workload(path);
+  dims[0] = spec.num_ranks;
+  dims[1] = spec.num_iterations;
+  std::uint64_t ni = 0, ns = 0, slot = 0;
+  for (const auto& it : its)
+    for (const auto& b : it) {
+      if (ids_out) counts_out[slot] = b.samples.size();
+      ++slot;
+      for (const auto& s : b.samples) {
+        if (ids_out) {
+          lens_out[ns] = s.uih.size();
+          labels_out[ns] = s.label;
+          for (auto x : s.uih) ids_out[ni++] = x;
+        } else {
+          ni += s.uih.size();
+        }
+        ++ns;
+      }
+    }
+  *n_ids = ni;
+  *n_samples = ns;
+  SHIM_CATCH
+}
+
 }  // extern "C"

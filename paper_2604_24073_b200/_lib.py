@@ -86,6 +86,8 @@ _SIGS = {
     "fsx_jagged_offsets": ([vp, vp, u64, vp, P(u64), vp], i32),
     "fsx_jagged_permute": ([vp, vp, u32, vp, u64, vp, u64, vp, u64, vp, vp, P(u64), vp], i32),
     "fsx_keyed_transpose_perm": ([vp, u64, u64, i32, vp, vp], i32),
+    "fsx_workload_scan": ([vp, u64, i32, i32, vp, vp, u64, P(u64), P(u64)], i32),
+    "fsx_workload_decode": ([vp, vp, u64, vp, u64, i32, vp, i32, vp, vp, vp, vp, u64, P(u64), vp], i32),
 }
 
 EXPORTED = sorted(_SIGS)

@@ -104,6 +104,9 @@ __global__ void __launch_bounds__(kJagThreads) k_tile_scan(const uint64_t* __res
   if (blockIdx.x == 0 && threadIdx.x == 0) offs[n] = *total;
 }
 
+}  // namespace
+
+// shared with workload.cu (record decode)
 void exclusive_offsets(Ctx* ctx, const uint64_t* len, uint64_t n, uint64_t* offs, DevBuf<uint64_t>& scratch,
                        cudaStream_t s) {
   const uint64_t tiles = ceil_div(n > 0 ? n : 1, kJagTile);
@@ -113,6 +116,8 @@ void exclusive_offsets(Ctx* ctx, const uint64_t* len, uint64_t n, uint64_t* offs
   FSX_LAUNCH(ctx, k_tile_scan, static_cast<unsigned>(tiles), kJagThreads, 0, s, len, n, scratch.p,
              scratch.p + tiles, offs);
 }
+
+namespace {
 
 // segment mover: warp per output segment, `U`-byte units (16/8/4/1),
 // coalesced over the segment; long segments stream, short ones finish fast

@@ -53,6 +53,7 @@ _BY_CODE = {
     -6: ConfigError,
     -7: CudaError,
     -8: CudaError,
+    -9: IoError,
 }
 
 
