@@ -14,9 +14,10 @@
 //   GPU   fsx_workload_decode one thread per record parses the record body
 //                             (uih count, candidate lists, label) and checks
 //                             it is consumed exactly (the reference's trailing
-//                             bytes IoError); u64 offsets scan; one warp per
-//                             record copies the UIH ids (4-byte aligned in the
-//                             file, 8-byte aligned in HBM) coalesced.
+//                             bytes IoError); u64 offsets scan; the UIH ids
+//                             (4-byte aligned in the file, 8-byte aligned in
+//                             HBM) move flattened over the output, 2,048 per
+//                             CTA tile, coalesced on both sides.
 //
 // Bytes per record moved on the device: the record once in (H2D of the raw
 // iteration), read once by the id mover, ids written once: ~2 x record bytes.
@@ -88,28 +89,75 @@ __global__ void k_rec_parse(const uint8_t* __restrict__ bytes, uint64_t nbytes, 
   }
 }
 
-// warp per record: uih ids -> values[offs[s] ..)
-__global__ void __launch_bounds__(256) k_rec_uih(const uint8_t* __restrict__ bytes,
-                                                 const uint64_t* __restrict__ rec_off, uint64_t n,
-                                                 const uint64_t* __restrict__ offs, uint64_t* __restrict__ values,
-                                                 uint64_t cap, DevErr* err) {
+// UIH id mover, flattened over the output ids so a 8,192-id record does not
+// serialise one warp (the power-law tail): a CTA takes 2,048 consecutive
+// output ids, finds the records that cover them (two binary searches over the
+// offsets), stages those records' offsets in shared memory, and each thread
+// resolves its id's record by a shared-memory binary search. Reads (4-byte
+// aligned u64 pairs in the file) and writes are coalesced over the tile.
+constexpr int kIdTile = 2048;
+constexpr int kIdThreads = 256;
+
+__device__ __forceinline__ uint64_t record_of(const uint64_t* offs, uint64_t lo, uint64_t hi, uint64_t x) {
+  // last r in [lo, hi) with offs[r] <= x (offs nondecreasing, offs[lo] <= x)
+  while (hi - lo > 1) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (offs[mid] <= x) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void __launch_bounds__(kIdThreads) k_rec_ids(const uint8_t* __restrict__ bytes,
+                                                        const uint64_t* __restrict__ rec_off, uint64_t n,
+                                                        const uint64_t* __restrict__ offs, uint64_t* __restrict__ values,
+                                                        uint64_t cap, DevErr* err) {
   FSX_PDL_ENTER();
-  const unsigned lane = threadIdx.x & 31u;
-  if (offs[n] > cap) {  // never write past the caller's buffer
-    if (blockIdx.x == 0 && threadIdx.x == 0) report(err, kErrIdCapacity, offs[n], cap);
+  __shared__ uint64_t sh_off[kIdTile + 1];
+  __shared__ uint64_t sh_src[kIdTile];
+  __shared__ uint64_t sh_r[2];
+  const uint64_t total = offs[n];
+  if (total > cap) {  // never write past the caller's buffer
+    if (blockIdx.x == 0 && threadIdx.x == 0) report(err, kErrIdCapacity, total, cap);
     return;
   }
-  const uint64_t warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t s = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5; s < n; s += warps) {
-    const uint8_t* src = bytes + rec_off[s] + 4;
-    const uint64_t b = offs[s], len = offs[s + 1] - b;
-    uint64_t* dst = values + b;
-    if ((reinterpret_cast<uintptr_t>(src) & 7u) == 0) {
-      const uint64_t* s8 = reinterpret_cast<const uint64_t*>(src);
-      for (uint64_t t = lane; t < len; t += 32) dst[t] = s8[t];
-    } else {
-      for (uint64_t t = lane; t < len; t += 32) dst[t] = ld_u64_a4(src + 8 * t);
+  for (uint64_t b = static_cast<uint64_t>(blockIdx.x) * kIdTile; b < total;
+       b += static_cast<uint64_t>(gridDim.x) * kIdTile) {
+    const uint64_t e = min(total, b + kIdTile);
+    if (threadIdx.x < 2) sh_r[threadIdx.x] = record_of(offs, 0, n, threadIdx.x == 0 ? b : e - 1);
+    __syncthreads();
+    const uint64_t r0 = sh_r[0], cnt = sh_r[1] - r0 + 1;
+    if (cnt <= kIdTile) {
+      for (uint64_t k = threadIdx.x; k < cnt; k += kIdThreads) {
+        sh_off[k] = offs[r0 + k];
+        sh_src[k] = rec_off[r0 + k] + 4;
+      }
+      __syncthreads();
+      // resolve all of this thread's ids first, then keep their loads in flight together
+      constexpr int kPer = kIdTile / kIdThreads;
+      const uint8_t* src[kPer];
+#pragma unroll
+      for (int j = 0; j < kPer; ++j) {
+        const uint64_t i = b + threadIdx.x + static_cast<uint64_t>(j) * kIdThreads;
+        src[j] = nullptr;
+        if (i < e) {
+          const uint64_t k = record_of(sh_off, 0, cnt, i);
+          src[j] = bytes + sh_src[k] + 8 * (i - sh_off[k]);
+        }
+      }
+      uint64_t v[kPer];
+#pragma unroll
+      for (int j = 0; j < kPer; ++j)
+        if (src[j]) v[j] = ld_u64_a4(src[j]);
+#pragma unroll
+      for (int j = 0; j < kPer; ++j)
+        if (src[j]) values[b + threadIdx.x + static_cast<uint64_t>(j) * kIdThreads] = v[j];
+    } else {  // more than kIdTile records (empty ones) behind 2,048 ids: search in global memory
+      for (uint64_t i = b + threadIdx.x; i < e; i += kIdThreads) {
+        const uint64_t r = record_of(offs, r0, r0 + cnt, i);
+        values[i] = ld_u64_a4(bytes + rec_off[r] + 4 + 8 * (i - offs[r]));
+      }
     }
+    __syncthreads();
   }
 }
 
@@ -181,8 +229,8 @@ int fsx_workload_decode(fsx_ctx* ctx, const uint8_t* d_bytes, uint64_t nbytes, c
                d_labels, ctx->d_err);
   exclusive_offsets(ctx, d_uih_len, n, d_offsets, scan_scratch(ctx), s);
   if (d_values && n)
-    FSX_LAUNCH(ctx, k_rec_uih, grid_for(ctx, n * 32, 256, 8), 256, 0, s, d_bytes, d_rec_off, n, d_offsets,
-               d_values, cap, ctx->d_err);
+    FSX_LAUNCH(ctx, k_rec_ids, static_cast<unsigned>(ctx->num_sms) * 6, kIdThreads, 0, s, d_bytes, d_rec_off, n,
+               d_offsets, d_values, cap, ctx->d_err);
   // one host sync: the error word and the id total together
   uint64_t tot = 0;
   FSX_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->d_err, sizeof(DevErr), cudaMemcpyDeviceToHost, s));
