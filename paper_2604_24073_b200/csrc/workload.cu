@@ -107,14 +107,28 @@ __device__ __forceinline__ uint64_t record_of(const uint64_t* offs, uint64_t lo,
   return lo;
 }
 
+// tile_first[t] = the record holding output id t * kIdTile (each tile boundary
+// lies in exactly one non-empty record: thread per record, no search);
+// tile_first[tiles] = n - 1 closes the last tile's record range
+__global__ void k_tile_first(const uint64_t* __restrict__ offs, uint64_t n, uint64_t* __restrict__ tile_first) {
+  FSX_PDL_ENTER();
+  const uint64_t total = offs[n];
+  for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r < n;
+       r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t lo = offs[r], hi = offs[r + 1];
+    for (uint64_t t = (lo + kIdTile - 1) / kIdTile; t * kIdTile < hi; ++t) tile_first[t] = r;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && n) tile_first[(total + kIdTile - 1) / kIdTile] = n - 1;
+}
+
 __global__ void __launch_bounds__(kIdThreads) k_rec_ids(const uint8_t* __restrict__ bytes,
                                                         const uint64_t* __restrict__ rec_off, uint64_t n,
-                                                        const uint64_t* __restrict__ offs, uint64_t* __restrict__ values,
-                                                        uint64_t cap, DevErr* err) {
+                                                        const uint64_t* __restrict__ offs,
+                                                        const uint64_t* __restrict__ tile_first,
+                                                        uint64_t* __restrict__ values, uint64_t cap, DevErr* err) {
   FSX_PDL_ENTER();
   __shared__ uint64_t sh_off[kIdTile + 1];
   __shared__ uint64_t sh_src[kIdTile];
-  __shared__ uint64_t sh_r[2];
   const uint64_t total = offs[n];
   if (total > cap) {  // never write past the caller's buffer
     if (blockIdx.x == 0 && threadIdx.x == 0) report(err, kErrIdCapacity, total, cap);
@@ -123,9 +137,10 @@ __global__ void __launch_bounds__(kIdThreads) k_rec_ids(const uint8_t* __restric
   for (uint64_t b = static_cast<uint64_t>(blockIdx.x) * kIdTile; b < total;
        b += static_cast<uint64_t>(gridDim.x) * kIdTile) {
     const uint64_t e = min(total, b + kIdTile);
-    if (threadIdx.x < 2) sh_r[threadIdx.x] = record_of(offs, 0, n, threadIdx.x == 0 ? b : e - 1);
-    __syncthreads();
-    const uint64_t r0 = sh_r[0], cnt = sh_r[1] - r0 + 1;
+    // records [tile_first[t], tile_first[t + 1]] cover the tile (a superset when
+    // the next tile's first record starts exactly at e: searches never pick it)
+    const uint64_t t = b / kIdTile;
+    const uint64_t r0 = tile_first[t], cnt = tile_first[t + 1] - r0 + 1;
     if (cnt <= kIdTile) {
       for (uint64_t k = threadIdx.x; k < cnt; k += kIdThreads) {
         sh_off[k] = offs[r0 + k];
@@ -163,11 +178,11 @@ __global__ void __launch_bounds__(kIdThreads) k_rec_ids(const uint8_t* __restric
 
 // offsets-scan scratch per (context, device), kept across iterations (a
 // cudaMalloc / cudaFree pair per call would serialise the device)
-DevBuf<uint64_t>& scan_scratch(const Ctx* ctx) {
+DevBuf<uint64_t>& scan_scratch(const Ctx* ctx, int which) {
   static std::mutex m;
   static std::unordered_map<uint64_t, DevBuf<uint64_t>>* bufs = new std::unordered_map<uint64_t, DevBuf<uint64_t>>();
   std::lock_guard<std::mutex> g(m);
-  return (*bufs)[reinterpret_cast<uintptr_t>(ctx) ^ (static_cast<uint64_t>(ctx->device) << 56)];
+  return (*bufs)[(reinterpret_cast<uintptr_t>(ctx) ^ (static_cast<uint64_t>(ctx->device) << 56)) * 2 + which];
 }
 
 uint32_t host_u32(const uint8_t* p) {
@@ -227,10 +242,14 @@ int fsx_workload_decode(fsx_ctx* ctx, const uint8_t* d_bytes, uint64_t nbytes, c
   if (n)
     FSX_LAUNCH(ctx, k_rec_parse, grid_for(ctx, n, 256, 8), 256, 0, s, d_bytes, nbytes, d_rec_off, n, d_uih_len,
                d_labels, ctx->d_err);
-  exclusive_offsets(ctx, d_uih_len, n, d_offsets, scan_scratch(ctx), s);
-  if (d_values && n)
+  exclusive_offsets(ctx, d_uih_len, n, d_offsets, scan_scratch(ctx, 0), s);
+  if (d_values && n) {
+    DevBuf<uint64_t>& tf = scan_scratch(ctx, 1);
+    tf.ensure(nbytes / 8 / kIdTile + 2);  // ids <= nbytes / 8
+    FSX_LAUNCH(ctx, k_tile_first, grid_for(ctx, n, 256, 8), 256, 0, s, d_offsets, n, tf.p);
     FSX_LAUNCH(ctx, k_rec_ids, static_cast<unsigned>(ctx->num_sms) * 6, kIdThreads, 0, s, d_bytes, d_rec_off, n,
-               d_offsets, d_values, cap, ctx->d_err);
+               d_offsets, tf.p, d_values, cap, ctx->d_err);
+  }
   // one host sync: the error word and the id total together
   uint64_t tot = 0;
   FSX_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->d_err, sizeof(DevErr), cudaMemcpyDeviceToHost, s));
