@@ -25,6 +25,7 @@ namespace freescale {
     case FSX_ERR_PROTOCOL: throw ProtocolError(msg);
     case FSX_ERR_COLLECTIVE: throw CollectiveError(msg);
     case FSX_ERR_CONFIG: throw ConfigError(msg);
+    case FSX_ERR_IO: throw IoError(msg);
     default: throw std::runtime_error(msg);
   }
 }
