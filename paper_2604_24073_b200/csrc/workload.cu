@@ -91,9 +91,9 @@ __global__ void k_rec_parse(const uint8_t* __restrict__ bytes, uint64_t nbytes, 
 
 // UIH id mover, flattened over the output ids so a 8,192-id record does not
 // serialise one warp (the power-law tail): a CTA takes 2,048 consecutive
-// output ids, finds the records that cover them (two binary searches over the
-// offsets), stages those records' offsets in shared memory, and each thread
-// resolves its id's record by a shared-memory binary search. Reads (4-byte
+// output ids, takes the records that cover them from the tile-first table,
+// paints each id's record index into shared memory (warp per record) and then
+// moves its ids with 8 loads in flight per thread. Reads (4-byte
 // aligned u64 pairs in the file) and writes are coalesced over the tile.
 constexpr int kIdTile = 2048;
 constexpr int kIdThreads = 256;
@@ -127,8 +127,8 @@ __global__ void __launch_bounds__(kIdThreads) k_rec_ids(const uint8_t* __restric
                                                         const uint64_t* __restrict__ tile_first,
                                                         uint64_t* __restrict__ values, uint64_t cap, DevErr* err) {
   FSX_PDL_ENTER();
-  __shared__ uint64_t sh_off[kIdTile + 1];
-  __shared__ uint64_t sh_src[kIdTile];
+  __shared__ uint16_t sh_rec[kIdTile];
+  __shared__ uint64_t sh_base[kIdTile];
   const uint64_t total = offs[n];
   if (total > cap) {  // never write past the caller's buffer
     if (blockIdx.x == 0 && threadIdx.x == 0) report(err, kErrIdCapacity, total, cap);
@@ -142,22 +142,22 @@ __global__ void __launch_bounds__(kIdThreads) k_rec_ids(const uint8_t* __restric
     const uint64_t t = b / kIdTile;
     const uint64_t r0 = tile_first[t], cnt = tile_first[t + 1] - r0 + 1;
     if (cnt <= kIdTile) {
-      for (uint64_t k = threadIdx.x; k < cnt; k += kIdThreads) {
-        sh_off[k] = offs[r0 + k];
-        sh_src[k] = rec_off[r0 + k] + 4;
+      // paint: sh_rec[id - b] = the id's record (warp per record, lanes over its
+      // ids inside the tile); sh_base[k] turns an id into its byte address
+      const unsigned warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+      for (uint64_t k = warp; k < cnt; k += kIdThreads / 32) {
+        const uint64_t lo = offs[r0 + k], hi = offs[r0 + k + 1];
+        if (lane == 0) sh_base[k] = rec_off[r0 + k] + 4 - 8 * lo;  // mod 2^64
+        const uint64_t x1 = min(hi, e);
+        for (uint64_t x = max(lo, b) + lane; x < x1; x += 32) sh_rec[x - b] = static_cast<uint16_t>(k);
       }
       __syncthreads();
-      // resolve all of this thread's ids first, then keep their loads in flight together
       constexpr int kPer = kIdTile / kIdThreads;
       const uint8_t* src[kPer];
 #pragma unroll
       for (int j = 0; j < kPer; ++j) {
         const uint64_t i = b + threadIdx.x + static_cast<uint64_t>(j) * kIdThreads;
-        src[j] = nullptr;
-        if (i < e) {
-          const uint64_t k = record_of(sh_off, 0, cnt, i);
-          src[j] = bytes + sh_src[k] + 8 * (i - sh_off[k]);
-        }
+        src[j] = i < e ? bytes + sh_base[sh_rec[i - b]] + 8 * i : nullptr;
       }
       uint64_t v[kPer];
 #pragma unroll
@@ -247,7 +247,7 @@ int fsx_workload_decode(fsx_ctx* ctx, const uint8_t* d_bytes, uint64_t nbytes, c
     DevBuf<uint64_t>& tf = scan_scratch(ctx, 1);
     tf.ensure(nbytes / 8 / kIdTile + 2);  // ids <= nbytes / 8
     FSX_LAUNCH(ctx, k_tile_first, grid_for(ctx, n, 256, 8), 256, 0, s, d_offsets, n, tf.p);
-    FSX_LAUNCH(ctx, k_rec_ids, static_cast<unsigned>(ctx->num_sms) * 6, kIdThreads, 0, s, d_bytes, d_rec_off, n,
+    FSX_LAUNCH(ctx, k_rec_ids, static_cast<unsigned>(ctx->num_sms) * 8, kIdThreads, 0, s, d_bytes, d_rec_off, n,
                d_offsets, tf.p, d_values, cap, ctx->d_err);
   }
   // one host sync: the error word and the id total together
