@@ -78,9 +78,22 @@ for _ in range(10):
     ms.append(e0.elapsed_time(e1))
 assert np.array_equal(d_vals[:tot.value].cpu().numpy().view(np.uint64), ids)
 med = float(np.median(ms))
+# the reference's own Reader on the same file (oracle/_ref, one host thread), per iteration
+cpu = None
+try:
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle"))
+    from oracle import Reference
+    if Reference.available():
+        R = Reference()
+        t0 = time.perf_counter()
+        R.load_workload(path)
+        cpu = {"kind": "reference", "cores": 1, "ms_per_iteration": round(1e3 * (time.perf_counter() - t0) / 8, 3),
+               "sample": "workload::load_workload of the same 8-iteration file"}
+except Exception as e:  # noqa: BLE001 — a reported baseline, not the measured path
+    cpu = {"unavailable": str(e)}
 print(json.dumps({"what": "workload replay, cfg2 shape (8 ranks x 8192 samples)", "record_bytes": used,
                   "ids": int(tot.value), "decode_ms": round(med, 4),
                   "decode_GBps_record_bytes": round(used / med / 1e6, 1),
                   "decode_GBps_moved": round((used + 8 * tot.value) / med / 1e6, 1),
                   "next_iteration_ms_median": round(1e3 * float(np.median(t[2:])), 3),
-                  "note": "decode includes 3 host syncs (error word, id total, end)"}))
+                  "note": "decode includes one host sync (error word + id total)", "cpu_baseline": cpu}))
