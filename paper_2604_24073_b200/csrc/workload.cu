@@ -14,7 +14,10 @@
 //   GPU   fsx_workload_decode one thread per record parses the record body
 //                             (uih count, candidate lists, label) and checks
 //                             it is consumed exactly (the reference's trailing
-//                             bytes IoError); u64 offsets scan; the UIH ids
+//                             bytes IoError) and sums its CTA's lengths; a
+//                             warp scans the tile sums; the offsets kernel
+//                             also marks which record opens each id tile; the
+//                             UIH ids
 //                             (4-byte aligned in the file, 8-byte aligned in
 //                             HBM) move flattened over the output, 2,048 per
 //                             CTA tile, coalesced on both sides.
@@ -31,9 +34,6 @@
 
 namespace fsx {
 
-void exclusive_offsets(Ctx* ctx, const uint64_t* len, uint64_t n, uint64_t* offs, DevBuf<uint64_t>& scratch,
-                       cudaStream_t s);
-
 namespace {
 
 constexpr int kErrRecTruncated = 101;  // a = record, b = iteration-local index
@@ -47,18 +47,43 @@ __device__ __forceinline__ uint64_t ld_u64_a4(const uint8_t* p) {
   return static_cast<uint64_t>(ld_u32(p)) | (static_cast<uint64_t>(ld_u32(p + 4)) << 32);
 }
 
+// UIH id mover, flattened over the output ids so a 8,192-id record does not
+// serialise one warp (the power-law tail): a CTA takes 2,048 consecutive
+// output ids, takes the records that cover them from the tile-first table,
+// paints each id's record index into shared memory (warp per record) and then
+// moves its ids with 8 loads in flight per thread. Reads (4-byte
+// aligned u64 pairs in the file) and writes are coalesced over the tile.
+constexpr int kIdTile = 2048;
+constexpr int kIdThreads = 256;
+
+constexpr int kRecTile = 256;  // records per CTA in the parse / offsets kernels
+
+__device__ __forceinline__ uint64_t block_sum_u64(uint64_t v) {
+  __shared__ uint64_t ws[kRecTile / 32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+  __syncthreads();
+  uint64_t t = 0;
+#pragma unroll
+  for (int w = 0; w < kRecTile / 32; ++w) t += ws[w];
+  return t;
+}
+
 // decode_sample (workload.cpp:405-418) without materialising the candidates:
-// uih length + label out, exact-consumption check
-__global__ void k_rec_parse(const uint8_t* __restrict__ bytes, uint64_t nbytes, const uint64_t* __restrict__ rec_off,
-                            uint64_t n, uint64_t* __restrict__ uih_len, double* __restrict__ labels,
-                            DevErr* err) { FSX_PDL_ENTER();
-  for (uint64_t s = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; s < n;
-       s += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+// thread per record, uih length + label out, exact-consumption check; the
+// CTA's length sum goes to tile_sums for the offsets scan
+__global__ void __launch_bounds__(kRecTile) k_rec_parse(const uint8_t* __restrict__ bytes,
+                                                        const uint64_t* __restrict__ rec_off, uint64_t n,
+                                                        uint64_t* __restrict__ uih_len, double* __restrict__ labels,
+                                                        uint64_t* __restrict__ tile_sums, DevErr* err) {
+  FSX_PDL_ENTER();
+  const uint64_t s = static_cast<uint64_t>(blockIdx.x) * kRecTile + threadIdx.x;
+  uint64_t nu = 0;
+  if (s < n) {
     const uint64_t off = rec_off[s];
     const uint64_t end = off + ld_u32(bytes + off - 4);  // scan checked end <= nbytes
     uint64_t pos = off;
     bool ok = pos + 4 <= end;
-    uint64_t nu = 0;
     if (ok) {
       nu = ld_u32(bytes + pos);
       pos += 4 + 8 * nu;
@@ -75,28 +100,70 @@ __global__ void k_rec_parse(const uint8_t* __restrict__ bytes, uint64_t nbytes, 
     }
     if (!ok) {
       report(err, kErrRecTruncated, s, 0);
-      uih_len[s] = 0;
-      continue;
-    }
-    pos += 8;
-    if (pos != end) {
+      nu = 0;
+    } else if (pos + 8 != end) {
       report(err, kErrRecTrailing, s, 0);
-      uih_len[s] = 0;
-      continue;
+      nu = 0;
+    } else if (labels) {
+      labels[s] = __longlong_as_double(static_cast<long long>(ld_u64_a4(bytes + pos)));
     }
     uih_len[s] = nu;
-    if (labels) labels[s] = __longlong_as_double(static_cast<long long>(ld_u64_a4(bytes + pos - 8)));
+  }
+  const uint64_t t = block_sum_u64(nu);
+  if (threadIdx.x == 0) tile_sums[blockIdx.x] = t;
+}
+
+// one warp: exclusive scan of the tile sums in place; offs[n] = total and the
+// closing tile_first entry (tile_first[ceil(total / kIdTile)] = n - 1)
+__global__ void k_rec_scan_tiles(uint64_t* tile_sums, uint64_t tiles, uint64_t n, uint64_t* __restrict__ offs,
+                                 uint64_t* __restrict__ tile_first) {
+  FSX_PDL_ENTER();
+  const unsigned lane = threadIdx.x & 31u;
+  uint64_t carry = 0;
+  for (uint64_t t0 = 0; t0 < tiles; t0 += 32) {
+    const uint64_t t = t0 + lane;
+    const uint64_t v = t < tiles ? tile_sums[t] : 0;
+    uint64_t x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= static_cast<unsigned>(o)) x += y;
+    }
+    if (t < tiles) tile_sums[t] = carry + x - v;
+    carry += __shfl_sync(0xffffffffu, x, 31);
+  }
+  if (lane == 0) {
+    offs[n] = carry;
+    if (tile_first) tile_first[(carry + kIdTile - 1) / kIdTile] = n - 1;
   }
 }
 
-// UIH id mover, flattened over the output ids so a 8,192-id record does not
-// serialise one warp (the power-law tail): a CTA takes 2,048 consecutive
-// output ids, takes the records that cover them from the tile-first table,
-// paints each id's record index into shared memory (warp per record) and then
-// moves its ids with 8 loads in flight per thread. Reads (4-byte
-// aligned u64 pairs in the file) and writes are coalesced over the tile.
-constexpr int kIdTile = 2048;
-constexpr int kIdThreads = 256;
+// offsets = tile prefix + block exclusive scan of the lengths; each record also
+// writes tile_first[t] for every id-tile boundary t * kIdTile it holds
+__global__ void __launch_bounds__(kRecTile) k_rec_offsets(const uint64_t* __restrict__ uih_len, uint64_t n,
+                                                          const uint64_t* __restrict__ tile_sums,
+                                                          uint64_t* __restrict__ offs,
+                                                          uint64_t* __restrict__ tile_first) {
+  FSX_PDL_ENTER();
+  __shared__ uint64_t ws[kRecTile / 32];
+  const uint64_t s = static_cast<uint64_t>(blockIdx.x) * kRecTile + threadIdx.x;
+  const uint64_t v = s < n ? uih_len[s] : 0;
+  const unsigned lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint64_t x = v;
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= static_cast<unsigned>(o)) x += y;
+  }
+  if (lane == 31) ws[warp] = x;
+  __syncthreads();
+  uint64_t lo = tile_sums[blockIdx.x] + x - v;
+  for (unsigned w = 0; w < warp; ++w) lo += ws[w];
+  if (s < n) {
+    offs[s] = lo;
+    if (tile_first)
+      for (uint64_t t = (lo + kIdTile - 1) / kIdTile; t * kIdTile < lo + v; ++t) tile_first[t] = s;
+  }
+}
+
 
 __device__ __forceinline__ uint64_t record_of(const uint64_t* offs, uint64_t lo, uint64_t hi, uint64_t x) {
   // last r in [lo, hi) with offs[r] <= x (offs nondecreasing, offs[lo] <= x)
@@ -105,20 +172,6 @@ __device__ __forceinline__ uint64_t record_of(const uint64_t* offs, uint64_t lo,
     if (offs[mid] <= x) lo = mid; else hi = mid;
   }
   return lo;
-}
-
-// tile_first[t] = the record holding output id t * kIdTile (each tile boundary
-// lies in exactly one non-empty record: thread per record, no search);
-// tile_first[tiles] = n - 1 closes the last tile's record range
-__global__ void k_tile_first(const uint64_t* __restrict__ offs, uint64_t n, uint64_t* __restrict__ tile_first) {
-  FSX_PDL_ENTER();
-  const uint64_t total = offs[n];
-  for (uint64_t r = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; r < n;
-       r += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t lo = offs[r], hi = offs[r + 1];
-    for (uint64_t t = (lo + kIdTile - 1) / kIdTile; t * kIdTile < hi; ++t) tile_first[t] = r;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0 && n) tile_first[(total + kIdTile - 1) / kIdTile] = n - 1;
 }
 
 __global__ void __launch_bounds__(kIdThreads) k_rec_ids(const uint8_t* __restrict__ bytes,
@@ -239,16 +292,25 @@ int fsx_workload_decode(fsx_ctx* ctx, const uint8_t* d_bytes, uint64_t nbytes, c
   FSX_API_BEGIN
   DeviceGuard dg(ctx->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (n)
-    FSX_LAUNCH(ctx, k_rec_parse, grid_for(ctx, n, 256, 8), 256, 0, s, d_bytes, nbytes, d_rec_off, n, d_uih_len,
-               d_labels, ctx->d_err);
-  exclusive_offsets(ctx, d_uih_len, n, d_offsets, scan_scratch(ctx, 0), s);
-  if (d_values && n) {
-    DevBuf<uint64_t>& tf = scan_scratch(ctx, 1);
-    tf.ensure(nbytes / 8 / kIdTile + 2);  // ids <= nbytes / 8
-    FSX_LAUNCH(ctx, k_tile_first, grid_for(ctx, n, 256, 8), 256, 0, s, d_offsets, n, tf.p);
-    FSX_LAUNCH(ctx, k_rec_ids, static_cast<unsigned>(ctx->num_sms) * 8, kIdThreads, 0, s, d_bytes, d_rec_off, n,
-               d_offsets, tf.p, d_values, cap, ctx->d_err);
+  if (n) {
+    const uint64_t tiles = (n + kRecTile - 1) / kRecTile;
+    DevBuf<uint64_t>& ts = scan_scratch(ctx, 0);
+    ts.ensure(tiles);
+    uint64_t* tf = nullptr;
+    if (d_values) {
+      DevBuf<uint64_t>& tfb = scan_scratch(ctx, 1);
+      tfb.ensure(nbytes / 8 / kIdTile + 2);  // ids <= nbytes / 8
+      tf = tfb.p;
+    }
+    FSX_LAUNCH(ctx, k_rec_parse, static_cast<unsigned>(tiles), kRecTile, 0, s, d_bytes, d_rec_off, n, d_uih_len,
+               d_labels, ts.p, ctx->d_err);
+    FSX_LAUNCH(ctx, k_rec_scan_tiles, 1, 32, 0, s, ts.p, tiles, n, d_offsets, tf);
+    FSX_LAUNCH(ctx, k_rec_offsets, static_cast<unsigned>(tiles), kRecTile, 0, s, d_uih_len, n, ts.p, d_offsets, tf);
+    if (d_values)
+      FSX_LAUNCH(ctx, k_rec_ids, static_cast<unsigned>(ctx->num_sms) * 8, kIdThreads, 0, s, d_bytes, d_rec_off, n,
+                 d_offsets, tf, d_values, cap, ctx->d_err);
+  } else {
+    FSX_CUDA(cudaMemsetAsync(d_offsets, 0, sizeof(uint64_t), s));
   }
   // one host sync: the error word and the id total together
   uint64_t tot = 0;
