@@ -227,15 +227,18 @@ static uint64_t shard_unique(int world, const uint64_t* ids, uint64_t n, int s, 
  * init and after every update, and the caller's gradient fixture is evaluated
  * in float arithmetic (g = fl(fl(scale*row) + shift), as a float32 tensor op
  * would); sums and the update itself stay f64, exactly as the reference. */
-int fso_run_engine_ex(int world, int iters, const uint64_t* ids, const uint64_t* lens,
-                      uint64_t total_rows, uint32_t dim, double lr, uint64_t seed, double grad_scale,
-                      double grad_shift, double* table, uint64_t* stats_out, int store_f32);
-
 int fso_run_engine(int world, int iters, const uint64_t* ids, const uint64_t* lens,
                    uint64_t total_rows, uint32_t dim, double lr, uint64_t seed, double grad_scale,
                    double grad_shift, double* table, uint64_t* stats_out) {
-  return fso_run_engine_ex(world, iters, ids, lens, total_rows, dim, lr, seed, grad_scale, grad_shift,
-                           table, stats_out, 0);
+  return fso_run_engine_ex2(world, iters, ids, lens, total_rows, dim, lr, seed, grad_scale, grad_shift,
+                            table, stats_out, 0, 0, 0);
+}
+
+int fso_run_engine_ex(int world, int iters, const uint64_t* ids, const uint64_t* lens,
+                      uint64_t total_rows, uint32_t dim, double lr, uint64_t seed, double grad_scale,
+                      double grad_shift, double* table, uint64_t* stats_out, int store_f32) {
+  return fso_run_engine_ex2(world, iters, ids, lens, total_rows, dim, lr, seed, grad_scale, grad_shift,
+                            table, stats_out, store_f32, 0, 0);
 }
 
 static double fixture(double row, double scale, double shift, int f32) {
@@ -245,9 +248,41 @@ static double fixture(double row, double scale, double shift, int f32) {
   return (double)b;
 }
 
-int fso_run_engine_ex(int world, int iters, const uint64_t* ids, const uint64_t* lens,
-                      uint64_t total_rows, uint32_t dim, double lr, uint64_t seed, double grad_scale,
-                      double grad_shift, double* table, uint64_t* stats_out, int store_f32) {
+/* The engine's fixed association of one row's gradient sum (the product's
+ * SgdPlanOp / k_sgd_* kernels; not a reference choice — the reference's
+ * embedding.cpp:165-168 is the chunk == 0 case): occurrences q[0..n) in their
+ * given order are left-folded from 0.0 when chunk == 0 or n <= chunk;
+ * otherwise each run of `chunk` consecutive occurrences is left-folded from
+ * 0.0 and the chunk sums are left-folded from 0.0 in chunk order. */
+static double chunk_fold(const occ_t* q, uint64_t n, uint32_t d, uint32_t dim, const double* served,
+                         double scale, double shift, int f32, uint32_t chunk) {
+  if (chunk == 0 || n <= chunk) {
+    double acc = 0.0;
+    for (uint64_t k = 0; k < n; ++k) acc += fixture(served[q[k].seq * dim + d], scale, shift, f32);
+    return acc;
+  }
+  double acc = 0.0;
+  for (uint64_t c0 = 0; c0 < n; c0 += chunk) {
+    double part = 0.0;
+    uint64_t c1 = c0 + chunk < n ? c0 + chunk : n;
+    for (uint64_t k = c0; k < c1; ++k) part += fixture(served[q[k].seq * dim + d], scale, shift, f32);
+    acc += part;
+  }
+  return acc;
+}
+
+/* reduce_chunk: see chunk_fold. presum (world > 1 only): a row of iteration
+ * i (0 < i < iters-1) that iteration i+1 also touches — a collision row,
+ * embedding.cpp:82-93 — is summed as the engine's PRESUM protocol does:
+ * each source rank's occurrences of the row (position order) are chunk-folded
+ * and rounded to the table type (the requester's pre-summed CO_G row), then
+ * those per-source rows are left-folded from 0.0 in source-rank order (the
+ * owner's k_co_apply). Every other row: one chunk_fold over all occurrences
+ * in (source rank, position) order. */
+int fso_run_engine_ex2(int world, int iters, const uint64_t* ids, const uint64_t* lens,
+                       uint64_t total_rows, uint32_t dim, double lr, uint64_t seed, double grad_scale,
+                       double grad_shift, double* table, uint64_t* stats_out, int store_f32,
+                       uint32_t reduce_chunk, int presum) {
   for (uint64_t g = 0; g < total_rows; ++g)
     for (uint32_t d = 0; d < dim; ++d) {
       double v = fso_initial_value(seed, g, d);
@@ -345,9 +380,21 @@ int fso_run_engine_ex(int world, int iters, const uint64_t* ids, const uint64_t*
 
   occ_t* occ = malloc((maxn + 1) * sizeof(occ_t));
   double* served = malloc(((size_t)maxn * dim + 1) * 8);
+  uint64_t* nxt_u = malloc((maxn + 1) * 8);
+  uint64_t* src_end = malloc(((size_t)world + 1) * 8);
   for (int i = 0; i < iters; ++i) {
     const uint64_t* cur = ids + it_start[i];
     uint64_t n = it_start[i + 1] - it_start[i];
+    /* collision rows of (i, i+1) for the PRESUM association */
+    const int split_co = presum && world > 1 && i > 0 && i + 1 < iters;
+    uint64_t nnu = 0;
+    if (split_co) {
+      nnu = it_start[i + 2] - it_start[i + 1];
+      memcpy(nxt_u, ids + it_start[i + 1], nnu * 8);
+      nnu = fso_sorted_unique(nxt_u, nnu);
+    }
+    uint64_t at2 = 0;
+    for (int r = 0; r < world; ++r) { at2 += lens[i * world + r]; src_end[r] = at2; }
     /* forward: all lookups see the table after iteration i-1 */
     for (uint64_t j = 0; j < n; ++j) memcpy(served + j * dim, table + cur[j] * dim, (size_t)dim * 8);
     /* backward: seq = flat (rank, position) order; stable per-row sums */
@@ -358,20 +405,36 @@ int fso_run_engine_ex(int world, int iters, const uint64_t* ids, const uint64_t*
       uint64_t e = k;
       while (e < n && occ[e].id == occ[k].id) ++e;
       double* row = table + occ[k].id * dim;
+      const int co_row = split_co && member(nxt_u, nnu, occ[k].id);
       for (uint32_t d = 0; d < dim; ++d) {
         double acc = 0.0;
-        for (uint64_t q = k; q < e; ++q) acc += fixture(served[occ[q].seq * dim + d], grad_scale, grad_shift, store_f32);
+        if (!co_row) {
+          acc = chunk_fold(occ + k, e - k, d, dim, served, grad_scale, grad_shift, store_f32, reduce_chunk);
+        } else {
+          /* occurrences are in seq order, so each source's run is contiguous */
+          uint64_t q = k;
+          for (int src = 0; src < world && q < e; ++src) {
+            uint64_t q1 = q;
+            while (q1 < e && occ[q1].seq < src_end[src]) ++q1;
+            if (q1 == q) continue;
+            double ps = chunk_fold(occ + q, q1 - q, d, dim, served, grad_scale, grad_shift, store_f32,
+                                   reduce_chunk);
+            if (store_f32) ps = (double)(float)ps;
+            acc += ps;
+            q = q1;
+          }
+        }
         row[d] -= lr * acc;
         if (store_f32) row[d] = (double)(float)row[d];
         if (!isfinite(row[d])) {
-          free(occ); free(served); free(it_start);
+          free(occ); free(served); free(it_start); free(nxt_u); free(src_end);
           return fail(FSO_DOMAIN, "embedding: non-finite value after update of row %llu%.0llu", occ[k].id, 0);
         }
       }
       k = e;
     }
   }
-  free(occ); free(served); free(it_start);
+  free(occ); free(served); free(it_start); free(nxt_u); free(src_end);
   return FSO_OK;
 }
 

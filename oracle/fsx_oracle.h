@@ -57,6 +57,13 @@ int fso_run_engine_ex(int world, int iters, const uint64_t* ids, const uint64_t*
                       uint64_t total_rows, uint32_t dim, double lr, uint64_t seed, double grad_scale,
                       double grad_shift, double* table_out, uint64_t* stats_out, int store_f32);
 
+/* + the engine's fixed chunk association (reduce_chunk) and its PRESUM
+ * two-level association of collision rows (presum); see fsx_oracle.c */
+int fso_run_engine_ex2(int world, int iters, const uint64_t* ids, const uint64_t* lens,
+                       uint64_t total_rows, uint32_t dim, double lr, uint64_t seed, double grad_scale,
+                       double grad_shift, double* table_out, uint64_t* stats_out, int store_f32,
+                       uint32_t reduce_chunk, int presum);
+
 int fso_fbs(const uint64_t* lens, const int* origin, const int* local, uint64_t m, int n,
             int* assignment, uint64_t* order, uint64_t* order_lens);
 int fso_vbs(const uint64_t* lens, const int* origin, const int* local, uint64_t m, int n,

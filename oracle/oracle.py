@@ -194,20 +194,25 @@ class Oracle(_Lib):
         return values.reshape(-1, dim) if dim else values, uq[:u], rows[:u * dim].reshape(u, dim)
 
     def run_engine(self, world, batches_per_iter, total_rows, dim, lr, seed,
-                   grad_scale=0.125, grad_shift=0.0625, with_stats=False, store_f32=False):
+                   grad_scale=0.125, grad_shift=0.0625, with_stats=False, store_f32=False,
+                   reduce_chunk=0, presum=False):
         """batches_per_iter[i][r] = id array. Returns (table [rows x dim], stats or None).
-        store_f32: model an fp32 table (fso_run_engine_ex)."""
+        store_f32: model an fp32 table; reduce_chunk / presum: the engine's
+        fixed chunk association and PRESUM two-level association
+        (fso_run_engine_ex2)."""
         iters = len(batches_per_iter)
         lens = _u64([len(b) for it in batches_per_iter for b in it])
         flat = [_u64(b) for it in batches_per_iter for b in it]
         ids = _u64(np.concatenate(flat)) if flat else _u64([])
         table = np.zeros(max(total_rows * dim, 1), np.float64)
         stats = np.zeros(max(3 * iters, 1), np.uint64)
-        f = self._fn("run_engine_ex", [C.c_int, C.c_int, u64p, u64p, C.c_uint64, C.c_uint32, C.c_double,
-                                       C.c_uint64, C.c_double, C.c_double, f64p, C.c_void_p, C.c_int])
+        f = self._fn("run_engine_ex2", [C.c_int, C.c_int, u64p, u64p, C.c_uint64, C.c_uint32, C.c_double,
+                                        C.c_uint64, C.c_double, C.c_double, f64p, C.c_void_p, C.c_int,
+                                        C.c_uint32, C.c_int])
         self._check(f(world, iters, ids if ids.size else np.zeros(1, np.uint64), lens if lens.size else
                       np.zeros(1, np.uint64), total_rows, dim, lr, seed, grad_scale, grad_shift, table,
-                      stats.ctypes.data if with_stats else None, int(store_f32)))
+                      stats.ctypes.data if with_stats else None, int(store_f32), int(reduce_chunk),
+                      int(presum)))
         return table[:total_rows * dim].reshape(total_rows, dim), (stats[:3 * iters].reshape(iters, 3)
                                                                     if with_stats else None)
 

@@ -595,9 +595,13 @@ struct Engine {
       FSX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       ev_pool.push_back(e);
     }
+    // Handles kept across an iteration (ev_merged, ev_next_ready, the deferred
+    // split, ev_pack) are waited on after both host threads recorded up to
+    // ~20 + 8p more events; the ring must not wrap within that window.
+    const size_t ring = std::max<size_t>(256, 128 * static_cast<size_t>(p));
     cudaEvent_t e = ev_pool[ev_next];
-    ev_next = (ev_next + 1) % 256;
-    if (ev_pool.size() < 256 && ev_next == 0) ev_next = ev_pool.size();
+    ev_next = (ev_next + 1) % ring;
+    if (ev_pool.size() < ring && ev_next == 0) ev_next = ev_pool.size();
     FSX_CUDA(cudaEventRecord(e, s));
     return e;
   }

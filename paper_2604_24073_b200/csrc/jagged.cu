@@ -6,6 +6,8 @@
 //
 // Layout: values = one contiguous array of `elem_bytes`-sized elements,
 // offsets = u64 [n + 1] exclusive prefix of the lengths (offsets[n] = total).
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "capi_util.cuh"
@@ -163,6 +165,22 @@ using namespace fsx;
 
 namespace {
 cudaStream_t JS(void* s) { return static_cast<cudaStream_t>(s); }
+
+// offsets-scan scratch per (context, device), reused across calls: a local
+// buffer meant a cudaMalloc / cudaFree pair per call, and cudaFree
+// synchronises the whole device (stalling the engine's lanes mid-training,
+// balancer stage 3). The lock covers a call's use of it (every call ends
+// with a stream sync before its scratch is free again).
+struct JagScratch {
+  std::mutex m;
+  DevBuf<uint64_t> buf;
+};
+JagScratch& jag_scratch(const Ctx* ctx) {
+  static std::mutex m;
+  static auto* bufs = new std::unordered_map<uint64_t, JagScratch>();
+  std::lock_guard<std::mutex> g(m);
+  return (*bufs)[reinterpret_cast<uintptr_t>(ctx) ^ (static_cast<uint64_t>(ctx->device) << 56)];
+}
 }  // namespace
 
 extern "C" {
@@ -172,8 +190,9 @@ int fsx_jagged_offsets(fsx_ctx* ctx, const uint64_t* d_lengths, uint64_t n, uint
   FSX_API_BEGIN
   DeviceGuard dg(ctx->device);
   cudaStream_t s = JS(stream);
-  DevBuf<uint64_t> scratch;
-  exclusive_offsets(ctx, d_lengths, n, d_offsets, scratch, s);
+  JagScratch& js = jag_scratch(ctx);
+  std::lock_guard<std::mutex> lk(js.m);
+  exclusive_offsets(ctx, d_lengths, n, d_offsets, js.buf, s);
   uint64_t tot = 0;
   FSX_CUDA(cudaMemcpyAsync(&tot, d_offsets + n, 8, cudaMemcpyDeviceToHost, s));
   FSX_CUDA(cudaStreamSynchronize(s));
@@ -194,8 +213,9 @@ int fsx_jagged_permute(fsx_ctx* ctx, const void* d_values, uint32_t elem_bytes, 
                d_out_lengths, ctx->d_err);
   }
   ctx->check_error(s);  // out-of-range index: the reference throws before moving anything
-  DevBuf<uint64_t> scratch;
-  exclusive_offsets(ctx, d_out_lengths, n_perm, d_out_offsets, scratch, s);
+  JagScratch& js = jag_scratch(ctx);
+  std::lock_guard<std::mutex> lk(js.m);
+  exclusive_offsets(ctx, d_out_lengths, n_perm, d_out_offsets, js.buf, s);
   uint64_t tot = 0;
   FSX_CUDA(cudaMemcpyAsync(&tot, d_out_offsets + n_perm, 8, cudaMemcpyDeviceToHost, s));
   FSX_CUDA(cudaStreamSynchronize(s));

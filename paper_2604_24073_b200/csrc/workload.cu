@@ -40,8 +40,14 @@ constexpr int kErrRecTruncated = 101;  // a = record, b = iteration-local index
 constexpr int kErrRecTrailing = 102;   // a = record
 constexpr int kErrIdCapacity = 103;    // a = ids, b = capacity
 
-__device__ __forceinline__ uint32_t ld_u32(const uint8_t* p) {  // little-endian, 4-byte aligned
-  return *reinterpret_cast<const uint32_t*>(p);
+// little-endian u32. Valid records are multiples of 4 bytes long, so every
+// field sits 4-byte aligned; a record of another length (always malformed,
+// the parse reports it) shifts the records behind it, which are then read
+// byte by byte instead of faulting with a misaligned access.
+__device__ __forceinline__ uint32_t ld_u32(const uint8_t* p) {
+  if ((reinterpret_cast<uintptr_t>(p) & 3u) == 0) return *reinterpret_cast<const uint32_t*>(p);
+  return static_cast<uint32_t>(p[0]) | (static_cast<uint32_t>(p[1]) << 8) | (static_cast<uint32_t>(p[2]) << 16) |
+         (static_cast<uint32_t>(p[3]) << 24);
 }
 __device__ __forceinline__ uint64_t ld_u64_a4(const uint8_t* p) {
   return static_cast<uint64_t>(ld_u32(p)) | (static_cast<uint64_t>(ld_u32(p + 4)) << 32);
@@ -75,7 +81,8 @@ __device__ __forceinline__ uint64_t block_sum_u64(uint64_t v) {
 __global__ void __launch_bounds__(kRecTile) k_rec_parse(const uint8_t* __restrict__ bytes,
                                                         const uint64_t* __restrict__ rec_off, uint64_t n,
                                                         uint64_t* __restrict__ uih_len, double* __restrict__ labels,
-                                                        uint64_t* __restrict__ tile_sums, DevErr* err) {
+                                                        uint64_t* __restrict__ tile_sums,
+                                                        unsigned long long* __restrict__ first_bad) {
   FSX_PDL_ENTER();
   const uint64_t s = static_cast<uint64_t>(blockIdx.x) * kRecTile + threadIdx.x;
   uint64_t nu = 0;
@@ -98,11 +105,13 @@ __global__ void __launch_bounds__(kRecTile) k_rec_parse(const uint8_t* __restric
       }
       ok = ok && pos + 8 <= end;
     }
+    // the reference decodes records in file order and raises at the first
+    // bad one: keep the smallest failing record (bit 0: trailing bytes)
     if (!ok) {
-      report(err, kErrRecTruncated, s, 0);
+      atomicMin(first_bad, static_cast<unsigned long long>(s) << 1);
       nu = 0;
     } else if (pos + 8 != end) {
-      report(err, kErrRecTrailing, s, 0);
+      atomicMin(first_bad, (static_cast<unsigned long long>(s) << 1) | 1ull);
       nu = 0;
     } else if (labels) {
       labels[s] = __longlong_as_double(static_cast<long long>(ld_u64_a4(bytes + pos)));
@@ -243,6 +252,25 @@ uint32_t host_u32(const uint8_t* p) {
          (static_cast<uint32_t>(p[3]) << 24);
 }
 
+// decode_sample's structure check of one record on the host (workload.cpp:
+// 405-418): 0 = decodes exactly, 1 = truncated, 2 = trailing bytes. Only the
+// error path uses it (see truncated_after).
+int host_record_status(const uint8_t* rec, uint64_t len) {
+  uint64_t pos = 0;
+  if (pos + 4 > len) return 1;
+  const uint64_t nu = host_u32(rec + pos);
+  pos += 4 + 8 * nu;
+  if (pos + 4 > len) return 1;
+  const uint32_t nc = host_u32(rec + pos);
+  pos += 4;
+  for (uint32_t c = 0; c < nc; ++c) {
+    if (pos + 4 > len) return 1;
+    pos += 4 + 8 * static_cast<uint64_t>(host_u32(rec + pos));
+  }
+  if (pos + 8 > len) return 1;
+  return pos + 8 == len ? 0 : 2;
+}
+
 // the reference's Reader::next_iteration truncation text (workload.cpp:511-516)
 [[noreturn]] void truncated(int iteration, int rank, long long sample_idx) {
   raise(FSX_ERR_IO, "workload: file truncated; last complete record is iteration " + std::to_string(iteration) +
@@ -262,15 +290,37 @@ int fsx_workload_scan(const uint8_t* h_bytes, uint64_t nbytes, int num_ranks, in
   FSX_API_BEGIN
   if (num_ranks <= 0) raise(FSX_ERR_INVALID_ARGUMENT, "workload: num_ranks must be positive");
   uint64_t pos = 0, k = 0;
+  // The reference decodes each record as it reads it (workload.cpp:518-537),
+  // so a malformed record before the truncation point raises first: on
+  // truncation, re-walk the complete records in file order and raise the
+  // first one's decode error, else the truncation.
+  auto truncated_after = [&](int rr, long long ii) {
+    uint64_t q = 0;
+    for (int r2 = 0; r2 <= rr; ++r2) {
+      const uint32_t cnt = host_u32(h_bytes + q);
+      q += 4;
+      for (uint32_t i2 = 0; i2 < cnt && (r2 < rr || i2 < static_cast<uint64_t>(ii)); ++i2) {
+        const uint32_t len2 = host_u32(h_bytes + q);
+        q += 4;
+        const int st = host_record_status(h_bytes + q, len2);
+        if (st == 1) raise(FSX_ERR_IO, "workload: record truncated");
+        if (st == 2)
+          raise(FSX_ERR_IO, "workload: record has trailing bytes at iteration " + std::to_string(iteration) +
+                                ", rank " + std::to_string(r2) + ", sample " + std::to_string(i2));
+        q += len2;
+      }
+    }
+    truncated(iteration, rr, ii);
+  };
   for (int r = 0; r < num_ranks; ++r) {
-    if (pos + 4 > nbytes) truncated(iteration, r, 0);
+    if (pos + 4 > nbytes) truncated_after(r, 0);
     const uint32_t count = host_u32(h_bytes + pos);
     pos += 4;
     for (uint32_t i = 0; i < count; ++i) {
-      if (pos + 4 > nbytes) truncated(iteration, r, i);
+      if (pos + 4 > nbytes) truncated_after(r, i);
       const uint32_t len = host_u32(h_bytes + pos);
       pos += 4;
-      if (pos + len > nbytes) truncated(iteration, r, i);
+      if (pos + len > nbytes) truncated_after(r, i);
       if (h_rec_off && k < cap) h_rec_off[k] = pos;
       ++k;
       pos += len;
@@ -292,6 +342,7 @@ int fsx_workload_decode(fsx_ctx* ctx, const uint8_t* d_bytes, uint64_t nbytes, c
   FSX_API_BEGIN
   DeviceGuard dg(ctx->device);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  uint64_t* first_bad = nullptr;
   if (n) {
     const uint64_t tiles = (n + kRecTile - 1) / kRecTile;
     DevBuf<uint64_t>& ts = scan_scratch(ctx, 0);
@@ -302,8 +353,12 @@ int fsx_workload_decode(fsx_ctx* ctx, const uint8_t* d_bytes, uint64_t nbytes, c
       tfb.ensure(nbytes / 8 / kIdTile + 2);  // ids <= nbytes / 8
       tf = tfb.p;
     }
+    DevBuf<uint64_t>& fb = scan_scratch(ctx, 2);
+    fb.ensure(1);
+    first_bad = fb.p;
+    FSX_CUDA(cudaMemsetAsync(first_bad, 0xff, 8, s));
     FSX_LAUNCH(ctx, k_rec_parse, static_cast<unsigned>(tiles), kRecTile, 0, s, d_bytes, d_rec_off, n, d_uih_len,
-               d_labels, ts.p, ctx->d_err);
+               d_labels, ts.p, reinterpret_cast<unsigned long long*>(first_bad));
     FSX_LAUNCH(ctx, k_rec_scan_tiles, 1, 32, 0, s, ts.p, tiles, n, d_offsets, tf);
     FSX_LAUNCH(ctx, k_rec_offsets, static_cast<unsigned>(tiles), kRecTile, 0, s, d_uih_len, n, ts.p, d_offsets, tf);
     if (d_values)
@@ -313,13 +368,14 @@ int fsx_workload_decode(fsx_ctx* ctx, const uint8_t* d_bytes, uint64_t nbytes, c
     FSX_CUDA(cudaMemsetAsync(d_offsets, 0, sizeof(uint64_t), s));
   }
   // one host sync: the error word and the id total together
-  uint64_t tot = 0;
+  uint64_t tot = 0, bad = ~0ull;
   FSX_CUDA(cudaMemcpyAsync(ctx->h_err, ctx->d_err, sizeof(DevErr), cudaMemcpyDeviceToHost, s));
   FSX_CUDA(cudaMemcpyAsync(&tot, d_offsets + n, 8, cudaMemcpyDeviceToHost, s));
+  if (first_bad) FSX_CUDA(cudaMemcpyAsync(&bad, first_bad, 8, cudaMemcpyDeviceToHost, s));
   FSX_CUDA(cudaStreamSynchronize(s));
-  const int kind = ctx->h_err->kind;
+  const int kind = bad != ~0ull ? ((bad & 1u) ? kErrRecTrailing : kErrRecTruncated) : ctx->h_err->kind;
   if (kind == kErrRecTruncated || kind == kErrRecTrailing || kind == kErrIdCapacity) {
-    const DevErr e = *ctx->h_err;
+    const DevErr e = bad != ~0ull ? DevErr{kind, 0, bad >> 1, 0} : *ctx->h_err;
     FSX_CUDA(cudaMemsetAsync(ctx->d_err, 0, sizeof(DevErr), s));
     FSX_CUDA(cudaStreamSynchronize(s));
     if (kind == kErrRecTruncated) raise(FSX_ERR_IO, "workload: record truncated");  // get_le, workload.cpp:312

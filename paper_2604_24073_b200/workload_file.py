@@ -100,8 +100,9 @@ class Reader:
             raise ProtocolError("workload: no more iterations in file")
         view = self._buf[self._pos:]
         nbytes = int(view.size)
-        # a record is >= 16 bytes of body (two u32 counts + f64 label) + its u32 length
-        cap = nbytes // 20 + 1
+        # every record carries at least its u32 length prefix (a short or empty
+        # record must reach the decode's IoError, not a capacity error)
+        cap = nbytes // 4 + 1
         rec_off = np.empty(cap, np.uint64)
         per_rank = np.zeros(self._ranks, np.uint64)
         n, used = C.c_uint64(), C.c_uint64()

@@ -1,7 +1,8 @@
 """GPU parity of the embedding engines (SynchronizedEmbedding /
 PrioritizedEmbedding over libfsx) against the reference's golden tables and
 the C oracle. f64 tables: bit-exact (same per-row accumulation order);
-fp32 tables: within 1e-6 floored relative error. Multi-rank cases run as
+fp32 tables: bit-exact with the oracle's fp32-storage model, including the
+engine's chunk and PRESUM associations. Multi-rank cases run as
 threads of one process (several ranks per GPU when the box has fewer GPUs),
 exactly like the reference's InProcessFabric tests."""
 import numpy as np
@@ -82,16 +83,14 @@ def test_sync_single_rank_dense(drv, oracle):
 
 
 @pytest.mark.parametrize("world", [1, 2, 4])
-def test_fp32_zipf_within_tolerance(drv, oracle, world):
-    """config-1-like Zipf traffic on fp32 tables.
-    * reduce_chunk=0 (reference accumulation order): bit-exact with the oracle
-      run on an fp32 table (store_f32: values rounded to float on store, the
-      gradient fixture evaluated in float as the torch op does) — the kernels
-      add no error beyond the storage rounding itself;
-    * reduce_chunk=64 (parallel hot rows): both engine modes agree bit for bit
-      and stay within 1e-6 normwise (max|a-b| / max|b|) of the f64 reference.
-      (A per-element floored 1e-6 vs f64 is not a property of fp32 storage:
-      the init rounding alone is ~4e-9 absolute, 4e-6 of the 1e-3 floor.)"""
+def test_fp32_zipf_bitwise(drv, oracle, world):
+    """config-1-like Zipf traffic on fp32 tables, bit-exact with the oracle
+    run on an fp32-storage table (store_f32: values rounded to float on store,
+    the gradient fixture evaluated in float as the torch op does):
+    * reduce_chunk=0: the reference's single left fold per row;
+    * reduce_chunk=64 (parallel hot rows): the engine's fixed chunk
+      association, restated in the oracle (chunk_fold); both engine modes
+      agree bit for bit."""
     from paper_2604_24073_b200 import workload
     from paper_2604_24073_b200.embedding import TableGeometry
     rows, dim, iters = 50_000, 64, 4
@@ -103,39 +102,45 @@ def test_fp32_zipf_within_tolerance(drv, oracle, world):
     assert np.array_equal(_bits(exact), _bits(want32))
     got_p, _ = drv.run_engine(True, batches, geom, 0.05, 3, dtype="f32", reduce_chunk=64)
     got_s, _ = drv.run_engine(False, batches, geom, 0.05, 3, dtype="f32", reduce_chunk=64)
-    assert np.array_equal(_bits(got_p), _bits(got_s))
-    want, _ = oracle.run_engine(world, batches, rows, dim, 0.05, 3)
-    assert float(np.max(np.abs(got_p - want)) / np.max(np.abs(want))) < 1e-6
+    want64, _ = oracle.run_engine(world, batches, rows, dim, 0.05, 3, store_f32=True, reduce_chunk=64)
+    assert np.array_equal(_bits(got_p), _bits(want64))
+    assert np.array_equal(_bits(got_s), _bits(want64))
 
 
-def test_f64_chunked_reduce_close(drv, oracle):
+def test_f64_chunked_reduce_bitwise(drv, oracle):
     from paper_2604_24073_b200 import workload
     from paper_2604_24073_b200.embedding import TableGeometry
     rows, dim = 20_000, 32
     batches = [[workload.zipf_batch(7, 8000, rows, offset=8000 * i)] for i in range(3)]
-    want, _ = oracle.run_engine(1, batches, rows, dim, 0.05, 3)
-    got, _ = drv.run_engine(True, batches, TableGeometry(rows, dim, 1), 0.05, 3, reduce_chunk=16)
-    assert frel(got, want) < 1e-12
+    want, _ = oracle.run_engine(1, batches, rows, dim, 0.05, 3, reduce_chunk=16)
+    for prio in (True, False):
+        got, _ = drv.run_engine(prio, batches, TableGeometry(rows, dim, 1), 0.05, 3, reduce_chunk=16)
+        assert np.array_equal(_bits(got), _bits(want)), prio
 
 
-def test_presum_golden_cases_close(drv, ENG):
+def test_presum_golden_cases_bitwise(drv, ENG, oracle):
     """FSX_ENGINE_PRESUM on every golden case (1-8 ranks, odd dims, empty
-    batches): the collision gradients are summed per (source, row) first, so
-    the f64 tables differ from the reference only by reassociation."""
+    batches): bit-exact with the oracle's PRESUM association (collision rows
+    summed per source, then over sources in rank order), and the
+    IterationStats identical to the reference's."""
     from paper_2604_24073_b200.embedding import TableGeometry
     for name, c in ENG.items():
         geom = TableGeometry(c["rows"], c["dim"], c["world"])
         got, stats = drv.run_engine(True, c["batches"], geom, c["lr"], c["seed"], presum=True, with_stats=True)
+        want, _ = oracle.run_engine(c["world"], c["batches"], c["rows"], c["dim"], c["lr"], c["seed"],
+                                    presum=True)
+        assert np.array_equal(_bits(got), _bits(want)), name
         assert frel(got, c["table"]) < 1e-12, name
         st = np.array([[s.collision_rows, s.unique_next_rows, s.blocking_bytes] for s in stats], np.uint64)
         assert np.array_equal(st, c["stats"]), name
 
 
 @pytest.mark.parametrize("world", [1, 2, 4])
-def test_presum_fp32_zipf_within_tolerance(drv, oracle, world):
-    """PRESUM on fp32 tables: deterministic (two runs bitwise equal), within
-    1e-6 normwise of the f64 reference, and the IterationStats (reference
-    accounting) identical to the exact protocol's."""
+def test_presum_fp32_zipf_bitwise(drv, oracle, world):
+    """PRESUM + reduce_chunk 64 on fp32 tables (the bench's numeric path at
+    N > 1): bit-exact with the oracle's fp32-storage PRESUM association, and
+    the IterationStats (reference accounting) identical to the exact
+    protocol's."""
     from paper_2604_24073_b200 import workload
     from paper_2604_24073_b200.embedding import TableGeometry
     rows, dim, iters = 50_000, 64, 4
@@ -144,13 +149,12 @@ def test_presum_fp32_zipf_within_tolerance(drv, oracle, world):
     geom = TableGeometry(rows, dim, world)
     a, st_a = drv.run_engine(True, batches, geom, 0.05, 3, dtype="f32", reduce_chunk=64, presum=True,
                              with_stats=True)
-    b, _ = drv.run_engine(True, batches, geom, 0.05, 3, dtype="f32", reduce_chunk=64, presum=True)
-    assert np.array_equal(_bits(a), _bits(b))
+    want, _ = oracle.run_engine(world, batches, rows, dim, 0.05, 3, store_f32=True, reduce_chunk=64,
+                                presum=True)
+    assert np.array_equal(_bits(a), _bits(want))
     _, st_x = drv.run_engine(True, batches, geom, 0.05, 3, dtype="f32", reduce_chunk=64, with_stats=True)
     key = lambda st: [(s.collision_rows, s.unique_next_rows, s.blocking_bytes) for s in st]  # noqa: E731
     assert key(st_a) == key(st_x)
-    want, _ = oracle.run_engine(world, batches, rows, dim, 0.05, 3)
-    assert float(np.max(np.abs(a - want)) / np.max(np.abs(want))) < 1e-6
 
 
 def test_protocol_order_errors(cuda):

@@ -107,3 +107,66 @@ def test_cfg2_scale_round_trip(cuda, tmp_path):
     assert np.array_equal(got_lens, lens.astype(np.uint64))
     assert np.array_equal(got_ids, ids)
     assert np.array_equal(got_labels, labels)
+
+
+def _write_records(p, W, per_rank_recs, truncate=0):
+    spec = {"batch_size": 2, "dist": {"hi": 4, "kind": "uniform", "lo": 0}, "max_uih": 4,
+            "num_iterations": 1, "num_ranks": len(per_rank_recs), "seed": 1, "table_rows": 10,
+            "target_collision": None}
+    w = W.Writer(str(p), spec)
+    w.close()
+    body = b""
+    for recs in per_rank_recs:
+        body += struct.pack("<I", len(recs))
+        for rec in recs:
+            body += struct.pack("<I", len(rec)) + rec
+    with open(p, "ab") as f:
+        f.write(body[:len(body) - truncate])
+
+
+def test_misaligned_record_is_an_io_error_not_a_fault(cuda, tmp_path):
+    """A record whose length is not a multiple of 4 (1 trailing byte) shifts
+    every later record off 4-byte alignment. The reference raises its
+    trailing-bytes IoError at that record; the GPU decode must do the same
+    (no misaligned-address fault poisoning the context) and stay usable."""
+    from paper_2604_24073_b200 import workload_file as W
+    from paper_2604_24073_b200.errors import IoError
+    good = [W.encode_sample([1, 2], [[3]], 0.5), W.encode_sample([4], [], 0.25)]
+    p = tmp_path / "misaligned.bin"
+    _write_records(p, W, [[good[0], W.encode_sample([5], [], 0.75) + b"\0"], [good[1], good[0]]])
+    with pytest.raises(IoError, match=r"^workload: record has trailing bytes at iteration 0, rank 0, sample 1$"):
+        W.Reader(str(p), cuda).next_iteration()
+    # the context is intact: a good file decodes afterwards
+    q = tmp_path / "good.bin"
+    _write_records(q, W, [good, good])
+    out = W.Reader(str(q), cuda).next_iteration()
+    assert len(out) == 2
+
+
+def test_first_bad_record_in_file_order_wins(cuda, tmp_path):
+    """Several malformed records: the reference decodes in file order and
+    names the first; a malformed record also beats a later file truncation."""
+    from paper_2604_24073_b200 import workload_file as W
+    from paper_2604_24073_b200.errors import IoError
+    ok = W.encode_sample([1], [], 0.5)
+    trail = W.encode_sample([2], [], 0.5) + b"\0\0\0\0"
+    recs = [[ok] * 40 + [trail] + [ok] * 300 + [trail], [ok] * 5 + [trail]]
+    p = tmp_path / "multi.bin"
+    _write_records(p, W, recs)
+    with pytest.raises(IoError, match=r"^workload: record has trailing bytes at iteration 0, rank 0, sample 40$"):
+        W.Reader(str(p), cuda).next_iteration()
+    q = tmp_path / "trail_then_cut.bin"
+    _write_records(q, W, [[ok, trail, ok], [ok, ok]], truncate=3)
+    with pytest.raises(IoError, match=r"^workload: record has trailing bytes at iteration 0, rank 0, sample 1$"):
+        W.Reader(str(q), cuda).next_iteration()
+
+
+def test_empty_records_reach_the_decode_error(cuda, tmp_path):
+    """Many zero-length records: the record table must hold them all, so the
+    decode reports the reference's 'record truncated', not a capacity error."""
+    from paper_2604_24073_b200 import workload_file as W
+    from paper_2604_24073_b200.errors import IoError
+    p = tmp_path / "empty.bin"
+    _write_records(p, W, [[b""] * 64, [b""] * 64])
+    with pytest.raises(IoError, match=r"^workload: record truncated$"):
+        W.Reader(str(p), cuda).next_iteration()

@@ -113,3 +113,82 @@ def test_restatement_matches_reference_live(oracle, reference):
     init = oracle.init_shard(1_000_000, 16, 1, 0, 3)
     v_or, u_or, r_or = oracle.apply_gradients(init, 1_000_000, 16, 1, 0, 0.05, ids, grads)
     assert np.array_equal(u_ref, u_or) and np.array_equal(r_ref, r_or) and np.array_equal(v_ref, v_or)
+
+
+def _py_engine(world, batches, rows, dim, lr, seed, oracle, chunk, presum, f32):
+    """Pure-Python restatement of fso_run_engine_ex2 for small cases: the
+    dense synchronized emulation (embedding.cpp:238-297) with the engine's
+    chunk and PRESUM associations spelled out loop by loop."""
+    import struct
+
+    def r32(x):
+        return struct.unpack("f", struct.pack("f", x))[0]
+
+    table = [[oracle.initial_value(seed, g, d) for d in range(dim)] for g in range(rows)]
+    if f32:
+        table = [[r32(v) for v in row] for row in table]
+
+    def fold(vals):
+        if chunk == 0 or len(vals) <= chunk:
+            acc = 0.0
+            for v in vals:
+                acc += v
+            return acc
+        acc = 0.0
+        for c0 in range(0, len(vals), chunk):
+            part = 0.0
+            for v in vals[c0:c0 + chunk]:
+                part += v
+            acc += part
+        return acc
+
+    iters = len(batches)
+    for i in range(iters):
+        occ = [(int(g), r, j) for r in range(world) for j, g in enumerate(batches[i][r])]
+        served = {(r, j): list(table[g]) for g, r, j in occ}
+        nxt = {int(g) for r in range(world) for g in batches[i + 1][r]} if i + 1 < iters else set()
+        split = presum and world > 1 and 0 < i < iters - 1
+        for g in sorted({o[0] for o in occ}):
+            mine = [(r, j) for gg, r, j in occ if gg == g]  # (rank, position) order
+            for d in range(dim):
+                def grad(rj):
+                    v = served[rj][d]
+                    return r32(r32(v * 0.125) + 0.0625) if f32 else v * 0.125 + 0.0625
+                if split and g in nxt:
+                    acc = 0.0
+                    for r in range(world):
+                        vals = [grad(rj) for rj in mine if rj[0] == r]
+                        if vals:
+                            ps = fold(vals)
+                            acc += r32(ps) if f32 else ps
+                else:
+                    acc = fold([grad(rj) for rj in mine])
+                v = table[g][d] - lr * acc
+                table[g][d] = r32(v) if f32 else v
+    return np.array(table, np.float64)
+
+
+@pytest.mark.parametrize("chunk,presum,f32", [(0, False, False), (2, False, False), (3, True, False),
+                                              (2, True, True), (0, True, True)])
+def test_engine_associations_match_python_restatement(oracle, chunk, presum, f32):
+    rng = np.random.default_rng(5)
+    world, rows, dim = 3, 12, 3
+    batches = [[rng.integers(0, rows // 2 if i % 2 else rows, size=rng.integers(0, 9)).astype(np.uint64)
+                for _ in range(world)] for i in range(4)]
+    want = _py_engine(world, batches, rows, dim, 0.5, 9, oracle, chunk, presum, f32)
+    got, _ = oracle.run_engine(world, batches, rows, dim, 0.5, 9, store_f32=f32, reduce_chunk=chunk,
+                               presum=presum)
+    assert np.array_equal(got.reshape(-1).view(np.uint64), want.reshape(-1).view(np.uint64))
+
+
+def test_engine_associations_degenerate_cases(oracle, ENG):
+    """chunk >= every row's occurrence count and presum at one rank are the
+    reference's single left fold: bit-exact with the reference goldens."""
+    for name, c in ENG.items():
+        big = max([len(b) for it in c["batches"] for b in it] + [1])
+        t, _ = oracle.run_engine(c["world"], c["batches"], c["rows"], c["dim"], c["lr"], c["seed"],
+                                 reduce_chunk=big)
+        assert np.array_equal(t.reshape(-1).view(np.uint64), c["table"].reshape(-1).view(np.uint64)), name
+        if c["world"] == 1:
+            t, _ = oracle.run_engine(1, c["batches"], c["rows"], c["dim"], c["lr"], c["seed"], presum=True)
+            assert np.array_equal(t.reshape(-1).view(np.uint64), c["table"].reshape(-1).view(np.uint64)), name
