@@ -103,6 +103,10 @@ struct Ctx {
   // Overridable for tuning: FSX_COPY_PER_SM, FSX_SINGLE_PER_SM, FSX_FLAT_PER_SM.
   unsigned copy_per_sm = 3, single_per_sm = 8, flat_per_sm = 16, warp_per_sm = 3;
   bool sgd_warp = true;  // FSX_SGD_WARP=0: the thread-per-vector k_sgd_flat + k_sgd_combine
+  // the bulk-copy staged persistent update (sgd_stream.cuh); FSX_SGD_STREAM=0:
+  // k_sgd_single + k_sgd_warp. stream_per_sm caps its CTAs (4 warps) per SM.
+  bool sgd_stream = true;
+  unsigned stream_per_sm = 6;
   unsigned warp_variant = 0;  // FSX_WARP_VARIANT (tuning): k_sgd_warp unroll / min CTAs per SM
   bool pdl = true;       // programmatic dependent launches (FSX_PDL=0: plain launches)
   bool onesweep = true;  // decoupled look-back radix passes (FSX_ONESWEEP=0: 3 launches per pass)

@@ -163,6 +163,8 @@ int fsx_ctx_create(int device, int rank, int world, fsx_ctx** out) {
   c->warp_per_sm = env_u("FSX_WARP_PER_SM", c->warp_per_sm);
   c->warp_variant = env_u("FSX_WARP_VARIANT", c->warp_variant);
   if (const char* v = std::getenv("FSX_SGD_WARP")) c->sgd_warp = std::atoi(v) != 0;
+  if (const char* v = std::getenv("FSX_SGD_STREAM")) c->sgd_stream = std::atoi(v) != 0;
+  c->stream_per_sm = env_u("FSX_STREAM_PER_SM", c->stream_per_sm);
   // onesweep radix passes: on (bench A/B on B200, after the one-rank side
   // lane was slimmed: 0.274 -> 0.259 ms at N = 1; on at N = 4 as well)
   c->onesweep = true;

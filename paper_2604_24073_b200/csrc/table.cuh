@@ -2,6 +2,11 @@
 // embedding.hpp:59-90) and its update machinery.
 #pragma once
 
+#include <algorithm>
+#include <mutex>
+#include <unordered_map>
+
+#include "sgd_stream.cuh"
 #include "sorter.cuh"
 
 namespace fsx {
@@ -81,6 +86,33 @@ void sgd_plan(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_cap, uint
   run_scan(ctx, plan, rows_cap, rs.d_u, s.scan, s.d_tot.p, stream);
 }
 
+// persistent grid of k_sgd_stream: as many 4-warp CTAs per SM as shared
+// memory allows, capped by ctx->stream_per_sm
+template <class T, int NV, int R>
+void launch_sgd_stream(Ctx* ctx, const SgdArgs<T>& a, uint32_t* done, uint32_t rb, cudaStream_t stream) {
+  constexpr int kWarps = 4;
+  const size_t smem = ((kWarps * R * 8 + 127) & ~static_cast<size_t>(127)) + static_cast<size_t>(kWarps) * R * rb;
+  static std::mutex m;
+  static std::unordered_map<size_t, int>* occ = new std::unordered_map<size_t, int>();
+  int per_sm;
+  {
+    std::lock_guard<std::mutex> g(m);
+    auto it = occ->find(smem);
+    if (it == occ->end()) {
+      if (smem > 48 * 1024)
+        FSX_CUDA(cudaFuncSetAttribute(k_sgd_stream<T, NV, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+      int b = 0;
+      FSX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sgd_stream<T, NV, R>, kWarps * 32, smem));
+      it = occ->emplace(smem, b > 0 ? b : 1).first;
+    }
+    per_sm = it->second;
+  }
+  per_sm = std::min<int>(per_sm, static_cast<int>(ctx->stream_per_sm));
+  FSX_LAUNCH(ctx, (k_sgd_stream<T, NV, R>), static_cast<unsigned>(ctx->num_sms * per_sm), kWarps * 32, smem,
+             stream, a, done, rb);
+}
+
 template <class T>
 void sgd_apply(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_cap, uint64_t occ_cap,
                const GradRows<T>& gr, uint32_t chunk, SgdScratch& s, T* rows_out, cudaStream_t stream,
@@ -101,6 +133,16 @@ void sgd_apply(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_cap, uin
   const unsigned g0 = grid_for(ctx, rows_cap * vpr / 2, 256, ctx->single_per_sm);
   const unsigned g1 = grid_for(ctx, work_cap * vpr, 256, ctx->flat_per_sm);
   const unsigned vpl = (vpr + 31) / 32;
+  if (ve == VE16 && ctx->sgd_stream && vpl <= 4 && vpl != 3) {
+    // one persistent kernel, rows staged by bulk copies (sgd_stream.cuh)
+    if (vpl == 1)
+      launch_sgd_stream<T, 1, 16>(ctx, a, s.done.p, rb, stream);
+    else if (vpl == 2)
+      launch_sgd_stream<T, 2, 8>(ctx, a, s.done.p, rb, stream);
+    else
+      launch_sgd_stream<T, 4, 8>(ctx, a, s.done.p, rb, stream);
+    return;
+  }
   if (ve == VE16 && ctx->sgd_warp && vpl <= 4 && vpl != 3) {
     // warp per work item, combine fused (k_sgd_warp)
     FSX_LAUNCH(ctx, (k_sgd_single<T, VE16>), g0, 256, 0, stream, a, shift);

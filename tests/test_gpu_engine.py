@@ -169,3 +169,22 @@ def test_protocol_order_errors(cuda):
     prio.forward([1], None)
     with pytest.raises(ProtocolError):
         prio.forward([1], None)
+
+
+@pytest.mark.parametrize("dtype,dim,world", [("f64", 256, 1), ("f32", 512, 2), ("f32", 96, 1), ("f64", 16, 2),
+                                             ("f32", 256, 3)])
+def test_update_row_widths_bitwise(drv, oracle, dtype, dim, world):
+    """Every row width the update kernels specialise on (1, 2 or 4 16-byte
+    vectors per lane, partial warps, f32 and f64): hot rows split into
+    chunks of 16 occurrences, bit-exact with the oracle's chunk association
+    in both engine modes."""
+    from paper_2604_24073_b200 import workload
+    from paper_2604_24073_b200.embedding import TableGeometry
+    rows, iters = 4_000, 3
+    batches = [[workload.zipf_batch(300 + r, 2500, rows, offset=2500 * i) for r in range(world)]
+               for i in range(iters)]
+    geom = TableGeometry(rows, dim, world)
+    want, _ = oracle.run_engine(world, batches, rows, dim, 0.05, 3, store_f32=dtype == "f32", reduce_chunk=16)
+    for prio in (True, False):
+        got, _ = drv.run_engine(prio, batches, geom, 0.05, 3, dtype=dtype, reduce_chunk=16)
+        assert np.array_equal(_bits(got), _bits(want)), prio
