@@ -106,7 +106,9 @@ struct Ctx {
   // the bulk-copy staged persistent update (sgd_stream.cuh); FSX_SGD_STREAM=0:
   // k_sgd_single + k_sgd_warp. stream_per_sm caps its CTAs (4 warps) per SM.
   bool sgd_stream = true;
-  unsigned stream_per_sm = 6;
+  unsigned stream_per_sm = 8;
+  unsigned stream_variant = 0;
+  unsigned long long stream_span_ns = 0, stream_span_n = 0;  // FSX_STREAM_SPAN (debug)  // FSX_STREAM_VARIANT (tuning): ring depth / CTAs per SM
   unsigned warp_variant = 0;  // FSX_WARP_VARIANT (tuning): k_sgd_warp unroll / min CTAs per SM
   bool pdl = true;       // programmatic dependent launches (FSX_PDL=0: plain launches)
   bool onesweep = true;  // decoupled look-back radix passes (FSX_ONESWEEP=0: 3 launches per pass)

@@ -496,6 +496,20 @@ struct Engine {
   }
   uint32_t seq[NCH] = {};
   cudaStream_t lo = nullptr, hi = nullptr, ux = nullptr;  // ux: deferred exclusive updates
+  // us: the caller's-stream row movers re-issued at the highest priority
+  // (FSX_C_PRIO: 1 = the one-rank update, 2 = + the merge), so the side lane
+  // (mid priority) does not take the SMs those kernels' CTAs wait for
+  cudaStream_t us = nullptr;
+  int c_prio = 0;
+  int self_serial = 0;
+  cudaStream_t boost(cudaStream_t c, int level) {
+    if (c_prio < level) return c;
+    wait(us, record(c));
+    return us;
+  }
+  void unboost(cudaStream_t c, cudaStream_t s) {
+    if (s != c) wait(c, record(s));
+  }
   // per-(lane, peer) copy streams: a lane's copies never queue behind another
   // lane's (the collision chain must not wait for prefetch or deferred
   // traffic issued earlier on the same peer)
@@ -918,7 +932,7 @@ struct Engine {
               cudaStream_t s, int phase = FSX_PHASE_UPDATE, const void* self_grads = nullptr,
               const uint32_t* self_pos = nullptr) {
     Span sp(this, phase, s);
-    RowSegments rs{o.srt.uniq.p, o.srt.seg_start.p, o.srt.perm, o.srt.d_u(), select, want};
+    RowSegments rs{o.srt.uniq.p, o.srt.seg_start.p, o.srt.perm, o.srt.d_u(), select, want, o.srt.inverse.p};
     const uint64_t m = o.m_cap;
     const char* sb = static_cast<const char*>(self_grads);
     if (t->dtype == FSX_F32) {
@@ -937,24 +951,28 @@ struct Engine {
   // whole iteration early; the backward only runs the update kernels.
   bool self_plan() const { return p == 1 && !presum(); }
   void plan_self(OwnBatch& o, cudaStream_t s) {
-    RowSegments rs{o.srt.uniq.p, o.srt.seg_start.p, o.srt.perm, o.srt.d_u(), nullptr, 0};
+    RowSegments rs{o.srt.uniq.p, o.srt.seg_start.p, o.srt.perm, o.srt.d_u(), nullptr, 0, o.srt.inverse.p};
     if (t->dtype == FSX_F32)
       sgd_plan<float>(ctx, *t, rs, o.m_cap, o.m_cap, nullptr, cfg.reduce_chunk, o.plan, s);
     else
       sgd_plan<double>(ctx, *t, rs, o.m_cap, o.m_cap, nullptr, cfg.reduce_chunk, o.plan, s);
     o.ev_plan = record(s);
   }
-  void apply_self(OwnBatch& o, const void* grads, cudaStream_t c) {
-    exposed_wait(c, {o.ev_plan});
-    Span sp(this, FSX_PHASE_CO_UPDATE, c);
-    RowSegments rs{o.srt.uniq.p, o.srt.seg_start.p, o.srt.perm, o.srt.d_u(), nullptr, 0};
-    if (t->dtype == FSX_F32) {
-      GradRows<float> gr{static_cast<const char*>(grads), 0, nullptr, nullptr, rb};
-      sgd_apply<float>(ctx, *t, rs, o.m_cap, o.m_cap, gr, cfg.reduce_chunk, o.plan, nullptr, c);
-    } else {
-      GradRows<double> gr{static_cast<const char*>(grads), 0, nullptr, nullptr, rb};
-      sgd_apply<double>(ctx, *t, rs, o.m_cap, o.m_cap, gr, cfg.reduce_chunk, o.plan, nullptr, c);
+  void apply_self(OwnBatch& o, const void* grads, cudaStream_t c0) {
+    exposed_wait(c0, {o.ev_plan});
+    cudaStream_t c = boost(c0, 1);
+    {
+      Span sp(this, FSX_PHASE_CO_UPDATE, c);
+      RowSegments rs{o.srt.uniq.p, o.srt.seg_start.p, o.srt.perm, o.srt.d_u(), nullptr, 0};
+      if (t->dtype == FSX_F32) {
+        GradRows<float> gr{static_cast<const char*>(grads), 0, nullptr, nullptr, rb};
+        sgd_apply<float>(ctx, *t, rs, o.m_cap, o.m_cap, gr, cfg.reduce_chunk, o.plan, nullptr, c);
+      } else {
+        GradRows<double> gr{static_cast<const char*>(grads), 0, nullptr, nullptr, rb};
+        sgd_apply<double>(ctx, *t, rs, o.m_cap, o.m_cap, gr, cfg.reduce_chunk, o.plan, nullptr, c);
+      }
     }
+    unboost(c0, c);
   }
   SgdScratch sgd[3];  // one per lane that updates: ux, hi, compute
   SgdScratch& sgd_for(cudaStream_t s) { return sgd[s == ux ? 0 : s == hi ? 1 : 2]; }
@@ -1315,7 +1333,12 @@ struct Engine {
   }
 
   // requester: merge E_ex / E_co into batch-major rows (embedding.cpp:453-484)
-  void merge(ReqBatch& r, void* d_out, cudaStream_t s, int part = 0) {
+  void merge(ReqBatch& r, void* d_out, cudaStream_t s0, int part = 0) {
+    cudaStream_t s = boost(s0, 2);
+    merge_on(r, d_out, s, part);
+    unboost(s0, s);
+  }
+  void merge_on(ReqBatch& r, void* d_out, cudaStream_t s, int part) {
     Span sp(this, FSX_PHASE_MERGE, s);
     if (r.idx_par < 0) raise(FSX_ERR_PROTOCOL, "embedding: merge without IDX messages");
     CSlots co{};
@@ -1531,6 +1554,14 @@ struct Engine {
       // runs at once on the caller's stream, reading the gradients in place.
       // It needs neither the masks nor the split plan (only the statistics
       // do, on H below), so it does not wait for the side lane.
+      // FSX_SELF_SERIAL (A/B): 1 = the update waits for the side lane's
+      // route / dedup / collision of i+1 (ev_mask), 2 = for its whole prep
+      // (ev_next_ready), so the update kernel does not share the SMs with it
+      if (self_serial == 1 && ev_mask) wait(c, ev_mask);
+      if (self_serial == 2) {
+        wait_next_ready();
+        if (ev_next_ready) wait(c, ev_next_ready);
+      }
       if (self_plan())
         apply_self(oc, grads, c);
       else
@@ -1662,6 +1693,7 @@ struct Engine {
     if (lo) cudaStreamDestroy(lo);
     if (hi) cudaStreamDestroy(hi);
     if (ux) cudaStreamDestroy(ux);
+    if (us) cudaStreamDestroy(us);
     for (auto& lane : cstream)
       for (auto cs : lane)
         if (cs) cudaStreamDestroy(cs);
@@ -1750,6 +1782,9 @@ int fsx_engine_create(fsx_ctx* ctx, fsx_table* table, const fsx_engine_config* c
   FSX_CUDA(cudaStreamCreateWithPriority(&e->lo, cudaStreamNonBlocking, mid));
   FSX_CUDA(cudaStreamCreateWithPriority(&e->hi, cudaStreamNonBlocking, greatest));
   FSX_CUDA(cudaStreamCreateWithPriority(&e->ux, cudaStreamNonBlocking, least));
+  FSX_CUDA(cudaStreamCreateWithPriority(&e->us, cudaStreamNonBlocking, greatest));
+  if (const char* v = std::getenv("FSX_C_PRIO")) e->c_prio = std::atoi(v);
+  if (const char* v = std::getenv("FSX_SELF_SERIAL")) e->self_serial = std::atoi(v);
   // one copy stream per peer: outgoing copies of an all-to-all run on
   // several copy engines at once instead of queueing on one
   for (int l = 0; l < Engine::kLanes; ++l) e->lane_map[l] = prio ? (l == 3 ? 1 : l) : 3;

@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(128) k_co_apply(T* __restrict__ table, ShardGe
 #pragma unroll
       for (int x = 0; x < VE; ++x) {
         r.v[x] = static_cast<T>(__dsub_rn(static_cast<double>(r.v[x]), __dmul_rn(lr, acc[x])));
-        bad |= !isfinite(static_cast<double>(r.v[x]));
+        bad |= !finite_val(r.v[x]);
       }
       *cell = r;
       if (bad) report(err, kErrNonFinite, l * static_cast<uint64_t>(g.p) + g.shard, 0);

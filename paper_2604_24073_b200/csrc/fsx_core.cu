@@ -165,6 +165,7 @@ int fsx_ctx_create(int device, int rank, int world, fsx_ctx** out) {
   if (const char* v = std::getenv("FSX_SGD_WARP")) c->sgd_warp = std::atoi(v) != 0;
   if (const char* v = std::getenv("FSX_SGD_STREAM")) c->sgd_stream = std::atoi(v) != 0;
   c->stream_per_sm = env_u("FSX_STREAM_PER_SM", c->stream_per_sm);
+  c->stream_variant = env_u("FSX_STREAM_VARIANT", c->stream_variant);
   // onesweep radix passes: on (bench A/B on B200, after the one-rank side
   // lane was slimmed: 0.274 -> 0.259 ms at N = 1; on at N = 4 as well)
   c->onesweep = true;
@@ -182,6 +183,9 @@ int fsx_ctx_destroy(fsx_ctx* ctx) {
   FSX_API_BEGIN
   if (!ctx) return FSX_OK;
   DeviceGuard dg(ctx->device);
+  if (ctx->stream_span_n)
+    std::fprintf(stderr, "[fsx] k_sgd_stream: %llu launches, mean span %.1f us\n", ctx->stream_span_n,
+                 1e-3 * static_cast<double>(ctx->stream_span_ns) / static_cast<double>(ctx->stream_span_n));
   cudaFree(ctx->d_err);
   cudaFreeHost(ctx->h_err);
   delete ctx;

@@ -301,6 +301,7 @@ struct RowSegments {
   const uint64_t* d_u;         // live row count U (device)
   const uint8_t* select;       // nullable: update only rows with select[u] == want
   uint8_t want;
+  const uint32_t* inverse = nullptr;  // nullable: occurrence -> row slot (k_stream_entries)
 };
 
 // Work lists. A selected row with exactly one occurrence becomes a "single"
@@ -315,6 +316,9 @@ struct SgdItem {
   const char* g0;         // gradient row of occurrence kb
 };
 constexpr uint32_t kSgdSingleChunk = 0x80000000u;
+
+// k_sgd_stream work split: cost = ring entries + kStreamItemCost per item
+constexpr uint64_t kStreamItemCost = 2;
 
 struct SgdPlanOp {
   static constexpr int NC = 4;
@@ -331,13 +335,34 @@ struct SgdPlanOp {
   const char* const* gptr;  // nullable: gradient row per sorted occurrence
                             // (nullptr: items carry no gradient pointer; the
                             // update kernels resolve rows from perm)
+  // Stream plan (k_sgd_stream, sgd_stream.cuh) when `ent` is set: every row
+  // — one-occurrence rows included — becomes work items in row order; c0
+  // counts the row's ring entries (its table row when updated in place, then
+  // one gradient row per occurrence), each item carries its first entry's
+  // offset in `g0`, the table-row entry is written here and the row's first
+  // gradient entry goes to row_ent[u] (~0: none) for k_stream_entries.
+  uint64_t* ent = nullptr;
+  uint32_t* row_ent = nullptr;
   __device__ uint32_t len(uint64_t u) const { return rs.seg_start[u + 1] - rs.seg_start[u]; }
   __device__ bool selected(uint64_t u) const { return !rs.select || rs.select[u] == rs.want; }
-  // c0: singles, c1: work items, c2: multi-chunk rows, c3: partial slots
+  __device__ char* single_dst(uint64_t u) const {
+    if (seg_out) return seg_out[u];
+    const uint64_t l = rs.uniq_local[u];
+    return l < local_rows ? table + l * row_bytes : nullptr;  // never outside the shard
+  }
+  // c0: singles (stream plan: entries), c1: work items, c2: multi-chunk rows, c3: partial slots
   __device__ void count(uint64_t u, uint32_t (&c)[4]) const {
     c[0] = c[1] = c[2] = c[3] = 0;
     if (!selected(u)) return;
     const uint32_t n = len(u);
+    if (ent) {
+      const uint32_t k = (chunk == 0 || n <= chunk) ? 1u : (n + chunk - 1) / chunk;
+      c[0] = k > 1 ? n : (single_dst(u) ? n + (seg_out ? 0u : 1u) : 0u);
+      c[1] = k;
+      c[2] = k > 1 ? 1u : 0u;
+      c[3] = k > 1 ? k : 0u;
+      return;
+    }
     if (n == 1) { c[0] = 1; return; }
     const uint32_t k = (chunk == 0 || n <= chunk) ? 1u : (n + chunk - 1) / chunk;
     c[1] = k;
@@ -346,6 +371,10 @@ struct SgdPlanOp {
   }
   __device__ void emit(uint64_t u, const uint32_t (&ex)[4], const uint32_t (&c)[4],
                        const uint32_t (&tot)[4]) const {
+    if (ent) {
+      emit_stream(u, ex, c);
+      return;
+    }
     if (c[0] == 0 && c[1] == 0) return;
     const uint32_t s = rs.seg_start[u], e = rs.seg_start[u + 1];
     char* dst = nullptr;
@@ -379,7 +408,61 @@ struct SgdPlanOp {
       part_base[u] = ex[3];
     }
   }
+  __device__ void emit_stream(uint64_t u, const uint32_t (&ex)[4], const uint32_t (&c)[4]) const {
+    if (c[1] == 0) {
+      row_ent[u] = ~0u;
+      return;
+    }
+    const uint32_t s = rs.seg_start[u], e = rs.seg_start[u + 1];
+    if (c[1] == 1) {
+      char* dst = single_dst(u);
+      const bool old = dst && !seg_out;
+      work[ex[1]] = SgdItem{static_cast<uint32_t>(u), kSgdSingleChunk, s, e, dst,
+                            reinterpret_cast<const char*>(static_cast<uintptr_t>(ex[0]))};
+      if (old) ent[ex[0]] = reinterpret_cast<uintptr_t>(dst);
+      row_ent[u] = dst ? ex[0] + (old ? 1u : 0u) : ~0u;
+      return;
+    }
+    for (uint32_t q = 0; q < c[1]; ++q) {
+      const uint32_t kb = s + q * chunk;
+      work[ex[1] + q] = SgdItem{static_cast<uint32_t>(u), q, kb, min(e, kb + chunk), nullptr,
+                                reinterpret_cast<const char*>(static_cast<uintptr_t>(ex[0] + q * chunk))};
+    }
+    multi[ex[2]] = static_cast<uint32_t>(u);
+    part_base[u] = ex[3];
+    row_ent[u] = ex[0];
+  }
 };
+
+// Gradient entries of a stream plan, one thread per sorted occurrence k: the
+// row is found by a search of seg_start, the entry holds the gradient row's
+// address (resolved plans) or the occurrence index tagged in bit 0 (plans
+// built ahead of the gradients: the update adds the base at issue time).
+static __global__ void k_stream_entries(const uint32_t* __restrict__ seg_start, const uint64_t* d_u,
+                                 const uint32_t* __restrict__ perm, const uint32_t* __restrict__ inverse,
+                                 const char* const* __restrict__ gptr, const uint32_t* __restrict__ row_ent,
+                                 uint64_t* __restrict__ ent) {
+  FSX_PDL_ENTER();
+  const uint64_t U = *d_u;
+  const uint64_t n = seg_start[U];
+  for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    uint64_t lo = 0;  // the row u of sorted position k
+    if (inverse) {
+      lo = inverse[perm[k]];
+    } else {  // last row u with seg_start[u] <= k
+      uint64_t hi = U;
+      while (hi - lo > 1) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (seg_start[mid] <= k) lo = mid; else hi = mid;
+      }
+    }
+    const uint32_t r = row_ent[lo];
+    if (r == ~0u) continue;
+    ent[r + (k - seg_start[lo])] = gptr ? reinterpret_cast<uintptr_t>(gptr[k])
+                                        : (static_cast<uint64_t>(perm[k]) << 1) | 1u;
+  }
+}
 
 // Gradient row of every occurrence in sorted order (perm -> source / rank ->
 // row), resolved once by a fully parallel pass
@@ -415,6 +498,7 @@ struct SgdArgs {
                               // written (as T) to seg_out[u] instead of updating
   const T* const* gptr;       // nullable: gradient row per sorted occurrence
                               // (k_grad_ptrs); nullptr: gr.row(perm[k])
+  const uint64_t* ent = nullptr;  // stream plan: ring entries (k_sgd_stream)
   __device__ __forceinline__ const T* grad(uint32_t k) const {
     return gptr ? gptr[k] : gr.row(rs.perm[k]);
   }
@@ -426,6 +510,11 @@ struct SgdArgs {
     return g ? reinterpret_cast<const T*>(g) : grad(it.kb);
   }
 };
+
+// isfinite of a stored value without widening it (an fp32 value is finite
+// exactly when its f64 widening is): one integer test for fp32
+__device__ __forceinline__ bool finite_val(float x) { return (__float_as_uint(x) & 0x7f800000u) != 0x7f800000u; }
+__device__ __forceinline__ bool finite_val(double x) { return isfinite(x); }
 
 // vector of VE elements of T moved as one 4/8/16-byte access
 template <class T, int VE>
@@ -452,7 +541,7 @@ __device__ __forceinline__ void sgd_apply_vec(const SgdArgs<T>& a, uint32_t u, u
   for (int e = 0; e < VE; ++e) {
     const double v = __dsub_rn(static_cast<double>(r.v[e]), __dmul_rn(a.lr, acc[e]));
     r.v[e] = static_cast<T>(v);
-    bad |= !isfinite(static_cast<double>(r.v[e]));
+    bad |= !finite_val(r.v[e]);
   }
   *cell = r;
   if (a.rows_out)
@@ -477,7 +566,7 @@ __device__ __forceinline__ void sgd_store_vec(const SgdArgs<T>& a, uint32_t u, T
 #pragma unroll
   for (int e = 0; e < VE; ++e) {
     r.v[e] = static_cast<T>(__dsub_rn(static_cast<double>(old.v[e]), __dmul_rn(a.lr, acc[e])));
-    bad |= !isfinite(static_cast<double>(r.v[e]));
+    bad |= !finite_val(r.v[e]);
   }
   *reinterpret_cast<VecOf<T, VE>*>(dst + col) = r;
   if (a.rows_out)

@@ -17,7 +17,10 @@ struct SgdScratch {
   DevBuf<uint32_t> multi, part_base;
   DevBuf<uint32_t> done;     // k_sgd_warp: chunks arrived per row (kept zeroed)
   DevBuf<double> partials;
-  DevBuf<uint64_t> d_tot;  // [0] singles, [1] work items, [2] multi rows, [3] partial slots
+  DevBuf<uint64_t> ent;      // stream plan: ring entries (k_sgd_stream)
+  DevBuf<uint32_t> row_ent;  // stream plan: first gradient entry per row
+  bool stream_plan = false;  // the last plan is a stream plan
+  DevBuf<uint64_t> d_tot;  // [0] singles (stream plan: entries), [1] work items, [2] multi rows, [3] partial slots
   ScanScratch scan;
   uint64_t cap_rows = 0, cap_work = 0, cap_occ = 0;
   bool resolved = false;  // the last plan stored gradient-row pointers
@@ -33,6 +36,8 @@ struct SgdScratch {
       done.alloc(cap_rows);
       FSX_CUDA(cudaMemset(done.p, 0, cap_rows * sizeof(uint32_t)));
       gptr.alloc(occ > rows ? occ : rows);
+      ent.alloc(occ + rows + 1);
+      row_ent.alloc(rows + 1);
       // a row with k > 1 chunks has > (k-1)*chunk occurrences: slots <= 2*occ/chunk
       partials.alloc(chunk ? (2 * occ / chunk + 1) * d : 1);
     }
@@ -68,12 +73,21 @@ struct Table {
 //  sgd_apply — the chunk kernels + combine over a plan.
 // seg_out != nullptr: reduce only — each segment's gradient sum (same
 // chunked association) goes to seg_out[u]; the table is not touched.
+// k_sgd_stream handles rows of 1, 2 or 4 16-byte vectors per lane
+template <class T>
+bool use_stream(const Ctx* ctx, const Table& t) {
+  const uint32_t rb = t.row_bytes();
+  const unsigned vpl = (rb / 16 + 31) / 32;
+  return ctx->sgd_stream && rb % 16 == 0 && (vpl == 1 || vpl == 2 || vpl == 4);
+}
+
 template <class T>
 void sgd_plan(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_cap, uint64_t occ_cap,
               const GradRows<T>* resolve_grads, uint32_t chunk, SgdScratch& s, cudaStream_t stream,
               char* const* seg_out = nullptr) {
   if (rows_cap == 0) return;
   s.reserve(rows_cap, occ_cap, t.g.dim, chunk);
+  s.stream_plan = use_stream<T>(ctx, t);
   const T** gptr = nullptr;
   if (resolve_grads) {
     gptr = reinterpret_cast<const T**>(s.gptr.p);
@@ -83,13 +97,20 @@ void sgd_plan(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_cap, uint
   s.resolved = gptr != nullptr;
   SgdPlanOp plan{rs, chunk, s.singles.p, s.work.p, s.multi.p, s.part_base.p, static_cast<char*>(t.values),
                  t.row_bytes(), t.g.local_rows, seg_out, reinterpret_cast<const char* const*>(gptr)};
+  if (s.stream_plan) {
+    plan.ent = s.ent.p;
+    plan.row_ent = s.row_ent.p;
+  }
   run_scan(ctx, plan, rows_cap, rs.d_u, s.scan, s.d_tot.p, stream);
+  if (s.stream_plan)
+    FSX_LAUNCH(ctx, k_stream_entries, grid_for(ctx, occ_cap, 256, 8), 256, 0, stream, rs.seg_start, rs.d_u, rs.perm,
+               rs.inverse, reinterpret_cast<const char* const*>(gptr), s.row_ent.p, s.ent.p);
 }
 
 // persistent grid of k_sgd_stream: as many 4-warp CTAs per SM as shared
 // memory allows, capped by ctx->stream_per_sm
-template <class T, int NV, int R>
-void launch_sgd_stream(Ctx* ctx, const SgdArgs<T>& a, uint32_t* done, uint32_t rb, cudaStream_t stream) {
+template <class T, int NV, int R, int MINB, bool kBulk, bool kFused>
+void launch_sgd_stream(Ctx* ctx, const SgdArgs<T>& a, uint32_t rb, uint32_t* done, cudaStream_t stream) {
   constexpr int kWarps = 4;
   const size_t smem = ((kWarps * R * 8 + 127) & ~static_cast<size_t>(127)) + static_cast<size_t>(kWarps) * R * rb;
   static std::mutex m;
@@ -100,17 +121,43 @@ void launch_sgd_stream(Ctx* ctx, const SgdArgs<T>& a, uint32_t* done, uint32_t r
     auto it = occ->find(smem);
     if (it == occ->end()) {
       if (smem > 48 * 1024)
-        FSX_CUDA(cudaFuncSetAttribute(k_sgd_stream<T, NV, R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        FSX_CUDA(cudaFuncSetAttribute(k_sgd_stream<T, NV, R, MINB, kBulk, kFused>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)));
+      // the ring is the point of the kernel: ask for the largest shared carveout
+      FSX_CUDA(cudaFuncSetAttribute(k_sgd_stream<T, NV, R, MINB, kBulk, kFused>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    cudaSharedmemCarveoutMaxShared));
       int b = 0;
-      FSX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sgd_stream<T, NV, R>, kWarps * 32, smem));
+      FSX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_sgd_stream<T, NV, R, MINB, kBulk, kFused>, kWarps * 32, smem));
+      if (std::getenv("FSX_DEBUG"))
+        std::fprintf(stderr, "[fsx] k_sgd_stream<%d,%d,%d> smem %zu B/CTA: %d CTAs/SM\n", static_cast<int>(sizeof(T)),
+                     NV, R, smem, b);
       it = occ->emplace(smem, b > 0 ? b : 1).first;
     }
     per_sm = it->second;
   }
   per_sm = std::min<int>(per_sm, static_cast<int>(ctx->stream_per_sm));
-  FSX_LAUNCH(ctx, (k_sgd_stream<T, NV, R>), static_cast<unsigned>(ctx->num_sms * per_sm), kWarps * 32, smem,
-             stream, a, done, rb);
+  // FSX_STREAM_SPAN=1 (debug): the kernel's own first-start / last-end
+  // global times per launch, summed into ctx->stream_span_ns
+  static unsigned long long* span = nullptr;  // device: [0] min start, [1] max end
+  static const bool want_span = std::getenv("FSX_STREAM_SPAN") != nullptr;
+  if (want_span) {
+    const unsigned long long init[2] = {~0ull, 0ull};
+    if (!span) {
+      FSX_CUDA(cudaMalloc(&span, sizeof(init)));
+    } else {
+      unsigned long long h[2];
+      FSX_CUDA(cudaMemcpyAsync(h, span, sizeof(h), cudaMemcpyDeviceToHost, stream));
+      FSX_CUDA(cudaStreamSynchronize(stream));
+      if (h[1] > h[0] && h[0] != ~0ull) {
+        ctx->stream_span_ns += h[1] - h[0];
+        ++ctx->stream_span_n;
+      }
+    }
+    FSX_CUDA(cudaMemcpyAsync(span, init, sizeof(init), cudaMemcpyHostToDevice, stream));
+    FSX_CUDA(cudaStreamSynchronize(stream));
+  }
+  FSX_LAUNCH(ctx, (k_sgd_stream<T, NV, R, MINB, kBulk, kFused>), static_cast<unsigned>(ctx->num_sms * per_sm), kWarps * 32, smem,
+             stream, a, rb, done, span);
 }
 
 template <class T>
@@ -133,14 +180,37 @@ void sgd_apply(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_cap, uin
   const unsigned g0 = grid_for(ctx, rows_cap * vpr / 2, 256, ctx->single_per_sm);
   const unsigned g1 = grid_for(ctx, work_cap * vpr, 256, ctx->flat_per_sm);
   const unsigned vpl = (vpr + 31) / 32;
-  if (ve == VE16 && ctx->sgd_stream && vpl <= 4 && vpl != 3) {
+  if (s.stream_plan) {
     // one persistent kernel, rows staged by bulk copies (sgd_stream.cuh)
+    a.ent = s.ent.p;
+    // Default (B200 A/B at config 4, one rank): rings of 16 rows, 3 CTAs of
+    // 4 warps per SM (12 warps x 16 KB in flight per SM), hot-row combine
+    // fused. Fewer, deeper rings leave registers and shared memory on every
+    // SM for the side lane's latency-bound kernels (route / dedup / collide
+    // of the next iteration), which the update otherwise starves.
+    // FSX_STREAM_VARIANT (tuning): 1 = 8-row rings at 5 CTAs per SM,
+    // 2 = separate k_sgd_combine, 3 = LDGSTS instead of bulk copies.
+    const unsigned var = ctx->stream_variant;
+    const bool fused = var != 2;
+    uint32_t* done = s.done.p;
     if (vpl == 1)
-      launch_sgd_stream<T, 1, 16>(ctx, a, s.done.p, rb, stream);
+      launch_sgd_stream<T, 1, 16, 5, true, true>(ctx, a, rb, done, stream);
+    else if (vpl == 2 && var == 1)
+      launch_sgd_stream<T, 2, 8, 5, true, true>(ctx, a, rb, done, stream);
+    else if (vpl == 2 && var == 2)
+      launch_sgd_stream<T, 2, 16, 3, true, false>(ctx, a, rb, done, stream);
+    else if (vpl == 2 && var == 3)
+      launch_sgd_stream<T, 2, 16, 3, false, true>(ctx, a, rb, done, stream);
     else if (vpl == 2)
-      launch_sgd_stream<T, 2, 8>(ctx, a, s.done.p, rb, stream);
+      launch_sgd_stream<T, 2, 16, 3, true, true>(ctx, a, rb, done, stream);
     else
-      launch_sgd_stream<T, 4, 8>(ctx, a, s.done.p, rb, stream);
+      launch_sgd_stream<T, 4, 8, 3, true, true>(ctx, a, rb, done, stream);
+    if (chunk && !fused) {  // hot rows: chunk partials in chunk order
+      if (t.g.dim % 2 == 0)
+        FSX_LAUNCH(ctx, (k_sgd_combine<T, 2>), g2, 128, 0, stream, a);
+      else
+        FSX_LAUNCH(ctx, (k_sgd_combine<T, 1>), g2, 128, 0, stream, a);
+    }
     return;
   }
   if (ve == VE16 && ctx->sgd_warp && vpl <= 4 && vpl != 3) {
