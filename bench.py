@@ -59,6 +59,15 @@ def parse():
                     help="also run config 5 (embedding + HSTU-style victim; blocking NCCL vs "
                          "prioritized copy-engine); default: on when N > 1")
     ap.add_argument("--victim-layers", type=int, default=1)
+    ap.add_argument("--cfg1", type=int, default=-1,
+                    help="also time config 1 (1M x 128 fp32, Zipf batches of 4,096, one rank) beside the "
+                         "reference at full size; default: on at N = 1")
+    ap.add_argument("--cfg2", type=int, default=-1,
+                    help="also time config 2 (FBS / VBS over 65,536 samples, 8 ranks) on the GPU beside the "
+                         "reference's FBS; default: on at N = 1")
+    ap.add_argument("--cfg2-ref-vbs", action="store_true",
+                    help="time the reference's VBS (alpha 1 and 2, ~60-80 s each) live instead of citing "
+                         "profiles/r2_cfg2_reference.json")
     return ap.parse_args()
 
 
@@ -206,7 +215,20 @@ class Victim:
 
 
 # ---- CPU baseline (the reference library, oracle/_ref) --------------------------
-def cpu_reference(args, world_threads, sample_samples, iters=3):
+def host_info():
+    """The GPU box's host: core count and CPU model."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def cpu_reference(args, world_threads, sample_samples, iters=5):
     """The reference's PrioritizedEmbedding (embedding.cpp:301-607) on an
     InProcessFabric with one thread per rank, tables shrunk to 125K rows each
     (the full 10M-row tables do not fit host RAM in f64), the same token stream
@@ -242,23 +264,26 @@ def cpu_reference(args, world_threads, sample_samples, iters=3):
         work += np.unique(allids).size
     secs = sum(us[i] for i in steady) * 1e-6
     return {"value": work / secs, "unit": "rows/s", "cores": world_threads, "kind": kind,
-            "sample": (f"reference PrioritizedEmbedding, {world_threads} rank thread(s), "
-                       f"{sample_samples} samples/rank/iter (~{batches[1][0].size} ids), "
-                       f"{args.tables_per_rank * world_threads} tables x {small_rows} rows x {args.dim} f64, "
-                       f"{len(steady)} steady iteration(s) timed")}
+            "sample": (f"reference PrioritizedEmbedding, {world_threads} rank thread(s) (one per rank, as the "
+                       f"reference runs), {sample_samples} samples/rank/iter (~{batches[1][0].size} ids, the GPU "
+                       f"arm's shape), {args.tables_per_rank * world_threads} tables x {small_rows} rows x "
+                       f"{args.dim} f64 (the 10M-row tables folded to fit host RAM), {len(steady)} steady "
+                       f"iteration(s) timed"),
+            "host": host_info()}
 
 
 def reference_arm(args, world, rank):
+    """The reference's own CPU path on the GPU arm's shape: one rank thread
+    per GPU rank (the reference runs exactly one thread per rank,
+    comm.cpp:140-149), the GPU arm's samples per rank, its tables folded to
+    fit host RAM, bootstrap + 3 steady + final iteration per step."""
     if rank != 0:
         return
-    threads = max(1, min(os.cpu_count() or 1, 8 * max(world, 1)))
-    threads = min(threads, os.cpu_count() or 1)
+    threads = max(1, world)
     vals = []
-    for _ in range(args.warmup):
-        pass  # the reference has no warm-up state worth timing; each step is a fresh bounded sample
     t0 = time.time()
     for k in range(args.steps):
-        r = cpu_reference(args, threads, 256, iters=3)
+        r = cpu_reference(args, threads, args.samples, iters=5)
         vals.append(r["value"])
         if time.time() - t0 > 150:
             break
@@ -266,12 +291,225 @@ def reference_arm(args, world, rank):
     line = {"metric": "lookup+update rows/s", "value": value, "unit": "rows/s", "n_gpus": world,
             "steps": len(vals), "warmup": args.warmup, "higher_is_better": True, "impl": "reference",
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "config4 per-rank share (bounded CPU sample)", "parallelism": f"{threads} rank threads"},
+            "config": {"workload": "BASELINE config4 per-GPU share (the GPU arm's samples per rank and tables "
+                                   "per rank; rows folded to fit host RAM)",
+                       "samples_per_rank": args.samples, "tables": args.tables_per_rank * threads,
+                       "parallelism": f"{threads} rank thread(s)"},
             "cpu_baseline": {"value": value, "unit": "rows/s", "cores": threads, "kind": "reference",
-                             "sample": r["sample"]},
+                             "sample": r["sample"], "host": r["host"]},
             "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "vs_baseline": None}
     print(json.dumps(line), flush=True)
+
+
+# ---- config 5: SM contention of the all-to-all transports --------------------------
+def contention(eng, victim, lens, dev, world, per_peer_bytes=32 << 20, reps=4):
+    """The victim's own duration (CUDA events on its stream) alone, then with
+    all-to-all traffic running concurrently on another stream: (a) the
+    copy-engine all-to-all (fsx_a2a_ce over the engine's windows: cudaMemcpyAsync
+    peer copies + stream memory-op flags, no kernels), (b) NCCL's all-to-all
+    (torch.distributed.all_to_all_single: SM-resident kernels). Also the
+    transfers' own rate (bytes out per GPU / time) while the victim runs and
+    alone. Collective: every rank calls it."""
+    import ctypes as C
+    import torch
+    import torch.distributed as dist
+    from paper_2604_24073_b200 import _lib
+    n64 = per_peer_bytes // 8
+    send = torch.zeros(world * n64, dtype=torch.int64, device=dev)
+    recv = torch.empty(world * n64, dtype=torch.int64, device=dev)
+    side = torch.cuda.Stream(device=dev)
+    offs = (C.c_uint64 * world)(*[d * per_peer_bytes for d in range(world)])
+    nb = (C.c_uint64 * world)(*[per_peer_bytes] * world)
+    got = (C.c_uint64 * world)()
+
+    def ce_once():
+        _lib.call("fsx_a2a_ce", eng.h, C.c_void_p(send.data_ptr()), offs, nb, C.c_void_p(recv.data_ptr()),
+                  per_peer_bytes, got, C.c_void_p(side.cuda_stream))
+
+    def nccl_once():
+        with torch.cuda.stream(side):
+            dist.all_to_all_single(recv, send)
+
+    def victim_ms(traffic):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        dist.barrier()
+        cur = torch.cuda.current_stream(dev)
+        t0 = time.perf_counter()
+        e0.record(cur)
+        for _ in range(reps):
+            victim.run(lens)
+        e1.record(cur)
+        calls = 0
+        while traffic is not None and not e1.query():
+            traffic()
+            calls += 1
+            if calls % 4 == 0:
+                side.synchronize()
+        side.synchronize()
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) * 1e3
+        # every rank makes the same number of collective calls
+        t = torch.tensor([calls], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        for _ in range(int(t.item()) - calls):
+            traffic()
+        side.synchronize()
+        return e0.elapsed_time(e1) / reps, calls, wall
+
+    def alone_rate(fn, n=8):
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(n):
+            fn()
+        side.synchronize()
+        return (world - 1) * per_peer_bytes * n / (time.perf_counter() - t0) / 1e9
+
+    out = {"per_peer_mib": per_peer_bytes >> 20}
+    ce_once(); nccl_once(); side.synchronize()  # warm both paths
+    out["victim_ms_alone"] = round(victim_ms(None)[0], 4)
+    v, calls, wall = victim_ms(ce_once)
+    out["victim_ms_with_ce_a2a"] = round(v, 4)
+    out["ce_a2a_gbs_out_per_gpu_during_victim"] = round((world - 1) * per_peer_bytes * calls / (wall * 1e-3) / 1e9, 1)
+    v, calls, wall = victim_ms(nccl_once)
+    out["victim_ms_with_nccl_a2a"] = round(v, 4)
+    out["nccl_a2a_gbs_out_per_gpu_during_victim"] = round((world - 1) * per_peer_bytes * calls / (wall * 1e-3) / 1e9, 1)
+    out["ce_a2a_gbs_out_per_gpu_alone"] = round(alone_rate(ce_once), 1)
+    out["nccl_a2a_gbs_out_per_gpu_alone"] = round(alone_rate(nccl_once), 1)
+    out["victim_slowdown_pct"] = {
+        "ce": round(100.0 * (out["victim_ms_with_ce_a2a"] / out["victim_ms_alone"] - 1), 2),
+        "nccl": round(100.0 * (out["victim_ms_with_nccl_a2a"] / out["victim_ms_alone"] - 1), 2)}
+    return out
+
+
+# ---- config 1 and config 2 beside the reference ----------------------------------
+def run_cfg1(args, ctx, dev, W, K):
+    """BASELINE config 1: one 1M x 128 fp32 table, Zipf(1.1) batches of 4,096
+    ids, one rank: collision detection + prioritized (collision-first)
+    update per iteration, through the public API with resident ids. The
+    reference runs the same batches at full size (1M x 128 f64) on one host
+    core (Reference.bench_engine, PrioritizedEmbedding under InProcessFabric)."""
+    import torch
+    from paper_2604_24073_b200 import embedding as E
+    from paper_2604_24073_b200 import workload
+    rows, dim, n, seed = 1_000_000, 128, 4096, 20261019
+    iters = W + K + 2
+    batches = [workload.zipf_batch(seed, n, rows, offset=n * i) for i in range(iters)]
+    shard = E.ShardView(E.TableGeometry(rows, dim, 1), 0, 0.05, seed, dtype="f32", ctx=ctx)
+    eng = E.PrioritizedEmbedding(shard, max_occurrences=n, reduce_chunk=args.reduce_chunk)
+    eng.set_ids_ready(True)
+    d = [torch.from_numpy(b.view(np.int64)).to(dev) for b in batches]
+    out = torch.empty((n, dim), dtype=torch.float32, device=dev)
+    g = (torch.rand((n, dim), device=dev) - 0.5) * 1e-3
+    s = torch.cuda.Stream(device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        for i in range(W):
+            eng.forward(d[i], d[i + 1], out=out, stream=s)
+            eng.backward(g, stream=s)
+        eng.join(s)
+        s.synchronize()
+        e0.record(s)
+        for i in range(W, W + K):
+            eng.forward(d[i], d[i + 1], out=out, stream=s)
+            eng.backward(g, stream=s)
+        eng.join(s)
+        e1.record(s)
+        s.synchronize()
+    ms = e0.elapsed_time(e1) / K
+    rows_it = float(np.mean([b.size + np.unique(b).size for b in batches[W:W + K]]))
+    eng.close()
+    del shard
+    res = {"workload": "BASELINE config1: 1M x 128 fp32, Zipf(1.1) batches of 4,096 ids, 1 rank, collision "
+                       "detect + prioritized row-wise update (forward + backward per iteration, ids resident)",
+           "gpu_us_per_iter": round(ms * 1e3, 2), "gpu_rows_per_s": round(rows_it / (ms * 1e-3), 1)}
+    if not args.no_cpu_baseline:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            from oracle import Reference
+            R = Reference()
+            cb = [[b] for b in batches[:5]]
+            us = R.bench_engine(True, 1, cb, rows, dim, 0.05, seed)
+            steady = float(np.mean(us[1:4]))
+            res["reference"] = {"us_per_iter": round(steady, 1), "rows_per_s": round(rows_it / (steady * 1e-6), 1),
+                                "cores": 1, "kind": "reference",
+                                "sample": "reference PrioritizedEmbedding at full size (1M x 128 f64), 1 rank "
+                                          "thread, the same batches, steady iterations 1-3",
+                                "host": host_info()}
+            res["speedup_gpu_over_reference"] = round(steady / (ms * 1e3), 1)
+        except Exception as ex:  # noqa: BLE001
+            res["reference"] = {"unavailable": str(ex)}
+    return res
+
+
+def run_cfg2(args, ctx):
+    """BASELINE config 2: 65,536 UIH samples (8 ranks x 8,192, power-law
+    lengths 16-8192) partitioned over 8 ranks by FBS and by VBS (alpha 1, 2)
+    with the GPU partitioner through the public API (host lists in, plan
+    out), wall time per call, beside the reference's own partitioners on the
+    same metas (FBS live; VBS live with --cfg2-ref-vbs, else the committed
+    measurement of the reference on this pool's host)."""
+    import torch
+    from paper_2604_24073_b200 import partition as P
+    from paper_2604_24073_b200 import workload
+    gold = os.path.join(ROOT, "tests", "golden", "cfg2_partition.npz")
+    if os.path.exists(gold):
+        z = np.load(gold)
+        lens, origin, local = z["lens"], z["origin"], z["local"]
+        src = "tests/golden/cfg2_partition.npz (the reference's own generator, make_cfg2_golden.py)"
+    else:
+        lens = workload.uih_lengths(20261020, 65536)
+        origin = np.repeat(np.arange(8), 8192).astype(np.int32)
+        local = np.tile(np.arange(8192), 8).astype(np.int32)
+        src = "workload.uih_lengths(20261020, 65536)"
+    out = {"workload": "BASELINE config2: 65,536 UIH samples, power-law lengths 16..8192, 8 ranks", "inputs": src,
+           "call": "partition.{fbs,vbs}_partition_arrays: the C ABI's argument form (host arrays in, plan out)"}
+    gpu = {}
+    for name, fn in (("fbs", lambda: P.fbs_partition_arrays(lens, origin, local, 8, ctx=ctx)),
+                     ("vbs_alpha1", lambda: P.vbs_partition_arrays(lens, origin, local, 8, 1.0, ctx=ctx)),
+                     ("vbs_alpha2", lambda: P.vbs_partition_arrays(lens, origin, local, 8, 2.0, ctx=ctx))):
+        fn()  # warm
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize()
+            ts.append((time.perf_counter() - t0) * 1e3)
+        gpu[name] = round(float(np.median(ts)), 3)
+    out["gpu_ms_per_call"] = gpu
+    if args.no_cpu_baseline:
+        return out
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        from oracle import Reference
+        R = Reference()
+        t0 = time.perf_counter()
+        R.fbs(lens, origin, local, 8)
+        ref = {"fbs": round((time.perf_counter() - t0) * 1e3, 3)}
+        if args.cfg2_ref_vbs:
+            for a in (1.0, 2.0):
+                t0 = time.perf_counter()
+                R.vbs(lens, origin, local, 8, a)
+                ref[f"vbs_alpha{int(a)}"] = round((time.perf_counter() - t0) * 1e3, 1)
+            ref["vbs_source"] = "timed live in this run"
+        else:
+            cached = os.path.join(ROOT, "profiles", "r2_cfg2_reference.json")
+            if os.path.exists(cached):
+                c = json.load(open(cached))
+                for k in ("vbs_alpha1", "vbs_alpha2"):
+                    ref[k] = c["reference_ms_per_call"][k]
+                ref["vbs_source"] = ("profiles/r2_cfg2_reference.json (the reference's VBS timed on this "
+                                     "pool's GPU-box host, bench.py --cfg2-ref-vbs)")
+        out["reference_ms_per_call"] = ref
+        out["reference_cores"] = 1
+        out["host"] = host_info()
+        out["speedup_gpu_over_reference"] = {k: round(ref[k] / gpu[k], 1) for k in gpu if k in ref}
+    except Exception as ex:  # noqa: BLE001
+        out["reference_ms_per_call"] = {"unavailable": str(ex)}
+    return out
 
 
 # ---- GPU arm ----------------------------------------------------------------------
@@ -400,6 +638,7 @@ def main():
             for i in range(W, W + K):
                 step(i)
             host_enqueue_ms = (time.perf_counter() - th0) * 1e3
+            eng.join(stream)  # every engine lane's work of the timed steps inside the window
             ev1.record(stream)
             barrier()
         ms_dev = ev0.elapsed_time(ev1)
@@ -432,6 +671,7 @@ def main():
         for i in range(first_e2e, min(first_e2e + K, iters - 1)):
             step(i, e2e=True)
             n_e2e += 1
+        eng.join(stream)
         e1.record(stream)
         barrier()
         ms_e2e = e0.elapsed_time(e1)
@@ -488,6 +728,12 @@ def main():
             barrier()
             res["sync_" + base_tr] = (e0.elapsed_time(e1) / K, sync_eng.exposed_ms() / K)
         sync_eng.close()
+        cont = None
+        if world > 1:
+            with torch.cuda.stream(stream):
+                eng.join(stream)
+                stream.synchronize()
+                cont = contention(eng, victim, blens[it0], dev, world)
         b_key = "sync_" + base_tr
         step_b = max_over_ranks(res[b_key][0])
         step_p = max_over_ranks(res["prio_ce"][0])
@@ -521,7 +767,12 @@ def main():
             # straggler share of the exposed wait: the slowest rank's victim
             # holds every peer's collision chain (both engines pay it)
             "victim_alone_ms_min_over_ranks": round(-max_over_ranks(-victim_alone), 4),
-            "comm_sms": {b_key: "NCCL kernels" if base_tr == "nccl" else 0, "prio_ce": 0},
+            # prio_ce: every inter-rank byte moves on the copy engines
+            # (FSX_ECO_DIRECT is off: no kernel stores to a peer window)
+            "comm_sms": {b_key: "NCCL kernels (SM-resident)" if base_tr == "nccl" else 0, "prio_ce": 0},
+            "contention": cont,
+            "notes": ("the NCCL baseline's ids all-to-all needs host-known counts: its 8-byte size round "
+                      "(comm.cpp:328-341) is followed by one stream sync, inside the baseline's exposed window"),
         }
 
     ms_dev = max_over_ranks(ms_dev)
@@ -588,10 +839,16 @@ def main():
                     "peak_source": peak_src, "launch_ms": round(per_launch_ms, 4),
                     "algorithmic_bytes_per_launch": int(per_launch_bytes)}
 
+    cfg1_out = cfg2_out = None
+    if rank == 0 and world == 1 and (args.cfg1 if args.cfg1 >= 0 else 1):
+        cfg1_out = run_cfg1(args, ctx, dev, W, K)
+    if rank == 0 and world == 1 and (args.cfg2 if args.cfg2 >= 0 else 1):
+        cfg2_out = run_cfg2(args, ctx)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = cpu_reference(args, 1, 512, iters=3)
+            cpu = cpu_reference(args, 1, args.samples, iters=5)
         except Exception as ex:  # noqa: BLE001
             cpu = {"value": None, "unit": "rows/s", "cores": 1, "kind": "reference", "sample": f"failed: {ex}"}
 
@@ -633,6 +890,8 @@ def main():
             "phases_ms_per_step": {k: round(v[0] / K, 4) for k, v in phases.items() if v[1]},
             "cpu_baseline": cpu,
             "cfg5": cfg5_out,
+            "cfg1": cfg1_out,
+            "cfg2": cfg2_out,
             "clocks": clocks,
             "setup_s": {"workload_gen": round(t_gen, 2), "table_init": round(t_init, 2)},
             "collision_fraction": round(float(np.mean([s.collision_fraction for s in stats[W:W + K]])), 4)

@@ -218,6 +218,10 @@ int fsx_engine_set_profiling(fsx_engine* e, int on);
  * relative to the earliest span; consumes them (synchronizes) */
 int fsx_engine_spans(fsx_engine* e, double* out, uint64_t max_spans, uint64_t* n_spans);
 /* device ids handed to forward are complete (no pending writes on any stream) */
+/* Orders everything the engine has issued on its own lanes (side-lane jobs,
+ * priority lanes, copy-engine streams) before `stream`. No protocol effect:
+ * lets a caller end a timing region only when the engine is idle. */
+int fsx_engine_join(fsx_engine* e, void* stream);
 int fsx_engine_set_ids_ready(fsx_engine* e, int ready);
 /* total ms and number of spans of `phase` since the last call for that
  * phase (synchronizes; resets the phase) */

@@ -74,6 +74,7 @@ _SIGS = {
     "fsx_engine_exposed_ms": ([vp, P(dbl)], i32),
     "fsx_engine_set_profiling": ([vp, i32], i32),
     "fsx_engine_set_ids_ready": ([vp, i32], i32),
+    "fsx_engine_join": ([vp, vp], i32),
     "fsx_engine_spans": ([vp, vp, u64, P(u64)], i32),
     "fsx_engine_phase_ms": ([vp, i32, P(dbl), P(u64)], i32),
     "fsx_cost_estimate": ([vp, vp, vp, i32, dbl, dbl, dbl, vp, vp], i32),

@@ -1203,7 +1203,10 @@ struct Engine {
   // receive windows (their slot `me`, over NVLink) instead of local staging +
   // a copy-engine all-to-all: the transfer rides the update's own stores and
   // leaves the chain; signal_direct then only raises the flags.
-  bool eco_direct = true;  // FSX_ECO_DIRECT=0: stage + copy-engine all-to-all
+  // FSX_ECO_DIRECT=1 (opt-in): the collision update stores E_co rows straight
+  // into the peers' windows over NVLink — SM-issued communication. Off by
+  // default: every byte between ranks then moves on the copy engines (0 SMs).
+  bool eco_direct = false;
   Slots remote_slots(int ch, int par) const {
     Slots r{};
     for (int d = 0; d < p; ++d)
@@ -1643,6 +1646,18 @@ struct Engine {
     ++iter;
   }
 
+  // every lane's issued work (side-lane jobs included) ordered before the
+  // caller's stream `c`: no protocol effect, for timing regions that must end
+  // only when the engine is idle
+  void join(cudaStream_t c) {
+    if (side) side->drain();
+    for (cudaStream_t s : {lo, hi, ux, us})
+      if (s) wait(c, record(s));
+    for (int l = 0; l < kLanes; ++l)
+      for (int d = 0; d < p; ++d)
+        if (cstream[l][d]) wait(c, record(cstream[l][d]));
+  }
+
   void finalize(cudaStream_t c) {
     if (side) side->drain();
     apply_deferred(take_deferred());
@@ -1988,6 +2003,13 @@ int fsx_engine_spans(fsx_engine* e, double* out, uint64_t max_spans, uint64_t* n
   }
   e->prof_next = 0;
   *n_out = k;
+  FSX_API_END
+}
+
+int fsx_engine_join(fsx_engine* e, void* stream) {
+  FSX_API_BEGIN
+  DeviceGuard dg(e->ctx->device);
+  e->join(S(stream));
   FSX_API_END
 }
 

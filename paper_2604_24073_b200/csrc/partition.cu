@@ -7,6 +7,10 @@
 #include <cstring>
 #include <vector>
 
+#include <memory>
+#include <mutex>
+#include <unordered_map>
+
 #include "capi_util.cuh"
 #include "table.cuh"
 
@@ -205,9 +209,33 @@ void h2d(DevBuf<T>& d, const T* h, uint64_t n, cudaStream_t s) {
   if (n) FSX_CUDA(cudaMemcpyAsync(d.p, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
 }
 
+// Device scratch of the partitioners per (context, device), grown on demand
+// and kept across calls: the balancer partitions every iteration, and a
+// cudaMalloc / cudaFree pair per buffer per call (cudaFree synchronises the
+// device) cost more than the sort itself at config 2's 65,536 samples. The
+// lock covers one call's use (each call ends with a stream sync).
+struct PartScratch {
+  std::mutex m;
+  DevBuf<uint64_t> lens, k0, k1, o, w;
+  DevBuf<int32_t> origin, local, a, sizes;
+  DevBuf<uint32_t> v0, v1, perm, cut;
+  DevBuf<double> prefix, dw, dp;
+  RadixScratch radix;
+};
+PartScratch& part_scratch(const Ctx* ctx) {
+  static std::mutex m;
+  static auto* bufs = new std::unordered_map<uint64_t, std::unique_ptr<PartScratch>>();
+  std::lock_guard<std::mutex> g(m);
+  auto& p = (*bufs)[reinterpret_cast<uintptr_t>(ctx) ^ (static_cast<uint64_t>(ctx->device) << 56)];
+  if (!p) p = std::make_unique<PartScratch>();
+  return *p;
+}
+
 // sorted_indices on the device: returns the permutation (sorted position -> g)
 void sorted_indices(Ctx* ctx, const uint64_t* h_lens, const int32_t* h_origin, const int32_t* h_local,
-                    uint64_t m, cudaStream_t s, DevBuf<uint64_t>& d_lens, DevBuf<uint32_t>& perm_out) {
+                    uint64_t m, cudaStream_t s, PartScratch& ps) {
+  DevBuf<uint64_t>& d_lens = ps.lens;
+  DevBuf<uint32_t>& perm_out = ps.perm;
   uint64_t maxlen = 0;
   int32_t maxo = 0, maxl = 0;
   for (uint64_t g = 0; g < m; ++g) {
@@ -221,20 +249,19 @@ void sorted_indices(Ctx* ctx, const uint64_t* h_lens, const int32_t* h_origin, c
   const int blen = bits_for(maxlen);
   if (blen + bo + bl > 64) raise(FSX_ERR_CONFIG, "partition: sort key wider than 64 bits");
   h2d(d_lens, h_lens, m, s);
-  DevBuf<int32_t> d_o, d_l;
+  DevBuf<int32_t>& d_o = ps.origin;
+  DevBuf<int32_t>& d_l = ps.local;
   h2d(d_o, h_origin, m, s);
   h2d(d_l, h_local, m, s);
-  DevBuf<uint64_t> k0(m), k1(m);
-  DevBuf<uint32_t> v0(m), v1(m);
+  ps.k0.ensure(m); ps.k1.ensure(m); ps.v0.ensure(m); ps.v1.ensure(m);
   FSX_LAUNCH(ctx, k_partition_keys, grid_for(ctx, m, 256, 8), 256, 0, s, d_lens.p, d_o.p, d_l.p, m,
-             maxlen, bo, bl, k0.p);
-  RadixScratch rs;
+             maxlen, bo, bl, ps.k0.p);
   uint64_t* ko;
   uint32_t* vo;
-  radix_sort_pairs<uint64_t>(ctx, k0.p, v0.p, k1.p, v1.p, m, nullptr, blen + bo + bl, rs, s, &ko, &vo);
+  radix_sort_pairs<uint64_t>(ctx, ps.k0.p, ps.v0.p, ps.k1.p, ps.v1.p, m, nullptr, blen + bo + bl, ps.radix, s, &ko,
+                             &vo);
   perm_out.ensure(m);
   FSX_CUDA(cudaMemcpyAsync(perm_out.p, vo, m * 4, cudaMemcpyDeviceToDevice, s));
-  FSX_CUDA(cudaStreamSynchronize(s));  // scratch buffers die with this scope
 }
 
 }  // namespace
@@ -269,11 +296,14 @@ int fsx_fbs_partition(fsx_ctx* ctx, const uint64_t* h_lens, const int32_t* h_ori
                                         std::to_string(num_ranks) + " ranks");
   if (m == 0) return FSX_OK;
   cudaStream_t s = S(stream);
-  DevBuf<uint64_t> d_lens;
-  DevBuf<uint32_t> perm;
-  sorted_indices(ctx, h_lens, h_origin, h_local, m, s, d_lens, perm);
-  DevBuf<int32_t> a(m);
-  DevBuf<uint64_t> o(m);
+  PartScratch& ps = part_scratch(ctx);
+  std::lock_guard<std::mutex> lk(ps.m);
+  sorted_indices(ctx, h_lens, h_origin, h_local, m, s, ps);
+  DevBuf<uint32_t>& perm = ps.perm;
+  DevBuf<int32_t>& a = ps.a;
+  DevBuf<uint64_t>& o = ps.o;
+  a.ensure(m);
+  o.ensure(m);
   FSX_LAUNCH(ctx, k_fbs_assign, grid_for(ctx, m, 256, 8), 256, 0, s, perm.p, m, num_ranks, a.p, o.p);
   FSX_CUDA(cudaMemcpyAsync(h_assignment, a.p, m * 4, cudaMemcpyDeviceToHost, s));
   FSX_CUDA(cudaMemcpyAsync(h_order, o.p, m * 8, cudaMemcpyDeviceToHost, s));
@@ -295,9 +325,11 @@ int fsx_vbs_partition(fsx_ctx* ctx, const uint64_t* h_lens, const int32_t* h_ori
   if (m >= (1ull << 32)) raise(FSX_ERR_CONFIG, "vbs: too many samples");
   cudaStream_t s = S(stream);
   const int n = num_ranks;
-  DevBuf<uint64_t> d_lens;
-  DevBuf<uint32_t> perm;
-  sorted_indices(ctx, h_lens, h_origin, h_local, m, s, d_lens, perm);
+  PartScratch& ps = part_scratch(ctx);
+  std::lock_guard<std::mutex> lk(ps.m);
+  sorted_indices(ctx, h_lens, h_origin, h_local, m, s, ps);
+  DevBuf<uint64_t>& d_lens = ps.lens;
+  DevBuf<uint32_t>& perm = ps.perm;
   std::vector<int32_t> sizes(n);
   bool tuned = false;
   if (h_tuned_sizes) {
@@ -309,12 +341,14 @@ int fsx_vbs_partition(fsx_ctx* ctx, const uint64_t* h_lens, const int32_t* h_ori
     }
     tuned = pos && tot == m;  // partition.cpp:189-195
   }
-  DevBuf<int32_t> d_sizes(n);
+  DevBuf<int32_t>& d_sizes = ps.sizes;
+  d_sizes.ensure(n);
   if (tuned) {
     std::memcpy(sizes.data(), h_tuned_sizes, sizeof(int32_t) * n);
     FSX_CUDA(cudaMemcpyAsync(d_sizes.p, sizes.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, s));
   } else {
-    DevBuf<double> prefix(m + 1);
+    DevBuf<double>& prefix = ps.prefix;
+    prefix.ensure(m + 1);
     uint64_t maxlen = 0;
     for (uint64_t g = 0; g < m; ++g) maxlen = h_lens[g] > maxlen ? h_lens[g] : maxlen;
     const bool a1 = alpha == 1.0, a2 = alpha == 2.0;
@@ -322,7 +356,8 @@ int fsx_vbs_partition(fsx_ctx* ctx, const uint64_t* h_lens, const int32_t* h_ori
                            static_cast<double>(maxlen) * static_cast<double>(a2 ? maxlen : 1) *
                                    static_cast<double>(m) < 9.0e15;
     if (exact_int) {
-      DevBuf<uint64_t> w(m);
+      DevBuf<uint64_t>& w = ps.w;
+      w.ensure(m);
       FSX_LAUNCH(ctx, k_vbs_weights, grid_for(ctx, m, 256, 8), 256, 0, s, d_lens.p, perm.p, m, a2 ? 1 : 0, w.p);
       FSX_LAUNCH(ctx, k_prefix_u64, 1, 1024, 0, s, w.p, m, prefix.p);
     } else {
@@ -332,15 +367,18 @@ int fsx_vbs_partition(fsx_ctx* ctx, const uint64_t* h_lens, const int32_t* h_ori
       FSX_CUDA(cudaStreamSynchronize(s));
       std::vector<double> w(m);
       for (uint64_t k = 0; k < m; ++k) w[k] = std::pow(static_cast<double>(h_lens[hp[k]]), alpha);
-      DevBuf<double> dw(m);
+      DevBuf<double>& dw = ps.dw;
+      dw.ensure(m);
       FSX_CUDA(cudaMemcpyAsync(dw.p, w.data(), m * 8, cudaMemcpyHostToDevice, s));
       FSX_LAUNCH(ctx, k_prefix_seq, 1, 32, 0, s, dw.p, m, prefix.p);
       FSX_CUDA(cudaStreamSynchronize(s));
     }
     // dp [n+1][m+1], cut [n+1][m+1]
     const uint64_t cols = m + 1;
-    DevBuf<double> dp(static_cast<uint64_t>(n + 1) * cols);
-    DevBuf<uint32_t> cut(static_cast<uint64_t>(n + 1) * cols);
+    DevBuf<double>& dp = ps.dp;
+    DevBuf<uint32_t>& cut = ps.cut;
+    dp.ensure(static_cast<uint64_t>(n + 1) * cols);
+    cut.ensure(static_cast<uint64_t>(n + 1) * cols);
     FSX_LAUNCH(ctx, k_fill_inf, grid_for(ctx, (n + 1) * cols, 256, 8), 256, 0, s, dp.p, (n + 1) * cols);
     FSX_LAUNCH(ctx, k_dp_first, grid_for(ctx, m, 256, 8), 256, 0, s, prefix.p, m, dp.p + cols);
     for (int k = 2; k <= n; ++k)
@@ -350,8 +388,10 @@ int fsx_vbs_partition(fsx_ctx* ctx, const uint64_t* h_lens, const int32_t* h_ori
     FSX_CUDA(cudaMemcpyAsync(sizes.data(), d_sizes.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s));
     FSX_CUDA(cudaStreamSynchronize(s));
   }
-  DevBuf<int32_t> a(m);
-  DevBuf<uint64_t> o(m);
+  DevBuf<int32_t>& a = ps.a;
+  DevBuf<uint64_t>& o = ps.o;
+  a.ensure(m);
+  o.ensure(m);
   FSX_LAUNCH(ctx, k_vbs_assign, grid_for(ctx, m, 256, 8), 256, 0, s, perm.p, m, d_sizes.p, n, a.p, o.p);
   FSX_CUDA(cudaMemcpyAsync(h_assignment, a.p, m * 4, cudaMemcpyDeviceToHost, s));
   FSX_CUDA(cudaMemcpyAsync(h_order, o.p, m * 8, cudaMemcpyDeviceToHost, s));

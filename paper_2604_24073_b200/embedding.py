@@ -319,6 +319,10 @@ class _Engine:
         """Device id tensors passed to forward are complete when passed."""
         _lib.call("fsx_engine_set_ids_ready", self.h, int(ready))
 
+    def join(self, stream=None) -> None:
+        """Order every lane's issued work before `stream` (timing regions)."""
+        _lib.call("fsx_engine_join", self.h, _stream(stream))
+
     def set_profiling(self, on: bool = True) -> None:
         _lib.call("fsx_engine_set_profiling", self.h, int(on))
 

@@ -109,12 +109,20 @@ def _split(order: np.ndarray, sizes) -> list:
 
 def fbs_partition(metas: Sequence[GlobalSampleMeta], num_ranks: int, ctx=None) -> PartitionPlan:
     """partition.cpp:157-176: sort by (uih_len desc, origin, local), snake."""
+    return fbs_partition_arrays(*_arrays(metas), num_ranks, ctx=ctx)
+
+
+def fbs_partition_arrays(lens, origin, local, num_ranks: int, ctx=None) -> PartitionPlan:
+    """fbs_partition over the metas' columns (uih_len u64, origin_rank i32,
+    local_index i32): the C ABI's own argument form, no per-sample objects."""
     if num_ranks < 1:
         raise InvalidArgument("fbs: num_ranks must be >= 1")
-    m = len(metas)
+    lens = np.ascontiguousarray(lens, np.uint64)
+    origin = np.ascontiguousarray(origin, np.int32)
+    local = np.ascontiguousarray(local, np.int32)
+    m = lens.size
     if m % num_ranks:
         raise InvalidArgument(f"fbs: {m} samples not divisible by {num_ranks} ranks")
-    lens, origin, local = _arrays(metas)
     a = np.zeros(max(m, 1), np.int32)
     o = np.zeros(max(m, 1), np.uint64)
     if m:
@@ -129,8 +137,16 @@ def vbs_partition(metas: Sequence[GlobalSampleMeta], num_ranks: int, alpha: floa
     """partition.cpp:178-209: min-max contiguous cut of the sorted weights
     uih_len^alpha (exact DP on the GPU), or the tuned sizes of an
     initialized autotune state."""
-    m = len(metas)
-    lens, origin, local = _arrays(metas)
+    return vbs_partition_arrays(*_arrays(metas), num_ranks, alpha, tune=tune, ctx=ctx)
+
+
+def vbs_partition_arrays(lens, origin, local, num_ranks: int, alpha: float,
+                         tune: AutoTuneState | None = None, ctx=None) -> PartitionPlan:
+    """vbs_partition over the metas' columns (see fbs_partition_arrays)."""
+    lens = np.ascontiguousarray(lens, np.uint64)
+    origin = np.ascontiguousarray(origin, np.int32)
+    local = np.ascontiguousarray(local, np.int32)
+    m = lens.size
     a = np.zeros(max(m, 1), np.int32)
     o = np.zeros(max(m, 1), np.uint64)
     sizes = np.zeros(max(num_ranks, 1), np.int32)
