@@ -331,51 +331,57 @@ def contention(eng, victim, lens, dev, world, per_peer_bytes=32 << 20, reps=4):
         with torch.cuda.stream(side):
             dist.all_to_all_single(recv, send)
 
-    def victim_ms(traffic):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        dist.barrier()
-        cur = torch.cuda.current_stream(dev)
-        t0 = time.perf_counter()
-        e0.record(cur)
-        for _ in range(reps):
-            victim.run(lens)
-        e1.record(cur)
-        calls = 0
-        while traffic is not None and not e1.query():
-            traffic()
-            calls += 1
-            if calls % 4 == 0:
-                side.synchronize()
-        side.synchronize()
-        torch.cuda.synchronize()
-        wall = (time.perf_counter() - t0) * 1e3
-        # every rank makes the same number of collective calls
-        t = torch.tensor([calls], dtype=torch.int64, device=dev)
+    def agree_max(x, op=None):
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        for _ in range(int(t.item()) - calls):
-            traffic()
-        side.synchronize()
-        return e0.elapsed_time(e1) / reps, calls, wall
+        return float(t.item())
 
-    def alone_rate(fn, n=8):
+    def per_call_ms(fn, n=6):
         torch.cuda.synchronize()
         dist.barrier()
         t0 = time.perf_counter()
         for _ in range(n):
             fn()
         side.synchronize()
-        return (world - 1) * per_peer_bytes * n / (time.perf_counter() - t0) / 1e9
+        return agree_max((time.perf_counter() - t0) * 1e3 / n)
+
+    def victim_ms(traffic, calls=0):
+        """The victim on the compute stream while this rank issues exactly
+        `calls` all-to-alls (the same count on every rank: collectives must
+        match) on the side stream."""
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        dist.barrier()
+        cur = torch.cuda.current_stream(dev)
+        e0.record(cur)
+        for _ in range(reps):
+            victim.run(lens)
+        e1.record(cur)
+        t0 = time.perf_counter()
+        for c in range(calls):
+            traffic()
+            if c % 4 == 3:
+                side.synchronize()
+        side.synchronize()
+        wall = (time.perf_counter() - t0) * 1e3
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps, wall
+
+    def alone_rate(fn, n=8):
+        return (world - 1) * per_peer_bytes / (per_call_ms(fn, n) * 1e-3) / 1e9
 
     out = {"per_peer_mib": per_peer_bytes >> 20}
     ce_once(); nccl_once(); side.synchronize()  # warm both paths
-    out["victim_ms_alone"] = round(victim_ms(None)[0], 4)
-    v, calls, wall = victim_ms(ce_once)
-    out["victim_ms_with_ce_a2a"] = round(v, 4)
-    out["ce_a2a_gbs_out_per_gpu_during_victim"] = round((world - 1) * per_peer_bytes * calls / (wall * 1e-3) / 1e9, 1)
-    v, calls, wall = victim_ms(nccl_once)
-    out["victim_ms_with_nccl_a2a"] = round(v, 4)
-    out["nccl_a2a_gbs_out_per_gpu_during_victim"] = round((world - 1) * per_peer_bytes * calls / (wall * 1e-3) / 1e9, 1)
+    alone = victim_ms(None)[0]
+    out["victim_ms_alone"] = round(alone, 4)
+    for name, fn in (("ce", ce_once), ("nccl", nccl_once)):
+        # enough calls to cover the victim's whole run, agreed across ranks
+        calls = int(np.ceil(agree_max(alone * reps / per_call_ms(fn))))
+        v, wall = victim_ms(fn, calls)
+        out[f"victim_ms_with_{name}_a2a"] = round(v, 4)
+        out[f"{name}_a2a_calls"] = calls
+        out[f"{name}_a2a_gbs_out_per_gpu_during_victim"] = round((world - 1) * per_peer_bytes * calls /
+                                                                 (wall * 1e-3) / 1e9, 1)
     out["ce_a2a_gbs_out_per_gpu_alone"] = round(alone_rate(ce_once), 1)
     out["nccl_a2a_gbs_out_per_gpu_alone"] = round(alone_rate(nccl_once), 1)
     out["victim_slowdown_pct"] = {

@@ -27,14 +27,14 @@ from paper_2604_24073_b200.comm import ProcessGroupFabric  # noqa: E402
 OVERSUB = os.environ.get("FSX_MP_OVERSUB") == "1"
 
 
-def run(prio, dtype, batches, geom, rank, world, dev, chunk, presum=False):
+def run(prio, dtype, batches, geom, rank, world, dev, chunk, presum=False, transport="ce"):
     fabric = ProcessGroupFabric(rank, world, dev)
     ctx = E.Context(dev, rank, world)
     shard = E.ShardView(geom, rank, 0.05, 3, dtype=dtype, ctx=ctx)
     cap = max(len(b) for it in batches for b in it)
     cls = E.PrioritizedEmbedding if prio else E.SynchronizedEmbedding
     kw = {"presum": True} if (prio and presum) else {}
-    eng = cls(shard, fabric.communicator(), max_occurrences=cap, reduce_chunk=chunk, **kw)
+    eng = cls(shard, fabric.communicator(), max_occurrences=cap, reduce_chunk=chunk, transport=transport, **kw)
     s = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(s):
         for i in range(len(batches)):
@@ -80,28 +80,31 @@ def main():
                for i in range(iters)]
     geom = E.TableGeometry(rows, dim, world)
     chunk = 0 if dtype == "f64" else 64
-    t_sync, _ = run(False, dtype, batches, geom, rank, world, dev, chunk)
-    presum = len(sys.argv) > 2 and sys.argv[2] == "presum"
+    presum = "presum" in sys.argv[2:]
+    # "nccl": the blocking baseline over NCCL (the comparison transport) must
+    # produce the same table bit for bit
+    sync_tr = "nccl" if "nccl" in sys.argv[2:] and not OVERSUB else "ce"
+    t_sync, _ = run(False, dtype, batches, geom, rank, world, dev, chunk, transport=sync_tr)
     t_prio, stats = run(True, dtype, batches, geom, rank, world, dev, chunk, presum)
     ok = True
     if rank == 0:
         from oracle import Oracle
         O = Oracle()
-        want, want_stats = O.run_engine(world, batches, rows, dim, 0.05, 3, with_stats=True)
-        same = np.array_equal(t_sync.view(np.uint64), t_prio.view(np.uint64))
-        print(f"[mp] world={world} dtype={dtype} presum={presum} sync==prio bitwise: {same}")
-        ok &= same or presum  # pre-summed collision gradients: fp32 tolerance, not bitwise
-        if dtype == "f64" and not presum:
-            exact = np.array_equal(t_prio.view(np.uint64), want.view(np.uint64))
-            got_stats = np.array([[s.collision_rows, s.unique_next_rows, s.blocking_bytes] for s in stats],
-                                 np.uint64)
-            st_ok = np.array_equal(got_stats, want_stats)
-            print(f"[mp] f64 bit-exact vs oracle: {exact}; stats equal: {st_ok}")
-            ok &= exact and st_ok
-        else:
-            nrm = float(np.max(np.abs(t_prio - want)) / np.max(np.abs(want)))
-            print(f"[mp] f32 normwise rel err vs f64 oracle: {nrm:.3e}")
-            ok &= nrm < 1e-6
+        f32 = dtype == "f32"
+        # bitwise against the oracle's model of the same numeric path: the
+        # fp32 storage model, the chunk association and (prio) PRESUM
+        want_s, want_stats = O.run_engine(world, batches, rows, dim, 0.05, 3, with_stats=True, store_f32=f32,
+                                          reduce_chunk=chunk)
+        want_p, _ = O.run_engine(world, batches, rows, dim, 0.05, 3, store_f32=f32, reduce_chunk=chunk,
+                                 presum=presum)
+        ok_s = np.array_equal(t_sync.view(np.uint64), want_s.view(np.uint64))
+        ok_p = np.array_equal(t_prio.view(np.uint64), want_p.view(np.uint64))
+        got_stats = np.array([[s.collision_rows, s.unique_next_rows, s.blocking_bytes] for s in stats], np.uint64)
+        st_ok = np.array_equal(got_stats, want_stats)
+        print(f"[mp] world={world} dtype={dtype} chunk={chunk} presum={presum} sync transport={sync_tr}: "
+              f"sync bit-exact vs oracle {ok_s}, "
+              f"prio bit-exact vs oracle {ok_p}, stats equal {st_ok}")
+        ok &= ok_s and ok_p and st_ok
         print("MP_OK" if ok else "MP_FAIL", flush=True)
     dist.barrier()
     dist.destroy_process_group()

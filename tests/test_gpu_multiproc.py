@@ -16,15 +16,19 @@ def _ngpus():
     return torch.cuda.device_count() if torch.cuda.is_available() else 0
 
 
-@pytest.mark.parametrize("dtype", ["f64", "f32"])
-def test_multiprocess_engine_parity(dtype):
+@pytest.mark.parametrize("dtype,flags", [("f64", []), ("f32", []), ("f32", ["presum"]), ("f64", ["nccl"]),
+                                         ("f32", ["presum", "nccl"])])
+def test_multiprocess_engine_parity(dtype, flags):
+    """One process per GPU: the blocking engine (copy engines, or NCCL with
+    "nccl") and the prioritized engine (PRESUM with "presum") bit-exact
+    against the oracle's model of the same numeric path."""
     n = _ngpus()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     world = min(n, 4)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "mp_engine_check.py"),
-           dtype]
+           dtype] + flags
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0 and "MP_OK" in r.stdout
