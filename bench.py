@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--cfg2", type=int, default=-1,
                     help="also time config 2 (FBS / VBS over 65,536 samples, 8 ranks) on the GPU beside the "
                          "reference's FBS; default: on at N = 1")
+    ap.add_argument("--cfg3", type=int, default=-1,
+                    help="also time config 3's pooled lookup + scatter (8 x 10M x 128 fp32 tables, bags of "
+                         "(sample, table)); default: on at N = 1")
     ap.add_argument("--cfg2-ref-vbs", action="store_true",
                     help="time the reference's VBS (alpha 1 and 2, ~60-80 s each) live instead of citing "
                          "profiles/r2_cfg2_reference.json")
@@ -388,6 +391,86 @@ def contention(eng, victim, lens, dev, world, per_peer_bytes=32 << 20, reps=4):
         "ce": round(100.0 * (out["victim_ms_with_ce_a2a"] / out["victim_ms_alone"] - 1), 2),
         "nccl": round(100.0 * (out["victim_ms_with_nccl_a2a"] / out["victim_ms_alone"] - 1), 2)}
     return out
+
+
+# ---- config 3: pooled lookup + scatter ---------------------------------------------
+def run_cfg3(args, ctx, dev, W, K, rank=0):
+    """BASELINE config 3's operator at one GPU's share: 8 tables x 10M rows x
+    128 fp32 (41 GB), 2,048 UIH samples per iteration, every (sample, table)
+    bag sum-pooled (PooledEmbedding: fused pooled gather + the backward's row
+    plan), then each bag's gradient scattered to its tokens and applied
+    (collision-free SGD with the chunk association). All 8 tables are local at
+    one rank (table-wise ownership gives one table per GPU at 8 GPUs; the
+    owner-side work per bag is the same). Ids resident; inputs >> L2."""
+    import torch
+    from paper_2604_24073_b200 import embedding as E
+    from paper_2604_24073_b200 import workload
+    T, R, dim = 8, args.rows_per_table, 128
+    iters = W + K + 1
+    bag_ids, bag_offs, tokens = [], [], []
+    for i in range(iters):
+        lens, ids = workload.cfg_tokens(args.seed + 3, i, rank, args.samples, T, R)
+        t = ids // np.uint64(R)
+        smp = np.repeat(np.arange(lens.size), lens.astype(np.int64))
+        order = np.lexsort((np.arange(ids.size), t, smp))  # bags = (sample, table), token order kept
+        key = smp[order] * T + t[order].astype(np.int64)
+        counts = np.bincount(key, minlength=lens.size * T)
+        bag_ids.append(ids[order])
+        bag_offs.append(np.concatenate([[0], np.cumsum(counts)]).astype(np.uint64))
+        tokens.append(ids.size)
+    shard = E.ShardView(E.TableGeometry(T * R, dim, 1), 0, 0.05, 7, dtype="f32", ctx=ctx)
+    cap = max(tokens) + 1
+    pe = E.PooledEmbedding(shard, max_occurrences=cap, max_bags=args.samples * T, reduce_chunk=args.reduce_chunk)
+    d_ids = [torch.from_numpy(b.view(np.int64)).to(dev) for b in bag_ids]
+    d_offs = [torch.from_numpy(o.view(np.int64)).to(dev) for o in bag_offs]
+    out = torch.empty((args.samples * T, dim), dtype=torch.float32, device=dev)
+    g = (torch.rand((args.samples * T, dim), device=dev) - 0.5) * 1e-3
+    s = torch.cuda.Stream(device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ef, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fwd_ms = bwd_ms = 0.0
+    with torch.cuda.stream(s):
+        for i in range(W):
+            pe.forward(d_ids[i], d_offs[i], out=out, stream=s)
+            pe.backward(g, stream=s)
+        s.synchronize()
+        e0.record(s)
+        for i in range(W, W + K):
+            pe.forward(d_ids[i], d_offs[i], out=out, stream=s)
+            pe.backward(g, stream=s)
+        e1.record(s)
+        s.synchronize()
+        # forward / backward split (separate pass: events between the halves)
+        for i in range(W, W + K):
+            ef.record(s)
+            pe.forward(d_ids[i], d_offs[i], out=out, stream=s)
+            eb.record(s)
+            pe.backward(g, stream=s)
+            s.synchronize()
+            fwd_ms += ef.elapsed_time(eb)
+    ms = e0.elapsed_time(e1) / K
+    fwd_ms /= K
+    ntok = float(np.mean(tokens[W:W + K]))
+    uq = float(np.mean([np.unique(b).size for b in bag_ids[W:W + K]]))
+    nb = args.samples * T
+    rb = dim * 4
+    # forward: each token's id + row read, each bag row written; the
+    # backward's sort/plan traffic is excluded (index work, bytes << rows)
+    fwd_bytes = ntok * (8 + rb) + nb * rb
+    peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else PEAKS_FALLBACK["hbm_gbs"]
+    pe.close()
+    del shard
+    torch.cuda.synchronize()
+    return {"workload": "BASELINE config3 operator, one GPU's share: 8 tables x 10M x 128 fp32, 2,048 UIH samples, "
+                        "sum-pooled (sample, table) bags, bag gradients scattered to tokens + row update",
+            "bags_per_iter": nb, "tokens_per_iter": int(ntok), "unique_rows_per_iter": int(uq),
+            "ms_per_iter": round(ms, 4), "forward_ms": round(fwd_ms, 4),
+            "rows_per_s": round((ntok + uq) / (ms * 1e-3), 1),
+            "forward_roofline": {"bound": "hbm", "achieved": round(fwd_bytes / (fwd_ms * 1e-3) / 1e9, 1),
+                                 "peak": peak, "unit": "GB/s",
+                                 "frac": round(fwd_bytes / (fwd_ms * 1e-3) / 1e9 / peak, 4),
+                                 "note": "forward includes the backward's row sort + plan (index work)"}}
 
 
 # ---- config 1 and config 2 beside the reference ----------------------------------
@@ -845,11 +928,13 @@ def main():
                     "peak_source": peak_src, "launch_ms": round(per_launch_ms, 4),
                     "algorithmic_bytes_per_launch": int(per_launch_bytes)}
 
-    cfg1_out = cfg2_out = None
+    cfg1_out = cfg2_out = cfg3_out = None
     if rank == 0 and world == 1 and (args.cfg1 if args.cfg1 >= 0 else 1):
         cfg1_out = run_cfg1(args, ctx, dev, W, K)
     if rank == 0 and world == 1 and (args.cfg2 if args.cfg2 >= 0 else 1):
         cfg2_out = run_cfg2(args, ctx)
+    if rank == 0 and world == 1 and (args.cfg3 if args.cfg3 >= 0 else 1):
+        cfg3_out = run_cfg3(args, ctx, dev, W, K)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -898,6 +983,7 @@ def main():
             "cfg5": cfg5_out,
             "cfg1": cfg1_out,
             "cfg2": cfg2_out,
+            "cfg3": cfg3_out,
             "clocks": clocks,
             "setup_s": {"workload_gen": round(t_gen, 2), "table_init": round(t_init, 2)},
             "collision_fraction": round(float(np.mean([s.collision_fraction for s in stats[W:W + K]])), 4)

@@ -131,6 +131,24 @@ int fsx_table_download(fsx_table* t, double* h_values);
 /* overwrite the shard from a host f64 array (test / checkpoint-restore aid) */
 int fsx_table_upload(fsx_table* t, const double* h_values);
 
+/* ---- pooled (bag) lookup + scatter: BASELINE config 3 ------- */
+/* No reference operator (the reference's toy model mean-pools whole samples,
+ * pipeline.cpp:59-67); restated in oracle/fsx_oracle.c fso_pooled_*.
+ * forward: d_out[b] (n_bags x dim, the table's type) = sum of row(ids[k]) over
+ * k in [offs[b], offs[b+1]) in token order (f64, one rounding); it also plans
+ * the backward (tokens sorted by row). Bad ids raise FSX_ERR_DOMAIN at the next
+ * sync (fsx_ctx_sync). backward: token k of bag b takes gradient row
+ * d_bag_grads[b]; rows are updated as fsx_table_sgd_update with the chunk
+ * association `reduce_chunk` (0: one left fold per row). Asynchronous on
+ * `stream`; one forward per backward. */
+typedef struct fsx_pooled fsx_pooled;
+int fsx_pooled_create(fsx_table* t, uint64_t max_occurrences, uint64_t max_bags, uint32_t reduce_chunk,
+                      fsx_pooled** out);
+int fsx_pooled_destroy(fsx_pooled* p);
+int fsx_pooled_forward(fsx_pooled* p, const uint64_t* d_ids, const uint64_t* d_bag_offsets, uint64_t n_bags,
+                       uint64_t n_ids, void* d_out, void* stream);
+int fsx_pooled_backward(fsx_pooled* p, const void* d_bag_grads, void* stream);
+
 /* ---- engines: Synchronized / Prioritized embedding ------------------------ */
 typedef struct fsx_engine fsx_engine;
 

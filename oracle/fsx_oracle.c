@@ -438,6 +438,67 @@ int fso_run_engine_ex2(int world, int iters, const uint64_t* ids, const uint64_t
   return FSO_OK;
 }
 
+/* ---- pooled (bag) lookup + scatter -------------------------------------------
+ * No reference operator exists (config 3's pooled lookup is an extension; the
+ * reference's toy model mean-pools whole samples, pipeline.cpp:59-67). This is
+ * the restatement of the product's fsx_pooled_* semantics, on a one-shard
+ * table [total_rows x dim]:
+ *   forward : out[b] = left fold from 0.0, in token order, of row(ids[k]) for
+ *             the bag's tokens k in [offs[b], offs[b+1]) (f64; rounded to float
+ *             when store_f32)
+ *   backward: token k of bag b takes gradient row g[b]; each row's tokens in
+ *             (row, token) order are chunk-folded (chunk_fold) and applied as
+ *             ShardView::apply_gradients (embedding.cpp:148-181). */
+int fso_pooled_forward(const double* table, uint64_t total_rows, uint32_t dim, const uint64_t* ids,
+                       const uint64_t* offs, uint64_t n_bags, int store_f32, double* out) {
+  for (uint64_t b = 0; b < n_bags; ++b)
+    for (uint32_t d = 0; d < dim; ++d) {
+      double acc = 0.0;
+      for (uint64_t k = offs[b]; k < offs[b + 1]; ++k) {
+        if (ids[k] >= total_rows)
+          return fail(FSO_DOMAIN, "embedding: row id %llu out of range (table has %llu rows)", ids[k], total_rows);
+        acc += table[ids[k] * dim + d];
+      }
+      out[b * dim + d] = store_f32 ? (double)(float)acc : acc;
+    }
+  return FSO_OK;
+}
+
+int fso_pooled_backward(double* table, uint64_t total_rows, uint32_t dim, double lr, const uint64_t* ids,
+                        const uint64_t* offs, uint64_t n_bags, const double* bag_grads, int store_f32,
+                        uint32_t reduce_chunk) {
+  uint64_t n = offs[n_bags];
+  occ_t* occ = malloc((n + 1) * sizeof(occ_t));
+  double* served = malloc(((size_t)n * dim + 1) * 8);  /* per-token gradient rows */
+  for (uint64_t b = 0; b < n_bags; ++b)
+    for (uint64_t k = offs[b]; k < offs[b + 1]; ++k) {
+      if (ids[k] >= total_rows) {
+        free(occ); free(served);
+        return fail(FSO_DOMAIN, "embedding: row id %llu out of range (table has %llu rows)", ids[k], total_rows);
+      }
+      occ[k].id = ids[k];
+      occ[k].seq = k;
+      memcpy(served + k * dim, bag_grads + b * dim, (size_t)dim * 8);
+    }
+  qsort(occ, n, sizeof(occ_t), cmp_occ);
+  uint64_t k = 0;
+  while (k < n) {
+    uint64_t e = k;
+    while (e < n && occ[e].id == occ[k].id) ++e;
+    double* row = table + occ[k].id * dim;
+    for (uint32_t d = 0; d < dim; ++d) {
+      /* the gradient rows are used as given (scale 1, shift 0: fixture()
+       * returns them unchanged, in float when store_f32 — they are floats) */
+      double acc = chunk_fold(occ + k, e - k, d, dim, served, 1.0, 0.0, 0, reduce_chunk);
+      row[d] -= lr * acc;
+      if (store_f32) row[d] = (double)(float)row[d];
+    }
+    k = e;
+  }
+  free(occ); free(served);
+  return FSO_OK;
+}
+
 /* ---- partition.cpp --------------------------------------------------------- */
 typedef struct { uint64_t len; int origin, local; uint64_t g; } meta_t;
 static int cmp_meta(const void* a, const void* b) {

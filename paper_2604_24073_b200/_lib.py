@@ -75,6 +75,10 @@ _SIGS = {
     "fsx_engine_set_profiling": ([vp, i32], i32),
     "fsx_engine_set_ids_ready": ([vp, i32], i32),
     "fsx_engine_join": ([vp, vp], i32),
+    "fsx_pooled_create": ([vp, u64, u64, u32, P(vp)], i32),
+    "fsx_pooled_destroy": ([vp], i32),
+    "fsx_pooled_forward": ([vp, vp, vp, u64, u64, vp, vp], i32),
+    "fsx_pooled_backward": ([vp, vp, vp], i32),
     "fsx_engine_spans": ([vp, vp, u64, P(u64)], i32),
     "fsx_engine_phase_ms": ([vp, i32, P(dbl), P(u64)], i32),
     "fsx_cost_estimate": ([vp, vp, vp, i32, dbl, dbl, dbl, vp, vp], i32),

@@ -438,10 +438,12 @@ struct SgdPlanOp {
 // row is found by a search of seg_start, the entry holds the gradient row's
 // address (resolved plans) or the occurrence index tagged in bit 0 (plans
 // built ahead of the gradients: the update adds the base at issue time).
+// remap (nullable): the gradient row of occurrence j is row remap[j] of the
+// gradient array (pooled backward: every token of a bag takes the bag's row)
 static __global__ void k_stream_entries(const uint32_t* __restrict__ seg_start, const uint64_t* d_u,
                                  const uint32_t* __restrict__ perm, const uint32_t* __restrict__ inverse,
                                  const char* const* __restrict__ gptr, const uint32_t* __restrict__ row_ent,
-                                 uint64_t* __restrict__ ent) {
+                                 uint64_t* __restrict__ ent, const uint32_t* __restrict__ remap) {
   FSX_PDL_ENTER();
   const uint64_t U = *d_u;
   const uint64_t n = seg_start[U];
@@ -459,8 +461,9 @@ static __global__ void k_stream_entries(const uint32_t* __restrict__ seg_start, 
     }
     const uint32_t r = row_ent[lo];
     if (r == ~0u) continue;
+    const uint32_t j = perm[k];
     ent[r + (k - seg_start[lo])] = gptr ? reinterpret_cast<uintptr_t>(gptr[k])
-                                        : (static_cast<uint64_t>(perm[k]) << 1) | 1u;
+                                        : (static_cast<uint64_t>(remap ? remap[j] : j) << 1) | 1u;
   }
 }
 

@@ -84,7 +84,7 @@ bool use_stream(const Ctx* ctx, const Table& t) {
 template <class T>
 void sgd_plan(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_cap, uint64_t occ_cap,
               const GradRows<T>* resolve_grads, uint32_t chunk, SgdScratch& s, cudaStream_t stream,
-              char* const* seg_out = nullptr) {
+              char* const* seg_out = nullptr, const uint32_t* grad_remap = nullptr) {
   if (rows_cap == 0) return;
   s.reserve(rows_cap, occ_cap, t.g.dim, chunk);
   s.stream_plan = use_stream<T>(ctx, t);
@@ -104,7 +104,7 @@ void sgd_plan(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_cap, uint
   run_scan(ctx, plan, rows_cap, rs.d_u, s.scan, s.d_tot.p, stream);
   if (s.stream_plan)
     FSX_LAUNCH(ctx, k_stream_entries, grid_for(ctx, occ_cap, 256, 8), 256, 0, stream, rs.seg_start, rs.d_u, rs.perm,
-               rs.inverse, reinterpret_cast<const char* const*>(gptr), s.row_ent.p, s.ent.p);
+               rs.inverse, reinterpret_cast<const char* const*>(gptr), s.row_ent.p, s.ent.p, grad_remap);
 }
 
 // persistent grid of k_sgd_stream: as many 4-warp CTAs per SM as shared

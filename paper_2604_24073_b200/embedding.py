@@ -449,3 +449,49 @@ def checkpoint_bytes(geom: TableGeometry, full_table: np.ndarray) -> bytes:
     """embedding.cpp:633-640: u64 rows, u64 dim, u64 shards, row-major f64."""
     hdr = np.array([geom.total_rows, geom.dim, geom.num_shards], np.uint64).tobytes()
     return hdr + np.ascontiguousarray(full_table, np.float64).tobytes()
+
+
+class PooledEmbedding:
+    """Pooled (bag) lookup on one shard — BASELINE config 3's operator (a
+    sum per (sample, table) bag; the reference has only a toy mean-pool over
+    whole samples, pipeline.cpp:59-67). forward(ids, offsets) returns one row
+    per bag: the sum of its tokens' rows in token order (f64 accumulate, one
+    rounding); backward(bag_grads) gives every token its bag's gradient row
+    and updates the rows as ShardView.apply_gradients (embedding.cpp:148-181)
+    with the engine's fixed chunk association. Oracle: fso_pooled_*."""
+
+    def __init__(self, shard: ShardView, max_occurrences: int, max_bags: int, reduce_chunk: int = 64):
+        self.shard = shard
+        h = C.c_void_p()
+        _lib.call("fsx_pooled_create", shard.h, int(max_occurrences), int(max_bags), int(reduce_chunk), C.byref(h))
+        self.h = h
+        self._nb = 0
+
+    def forward(self, ids, offsets, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        dev = self.shard.ctx.torch_device
+        ids = _dev_u64(ids, dev)
+        offsets = _dev_u64(offsets, dev)
+        nb = int(offsets.numel()) - 1
+        if out is None:
+            out = torch.empty((max(nb, 0), self.shard.geom.dim), dtype=self.shard.torch_dtype, device=dev)
+        self._nb = nb
+        _lib.call("fsx_pooled_forward", self.h, C.c_void_p(ids.data_ptr()), C.c_void_p(offsets.data_ptr()), nb,
+                  int(ids.numel()), C.c_void_p(out.data_ptr()), _stream(stream))
+        self._keep = (ids, offsets)  # alive until the backward's plan has run
+        return out
+
+    def backward(self, bag_grads: torch.Tensor, stream=None) -> None:
+        g = bag_grads.to(self.shard.torch_dtype).contiguous()
+        _lib.call("fsx_pooled_backward", self.h, C.c_void_p(g.data_ptr()), _stream(stream))
+        self._keep_g = g
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            _lib.call("fsx_pooled_destroy", self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass

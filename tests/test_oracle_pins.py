@@ -192,3 +192,53 @@ def test_engine_associations_degenerate_cases(oracle, ENG):
         if c["world"] == 1:
             t, _ = oracle.run_engine(1, c["batches"], c["rows"], c["dim"], c["lr"], c["seed"], presum=True)
             assert np.array_equal(t.reshape(-1).view(np.uint64), c["table"].reshape(-1).view(np.uint64)), name
+
+
+@pytest.mark.parametrize("chunk,f32", [(0, False), (2, False), (3, True)])
+def test_pooled_oracle_matches_python_restatement(oracle, chunk, f32):
+    """fso_pooled_* against a loop-by-loop restatement: bag sums in token
+    order, then each row's tokens (row, token order) chunk-folded."""
+    import struct
+
+    def r32(x):
+        return struct.unpack("f", struct.pack("f", x))[0]
+
+    rng = np.random.default_rng(chunk)
+    rows, dim = 10, 3
+    lens = [3, 0, 5, 1, 4]
+    offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
+    ids = rng.integers(0, 4, int(offs[-1])).astype(np.uint64)
+    table = oracle.init_shard(rows, dim, 1, 0, 2)
+    if f32:
+        table = np.array([[r32(v) for v in row] for row in table])
+    want_out = np.zeros((len(lens), dim))
+    for b in range(len(lens)):
+        for d in range(dim):
+            acc = 0.0
+            for k in range(int(offs[b]), int(offs[b + 1])):
+                acc += table[int(ids[k]), d]
+            want_out[b, d] = r32(acc) if f32 else acc
+    got = oracle.pooled_forward(table, ids, offs, store_f32=f32)
+    assert np.array_equal(got.view(np.uint64), want_out.view(np.uint64))
+    g = want_out * 0.5 - 0.25
+    want_t = table.copy()
+    bag_of = np.repeat(np.arange(len(lens)), lens)
+    for r in sorted(set(int(x) for x in ids)):
+        ks = [k for k in range(ids.size) if int(ids[k]) == r]
+        for d in range(dim):
+            vals = [g[bag_of[k], d] for k in ks]
+            if chunk == 0 or len(vals) <= chunk:
+                acc = 0.0
+                for v in vals:
+                    acc += v
+            else:
+                acc = 0.0
+                for c0 in range(0, len(vals), chunk):
+                    part = 0.0
+                    for v in vals[c0:c0 + chunk]:
+                        part += v
+                    acc += part
+            v = want_t[r, d] - 0.05 * acc
+            want_t[r, d] = r32(v) if f32 else v
+    got_t = oracle.pooled_backward(table, ids, offs, g, 0.05, store_f32=f32, reduce_chunk=chunk)
+    assert np.array_equal(got_t.view(np.uint64), want_t.view(np.uint64))
