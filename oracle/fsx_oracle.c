@@ -443,24 +443,31 @@ int fso_run_engine_ex2(int world, int iters, const uint64_t* ids, const uint64_t
  * reference's toy model mean-pools whole samples, pipeline.cpp:59-67). This is
  * the restatement of the product's fsx_pooled_* semantics, on a one-shard
  * table [total_rows x dim]:
- *   forward : out[b] = left fold from 0.0, in token order, of row(ids[k]) for
- *             the bag's tokens k in [offs[b], offs[b+1]) (f64; rounded to float
- *             when store_f32)
+ *   forward : out[b] = chunk_fold, in token order, of row(ids[k]) over the
+ *             bag's tokens k in [offs[b], offs[b+1]) (f64; rounded to float when
+ *             store_f32) — the product runs it as its update kernels' reduce,
+ *             so the association is theirs
  *   backward: token k of bag b takes gradient row g[b]; each row's tokens in
  *             (row, token) order are chunk-folded (chunk_fold) and applied as
  *             ShardView::apply_gradients (embedding.cpp:148-181). */
 int fso_pooled_forward(const double* table, uint64_t total_rows, uint32_t dim, const uint64_t* ids,
-                       const uint64_t* offs, uint64_t n_bags, int store_f32, double* out) {
+                       const uint64_t* offs, uint64_t n_bags, int store_f32, uint32_t reduce_chunk, double* out) {
+  uint64_t n = offs[n_bags];
+  occ_t* occ = malloc((n + 1) * sizeof(occ_t));
+  for (uint64_t k = 0; k < n; ++k) {
+    if (ids[k] >= total_rows) {
+      free(occ);
+      return fail(FSO_DOMAIN, "embedding: row id %llu out of range (table has %llu rows)", ids[k], total_rows);
+    }
+    occ[k].id = ids[k];
+    occ[k].seq = ids[k]; /* chunk_fold reads served[seq * dim + d]: the table row itself */
+  }
   for (uint64_t b = 0; b < n_bags; ++b)
     for (uint32_t d = 0; d < dim; ++d) {
-      double acc = 0.0;
-      for (uint64_t k = offs[b]; k < offs[b + 1]; ++k) {
-        if (ids[k] >= total_rows)
-          return fail(FSO_DOMAIN, "embedding: row id %llu out of range (table has %llu rows)", ids[k], total_rows);
-        acc += table[ids[k] * dim + d];
-      }
+      double acc = chunk_fold(occ + offs[b], offs[b + 1] - offs[b], d, dim, table, 1.0, 0.0, 0, reduce_chunk);
       out[b * dim + d] = store_f32 ? (double)(float)acc : acc;
     }
+  free(occ);
   return FSO_OK;
 }
 

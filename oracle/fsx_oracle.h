@@ -66,7 +66,7 @@ int fso_run_engine_ex2(int world, int iters, const uint64_t* ids, const uint64_t
 
 /* pooled (bag) lookup and its backward scatter + update (see fsx_oracle.c) */
 int fso_pooled_forward(const double* table, uint64_t total_rows, uint32_t dim, const uint64_t* ids,
-                       const uint64_t* offs, uint64_t n_bags, int store_f32, double* out);
+                       const uint64_t* offs, uint64_t n_bags, int store_f32, uint32_t reduce_chunk, double* out);
 int fso_pooled_backward(double* table, uint64_t total_rows, uint32_t dim, double lr, const uint64_t* ids,
                         const uint64_t* offs, uint64_t n_bags, const double* bag_grads, int store_f32,
                         uint32_t reduce_chunk);

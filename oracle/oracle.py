@@ -216,15 +216,17 @@ class Oracle(_Lib):
         return table[:total_rows * dim].reshape(total_rows, dim), (stats[:3 * iters].reshape(iters, 3)
                                                                     if with_stats else None)
 
-    def pooled_forward(self, table, ids, offs, store_f32=False):
+    def pooled_forward(self, table, ids, offs, store_f32=False, reduce_chunk=0):
         """Sum-pooled bags of a one-shard table [rows x dim] (fso_pooled_forward)."""
         table = np.ascontiguousarray(table, np.float64)
         rows, dim = table.shape
         ids, offs = _u64(ids), _u64(offs)
         nb = offs.size - 1
         out = np.zeros(max(nb * dim, 1), np.float64)
-        f = self._fn("pooled_forward", [f64p, C.c_uint64, C.c_uint32, u64p, u64p, C.c_uint64, C.c_int, f64p])
-        self._check(f(table, rows, dim, ids if ids.size else np.zeros(1, np.uint64), offs, nb, int(store_f32), out))
+        f = self._fn("pooled_forward", [f64p, C.c_uint64, C.c_uint32, u64p, u64p, C.c_uint64, C.c_int,
+                                        C.c_uint32, f64p])
+        self._check(f(table, rows, dim, ids if ids.size else np.zeros(1, np.uint64), offs, nb, int(store_f32),
+                      int(reduce_chunk), out))
         return out[:nb * dim].reshape(nb, dim)
 
     def pooled_backward(self, table, ids, offs, bag_grads, lr, store_f32=False, reduce_chunk=0):

@@ -297,7 +297,7 @@ struct GradRows {
 struct RowSegments {
   const uint64_t* uniq_local;  // sorted local row index per slot
   const uint32_t* seg_start;   // [U+1] into the sorted occurrence order
-  const uint32_t* perm;        // sorted position -> occurrence j
+  const uint32_t* perm;        // sorted position -> occurrence j (nullable: identity)
   const uint64_t* d_u;         // live row count U (device)
   const uint8_t* select;       // nullable: update only rows with select[u] == want
   uint8_t want;
@@ -389,7 +389,8 @@ struct SgdPlanOp {
     // first gradient row: a pointer (resolved plans), or, for plans built
     // ahead of the gradients, the occurrence index tagged in bit 0 — the
     // update kernels then skip the perm load
-    const char* g0 = gptr ? gptr[s] : reinterpret_cast<const char*>((static_cast<uintptr_t>(rs.perm[s]) << 1) | 1u);
+    const char* g0 = gptr ? gptr[s]
+                          : reinterpret_cast<const char*>((static_cast<uintptr_t>(rs.perm ? rs.perm[s] : s) << 1) | 1u);
     if (c[0]) {
       singles[ex[0]] = SgdItem{static_cast<uint32_t>(u), kSgdSingleChunk, s, e, dst, g0};
       return;
@@ -450,8 +451,9 @@ static __global__ void k_stream_entries(const uint32_t* __restrict__ seg_start, 
   for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n;
        k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
     uint64_t lo = 0;  // the row u of sorted position k
+    const uint32_t j = perm ? perm[k] : static_cast<uint32_t>(k);
     if (inverse) {
-      lo = inverse[perm[k]];
+      lo = inverse[j];
     } else {  // last row u with seg_start[u] <= k
       uint64_t hi = U;
       while (hi - lo > 1) {
@@ -461,7 +463,6 @@ static __global__ void k_stream_entries(const uint32_t* __restrict__ seg_start, 
     }
     const uint32_t r = row_ent[lo];
     if (r == ~0u) continue;
-    const uint32_t j = perm[k];
     ent[r + (k - seg_start[lo])] = gptr ? reinterpret_cast<uintptr_t>(gptr[k])
                                         : (static_cast<uint64_t>(remap ? remap[j] : j) << 1) | 1u;
   }
@@ -476,7 +477,7 @@ __global__ void k_grad_ptrs(GradRows<T> gr, const uint32_t* __restrict__ perm,
   const uint64_t n = seg_start[*d_u];
   for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n;
        k += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    gptr[k] = gr.row(perm[k]);
+    gptr[k] = gr.row(perm ? perm[k] : static_cast<uint32_t>(k));
 }
 
 template <class T>
@@ -503,7 +504,7 @@ struct SgdArgs {
                               // (k_grad_ptrs); nullptr: gr.row(perm[k])
   const uint64_t* ent = nullptr;  // stream plan: ring entries (k_sgd_stream)
   __device__ __forceinline__ const T* grad(uint32_t k) const {
-    return gptr ? gptr[k] : gr.row(rs.perm[k]);
+    return gptr ? gptr[k] : gr.row(rs.perm ? rs.perm[k] : k);
   }
   // gradient row of an item's first occurrence (SgdItem::g0: pointer,
   // tagged occurrence index, or nullptr)

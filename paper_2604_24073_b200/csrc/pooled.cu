@@ -7,13 +7,16 @@
 // traffic of a table-wise shard is bags x D instead of tokens x D).
 //
 //   forward : pooled[b] = sum over the bag's tokens k, in order, of row(ids[k])
-//             (f64 left fold from 0.0, one rounding to the table type)
+//             (f64, the chunk association below, one rounding to the table type)
 //   backward: every token k of bag b takes gradient row g[b]; rows are then
 //             updated exactly as ShardView::apply_gradients
 //             (embedding.cpp:148-181) with the engine's chunk association
 //
-// The forward sorts the bag tokens by row (the update plan) right behind the
-// pooled gather, so the backward is one update launch.
+// The forward is the update kernels' segmented reduce in reduce-only mode over
+// bags (so its association is theirs: tokens left-folded from 0.0 in order,
+// bags longer than `reduce_chunk` tokens as chunk partials folded in chunk
+// order), then sorts the tokens by row (the update plan), so the backward is
+// one update launch.
 #include <cstdint>
 #include <memory>
 #include <string>
@@ -25,100 +28,43 @@
 namespace fsx {
 namespace {
 
-// warp per bag: lanes hold the 16-byte vectors of the row (NV per lane), U
-// rows of the bag in flight per step; the token -> bag map for the backward
-// is written on the way
-template <class T, int NV, int U>
-__global__ void __launch_bounds__(256) k_pool_bags(const T* __restrict__ table, ShardGeom g,
-                                                   const uint64_t* __restrict__ ids,
-                                                   const uint64_t* __restrict__ offs, uint64_t n_bags,
-                                                   T* __restrict__ out, uint32_t* __restrict__ bag_of,
-                                                   DevErr* err) {
+// Per bag: its start as a u32 segment offset, its output row's address (the
+// reduce-only destinations) and a zero row for an empty bag; per token: its
+// local table row (the gradient-row index the segmented reduce reads) and
+// its bag (the backward's gradient row). A bad id reads row 0 and raises the
+// reference's domain_error at the next sync. Warp per bag.
+__global__ void k_pool_prep(ShardGeom g, const uint64_t* __restrict__ ids, const uint64_t* __restrict__ offs,
+                            uint64_t n_bags, char* out, uint32_t row_bytes, uint32_t* __restrict__ bag_start,
+                            char** __restrict__ seg_out, uint32_t* __restrict__ row_of,
+                            uint32_t* __restrict__ bag_of, uint64_t* __restrict__ d_nbags, DevErr* err) {
   FSX_PDL_ENTER();
-  constexpr int VE = static_cast<int>(16 / sizeof(T));
-  using V = VecOf<T, VE>;
   const unsigned lane = threadIdx.x & 31u;
-  const uint32_t vpr = g.dim / VE;
   const uint64_t warps = (static_cast<uint64_t>(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t b = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; b < n_bags; b += warps) {
-    const uint64_t k0 = offs[b], k1 = offs[b + 1];
-    double acc[NV][VE];
-#pragma unroll
-    for (int v = 0; v < NV; ++v)
-#pragma unroll
-      for (int x = 0; x < VE; ++x) acc[v][x] = 0.0;
-    for (uint64_t kb = k0; kb < k1; kb += 32) {
-      const uint32_t nk = static_cast<uint32_t>(min(static_cast<uint64_t>(32), k1 - kb));
-      // lane l: token kb + l's row (validated: a bad id contributes nothing
-      // and raises the reference's domain_error at the next sync)
-      const T* myrow = nullptr;
-      if (lane < nk) {
-        const uint64_t id = ids[kb + lane];
-        bag_of[kb + lane] = static_cast<uint32_t>(b);
-        if (g.owns(id))
-          myrow = table + (id / static_cast<uint64_t>(g.p)) * g.dim;
-        else
-          report(err, id >= g.total_rows ? kErrRowRange : kErrNotOwned, id,
-                 id >= g.total_rows ? g.total_rows : static_cast<unsigned long long>(g.shard));
-      }
-      for (uint32_t t0 = 0; t0 < nk; t0 += U) {
-        V r[U][NV];
-        bool live[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const T* p = reinterpret_cast<const T*>(
-              __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(myrow), (t0 + u) & 31u));
-          live[u] = t0 + u < nk && p != nullptr;
-#pragma unroll
-          for (int v = 0; v < NV; ++v)
-            if (live[u] && lane + 32u * v < vpr) r[u][v] = *reinterpret_cast<const V*>(p + (lane + 32u * v) * VE);
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (live[u]) {
-#pragma unroll
-            for (int v = 0; v < NV; ++v)
-#pragma unroll
-              for (int x = 0; x < VE; ++x) acc[v][x] = __dadd_rn(acc[v][x], static_cast<double>(r[u][v].v[x]));
-          }
-      }
-    }
-#pragma unroll
-    for (int v = 0; v < NV; ++v)
-      if (lane + 32u * v < vpr) {
-        V o;
-#pragma unroll
-        for (int x = 0; x < VE; ++x) o.v[x] = static_cast<T>(acc[v][x]);
-        *reinterpret_cast<V*>(out + b * g.dim + (lane + 32u * v) * VE) = o;
-      }
+  const uint64_t w0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  if (w0 == 0 && lane == 0) {
+    *d_nbags = n_bags;
+    bag_start[n_bags] = static_cast<uint32_t>(offs[n_bags]);
   }
-}
-
-// scalar fallback for rows that are not whole 16-byte vectors: thread per
-// (bag, column), tokens in order
-template <class T>
-__global__ void k_pool_bags_scalar(const T* __restrict__ table, ShardGeom g, const uint64_t* __restrict__ ids,
-                                   const uint64_t* __restrict__ offs, uint64_t n_bags, T* __restrict__ out,
-                                   uint32_t* __restrict__ bag_of, DevErr* err) {
-  FSX_PDL_ENTER();
-  const uint64_t total = n_bags * g.dim;
-  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-    const uint64_t b = i / g.dim;
-    const uint32_t d = static_cast<uint32_t>(i - b * g.dim);
-    double acc = 0.0;
-    for (uint64_t k = offs[b]; k < offs[b + 1]; ++k) {
-      const uint64_t id = ids[k];
-      if (d == 0) bag_of[k] = static_cast<uint32_t>(b);
-      if (!g.owns(id)) {
-        if (d == 0)
-          report(err, id >= g.total_rows ? kErrRowRange : kErrNotOwned, id,
-                 id >= g.total_rows ? g.total_rows : static_cast<unsigned long long>(g.shard));
-        continue;
-      }
-      acc = __dadd_rn(acc, static_cast<double>(table[(id / static_cast<uint64_t>(g.p)) * g.dim + d]));
+  for (uint64_t b = w0; b < n_bags; b += warps) {
+    const uint64_t k0 = offs[b], k1 = offs[b + 1];
+    char* row = out + b * row_bytes;
+    if (lane == 0) {
+      bag_start[b] = static_cast<uint32_t>(k0);
+      seg_out[b] = row;
     }
-    out[i] = static_cast<T>(acc);
+    if (k0 == k1)
+      for (uint32_t x = lane * 4; x < row_bytes; x += 128) *reinterpret_cast<uint32_t*>(row + x) = 0u;
+    for (uint64_t k = k0 + lane; k < k1; k += 32) {
+      const uint64_t id = ids[k];
+      bag_of[k] = static_cast<uint32_t>(b);
+      uint32_t r = 0;
+      if (g.owns(id))
+        r = static_cast<uint32_t>(id / static_cast<uint64_t>(g.p));
+      else
+        report(err, id >= g.total_rows ? kErrRowRange : kErrNotOwned, id,
+               id >= g.total_rows ? g.total_rows : static_cast<unsigned long long>(g.shard));
+      row_of[k] = r;
+    }
   }
 }
 
@@ -131,38 +77,39 @@ struct fsx_pooled {
   Table* t = nullptr;
   uint64_t cap_occ = 0, cap_bags = 0;
   uint32_t chunk = 0;
-  SortedIds srt;
-  SgdScratch plan;
-  DevBuf<uint32_t> bag_of;
-  DevBuf<uint64_t> d_n;
+  SortedIds srt;          // the backward's tokens sorted by row
+  SgdScratch fplan, plan; // forward (bags) and backward (rows) work lists
+  DevBuf<uint32_t> bag_of, row_of, bag_start;
+  DevBuf<char*> seg_out;
+  DevBuf<uint64_t> d_nbags;
   bool planned = false;
   uint64_t n_occ = 0, n_bags = 0;
 };
 
 namespace {
 
+// forward: the segmented reduce of the update kernels in reduce-only mode —
+// segments = bags (tokens already in bag order: identity permutation),
+// "gradient" rows = the tokens' table rows, the same fixed chunk association
+// (k_sgd_stream: rows staged by bulk copies, balanced across warps, hot bags
+// split into chunks), each bag's f64 sum rounded once into its output row.
+// Then the backward's plan: tokens sorted by row.
 template <class T>
 void pooled_forward(fsx_pooled* p, const uint64_t* d_ids, const uint64_t* d_offs, uint64_t n_bags, uint64_t n,
                     void* d_out, cudaStream_t s) {
   Table& t = *p->t;
   Ctx* ctx = t.ctx;
-  constexpr int VE = static_cast<int>(16 / sizeof(T));
   const uint32_t rb = t.row_bytes();
-  const unsigned vpl = (rb / 16 + 31) / 32;
-  if (rb % 16 == 0 && vpl <= 2) {
-    const unsigned grid = grid_for(ctx, n_bags * 32, 256, 8);
-    if (vpl == 1)
-      FSX_LAUNCH(ctx, (k_pool_bags<T, 1, 8>), grid, 256, 0, s, static_cast<const T*>(t.values), t.g, d_ids, d_offs,
-                 n_bags, static_cast<T*>(d_out), p->bag_of.p, ctx->d_err);
-    else
-      FSX_LAUNCH(ctx, (k_pool_bags<T, 2, 4>), grid, 256, 0, s, static_cast<const T*>(t.values), t.g, d_ids, d_offs,
-                 n_bags, static_cast<T*>(d_out), p->bag_of.p, ctx->d_err);
-  } else {
-    FSX_LAUNCH(ctx, k_pool_bags_scalar<T>, grid_for(ctx, n_bags * t.g.dim, 256, 8), 256, 0, s,
-               static_cast<const T*>(t.values), t.g, d_ids, d_offs, n_bags, static_cast<T*>(d_out), p->bag_of.p,
-               ctx->d_err);
+  FSX_LAUNCH(ctx, k_pool_prep, grid_for(ctx, n_bags * 32, 256, 8), 256, 0, s, t.g, d_ids, d_offs, n_bags,
+             static_cast<char*>(d_out), rb, p->bag_start.p, p->seg_out.p, p->row_of.p, p->bag_of.p,
+             p->d_nbags.p, ctx->d_err);
+  if (n) {
+    RowSegments bags{nullptr, p->bag_start.p, nullptr, p->d_nbags.p, nullptr, 0, p->bag_of.p};
+    sgd_plan<T>(ctx, t, bags, n_bags, n, nullptr, p->chunk, p->fplan, s, p->seg_out.p, p->row_of.p);
+    GradRows<T> rows{static_cast<const char*>(t.values), 0, nullptr, p->fplan.stream_plan ? nullptr : p->row_of.p,
+                     rb};
+    sgd_apply<T>(ctx, t, bags, n_bags, n, rows, p->chunk, p->fplan, nullptr, s, p->seg_out.p);
   }
-  (void)VE;
   // the backward's plan: tokens sorted by row (stable: bag order within a
   // row), the update work lists with each token's gradient row = its bag's
   FSX_CUDA(cudaMemcpyAsync(p->srt.d_n(), &p->n_occ, 8, cudaMemcpyHostToDevice, s));
@@ -199,6 +146,10 @@ int fsx_pooled_create(fsx_table* t, uint64_t max_occurrences, uint64_t max_bags,
   p->chunk = reduce_chunk;
   p->srt.reserve(p->cap_occ);
   p->bag_of.alloc(p->cap_occ);
+  p->row_of.alloc(p->cap_occ);
+  p->bag_start.alloc(p->cap_bags + 1);
+  p->seg_out.alloc(p->cap_bags);
+  p->d_nbags.alloc(1);
   *out = p.release();
   FSX_API_END
 }
@@ -223,8 +174,9 @@ int fsx_pooled_forward(fsx_pooled* p, const uint64_t* d_ids, const uint64_t* d_b
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   p->n_occ = n_ids;
   p->n_bags = n_bags;
-  p->planned = false;
+  p->planned = true;  // (an empty batch has nothing to plan)
   if (n_bags == 0) return FSX_OK;
+  p->planned = false;
   if (p->t->dtype == FSX_F32)
     pooled_forward<float>(p, d_ids, d_bag_offsets, n_bags, n_ids, d_out, s);
   else
@@ -236,7 +188,7 @@ int fsx_pooled_forward(fsx_pooled* p, const uint64_t* d_ids, const uint64_t* d_b
 int fsx_pooled_backward(fsx_pooled* p, const void* d_bag_grads, void* stream) {
   FSX_API_BEGIN
   DeviceGuard dg(p->t->ctx->device);
-  if (!p->planned && p->n_bags) raise(FSX_ERR_PROTOCOL, "pooled: backward before forward");
+  if (!p->planned) raise(FSX_ERR_PROTOCOL, "pooled: backward before forward");
   if (p->n_occ == 0) return FSX_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (p->t->dtype == FSX_F32)

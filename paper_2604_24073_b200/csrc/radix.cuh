@@ -289,13 +289,29 @@ __global__ void __launch_bounds__(kRadixThreads) k_os_scatter(
       continue;
     }
     *reinterpret_cast<volatile uint32_t*>(my + d) = kOsAgg | run;
+    // look-back, 8 predecessors' words loaded at once (independent loads:
+    // one round trip per 8 tiles instead of one per tile), consumed in order
+    // until an inclusive prefix; an unpublished word is re-read
     uint32_t acc = 0;
     for (int64_t t = static_cast<int64_t>(tile) - 1; t >= 0;) {
-      const uint32_t st = *reinterpret_cast<volatile const uint32_t*>(status + static_cast<uint64_t>(t) * kRadixBins + d);
-      if ((st & ~kOsCount) == 0) continue;  // not published yet: spin
-      acc += st & kOsCount;
-      if (st & kOsIncl) break;
-      --t;
+      constexpr int kLook = 8;
+      uint32_t st[kLook];
+#pragma unroll
+      for (int j = 0; j < kLook; ++j)
+        st[j] = t - j >= 0 ? *reinterpret_cast<volatile const uint32_t*>(status + static_cast<uint64_t>(t - j) * kRadixBins + d)
+                           : 0u;
+      int j = 0;
+      bool incl = false;
+      for (; j < kLook && t - j >= 0; ++j) {
+        if ((st[j] & ~kOsCount) == 0) break;  // not published yet: spin from here
+        acc += st[j] & kOsCount;
+        if (st[j] & kOsIncl) {
+          incl = true;
+          break;
+        }
+      }
+      if (incl) break;
+      t -= j;
     }
     *reinterpret_cast<volatile uint32_t*>(my + d) = kOsIncl | (acc + run);
     tile_off[d] += acc;

@@ -18,6 +18,7 @@ def _bits(x):
 def _bags(rng, n_bags, rows, max_len, zipf=True, mul=1, add=0):
     lens = rng.integers(0, max_len + 1, n_bags)
     lens[::7] = 0  # empty bags
+    lens[5] = 9 * max_len  # a hot bag: split into chunks
     offs = np.concatenate([[0], np.cumsum(lens)]).astype(np.uint64)
     n = int(offs[-1])
     if zipf:
@@ -61,7 +62,7 @@ def test_pooled_bitwise(cuda, oracle, dtype, dim, chunk):
     if f32:
         table = table.astype(np.float32).astype(np.float64)
     for out in outs:
-        want = oracle.pooled_forward(table, ids, offs, store_f32=f32)
+        want = oracle.pooled_forward(table, ids, offs, store_f32=f32, reduce_chunk=chunk)
         assert np.array_equal(_bits(out), _bits(want))
         g = want * 0.125 + 0.0625
         if f32:  # the torch fixture in float: fl(fl(x * 0.125) + 0.0625)
@@ -82,7 +83,7 @@ def test_pooled_table_wise_shard(cuda, oracle):
     outs, vals = _run(cuda, geom, t, "f32", ids, offs, lambda o: o * 0.125 + 0.0625, 64)
     table = oracle.init_shard(T * R, dim, 1, 0, 11).astype(np.float32).astype(np.float64)
     for out in outs:
-        want = oracle.pooled_forward(table, ids, offs, store_f32=True)
+        want = oracle.pooled_forward(table, ids, offs, store_f32=True, reduce_chunk=64)
         assert np.array_equal(_bits(out), _bits(want))
         g = ((want.astype(np.float32) * np.float32(0.125)) + np.float32(0.0625)).astype(np.float64)
         table = oracle.pooled_backward(table, ids, offs, g, 0.05, store_f32=True, reduce_chunk=64)

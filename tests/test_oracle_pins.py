@@ -211,14 +211,26 @@ def test_pooled_oracle_matches_python_restatement(oracle, chunk, f32):
     table = oracle.init_shard(rows, dim, 1, 0, 2)
     if f32:
         table = np.array([[r32(v) for v in row] for row in table])
+    def fold(vals):
+        if chunk == 0 or len(vals) <= chunk:
+            acc = 0.0
+            for v in vals:
+                acc += v
+            return acc
+        acc = 0.0
+        for c0 in range(0, len(vals), chunk):
+            part = 0.0
+            for v in vals[c0:c0 + chunk]:
+                part += v
+            acc += part
+        return acc
+
     want_out = np.zeros((len(lens), dim))
     for b in range(len(lens)):
         for d in range(dim):
-            acc = 0.0
-            for k in range(int(offs[b]), int(offs[b + 1])):
-                acc += table[int(ids[k]), d]
+            acc = fold([table[int(ids[k]), d] for k in range(int(offs[b]), int(offs[b + 1]))])
             want_out[b, d] = r32(acc) if f32 else acc
-    got = oracle.pooled_forward(table, ids, offs, store_f32=f32)
+    got = oracle.pooled_forward(table, ids, offs, store_f32=f32, reduce_chunk=chunk)
     assert np.array_equal(got.view(np.uint64), want_out.view(np.uint64))
     g = want_out * 0.5 - 0.25
     want_t = table.copy()
@@ -226,18 +238,7 @@ def test_pooled_oracle_matches_python_restatement(oracle, chunk, f32):
     for r in sorted(set(int(x) for x in ids)):
         ks = [k for k in range(ids.size) if int(ids[k]) == r]
         for d in range(dim):
-            vals = [g[bag_of[k], d] for k in ks]
-            if chunk == 0 or len(vals) <= chunk:
-                acc = 0.0
-                for v in vals:
-                    acc += v
-            else:
-                acc = 0.0
-                for c0 in range(0, len(vals), chunk):
-                    part = 0.0
-                    for v in vals[c0:c0 + chunk]:
-                        part += v
-                    acc += part
+            acc = fold([g[bag_of[k], d] for k in ks])
             v = want_t[r, d] - 0.05 * acc
             want_t[r, d] = r32(v) if f32 else v
     got_t = oracle.pooled_backward(table, ids, offs, g, 0.05, store_f32=f32, reduce_chunk=chunk)
