@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <functional>
+#include <limits>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -87,78 +89,58 @@ std::vector<std::uint64_t> sorted_unique_dev(const std::vector<std::uint64_t>& v
 
 }  // namespace
 
-// ---- comm ------------------------------------------------------------------------
-namespace comm {
+// ---- jagged reshuffle (jagged.hpp) ----------------------------------------------------
+namespace jagged_detail {
 
-InProcessFabric::InProcessFabric(int world_size) : world_(world_size) {
-  if (world_size < 1) throw std::invalid_argument("fabric: world_size must be >= 1");
-  int ndev = 1;
-  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1) ndev = 1;
-  for (int r = 0; r < world_size; ++r) {
-    auto t = std::make_unique<Transport>();
-    t->rank_ = r;
-    t->world_ = world_size;
-    t->device_ = r % ndev;
-    t->fabric_ = this;
-    fsx_ok(fsx_ctx_create(t->device_, r, world_size, &t->ctx_));
-    eps_.push_back(std::move(t));
-  }
+void permute(const void* values, std::size_t elem_bytes, std::span<const std::size_t> lengths,
+             std::span<const std::size_t> perm, std::vector<unsigned char>& out_values,
+             std::vector<std::size_t>& out_lengths) {
+  const std::size_t nseg = lengths.size(), np = perm.size();
+  // the reference validates every index before moving anything
+  for (std::size_t idx : perm)
+    if (idx >= nseg)
+      throw std::out_of_range("indexed_permute: segment index " + std::to_string(idx) + " out of range (have " +
+                              std::to_string(nseg) + ")");
+  out_lengths.assign(np, 0);
+  out_values.clear();
+  if (np == 0) return;
+  fsx_ctx* ctx = thread_ctx();
+  std::vector<std::uint64_t> h_len(lengths.begin(), lengths.end()), h_perm(perm.begin(), perm.end());
+  std::uint64_t total_in = 0;
+  for (auto l : h_len) total_in += l;
+  Dev<std::uint64_t> d_len(nseg + 1), d_off(nseg + 1), d_perm(np), d_olen(np), d_ooff(np + 1);
+  Dev<unsigned char> d_vals(total_in * elem_bytes + 16);
+  h2d(d_len.p, h_len.data(), nseg);
+  h2d(d_perm.p, h_perm.data(), np);
+  if (total_in) h2d(d_vals.p, static_cast<const unsigned char*>(values), total_in * elem_bytes);
+  std::uint64_t tot = 0;
+  fsx_ok(fsx_jagged_offsets(ctx, d_len.p, nseg, d_off.p, &tot, nullptr));
+  std::uint64_t out_total = 0;
+  fsx_ok(fsx_jagged_permute(ctx, d_vals.p, static_cast<std::uint32_t>(elem_bytes), d_off.p, nseg, d_perm.p, np,
+                            nullptr, 0, d_olen.p, d_ooff.p, &out_total, nullptr));  // sizing
+  Dev<unsigned char> d_out(out_total * elem_bytes + 16);
+  fsx_ok(fsx_jagged_permute(ctx, d_vals.p, static_cast<std::uint32_t>(elem_bytes), d_off.p, nseg, d_perm.p, np,
+                            d_out.p, out_total, d_olen.p, d_ooff.p, &out_total, nullptr));
+  std::vector<std::uint64_t> olen(np);
+  d2h(olen.data(), d_olen.p, np);
+  out_lengths.assign(olen.begin(), olen.end());
+  out_values.resize(out_total * elem_bytes);
+  if (out_total) d2h(out_values.data(), d_out.p, out_values.size());
 }
 
-InProcessFabric::~InProcessFabric() {
-  for (auto& t : eps_) fsx_ctx_destroy(t->ctx_);
+std::vector<std::size_t> transpose_perm(std::size_t num_keys, std::size_t num_samples, bool feature_major) {
+  const std::size_t n = num_keys * num_samples;
+  std::vector<std::size_t> perm(n);
+  if (n == 0) return perm;
+  Dev<std::uint64_t> d(n);
+  fsx_ok(fsx_keyed_transpose_perm(thread_ctx(), num_keys, num_samples, feature_major ? 1 : 0, d.p, nullptr));
+  std::vector<std::uint64_t> h(n);
+  d2h(h.data(), d.p, n);
+  perm.assign(h.begin(), h.end());
+  return perm;
 }
 
-Transport& InProcessFabric::transport(int rank) { return *eps_.at(static_cast<size_t>(rank)); }
-
-void InProcessFabric::poison(const std::string& why) {
-  {
-    std::lock_guard<std::mutex> lk(mu_);
-    poisoned_ = true;
-    poison_msg_ = "collective aborted: " + why;
-  }
-  cv_.notify_all();
-}
-
-std::vector<std::vector<std::uint8_t>> InProcessFabric::exchange(int rank, std::vector<std::uint8_t> mine) {
-  std::unique_lock<std::mutex> lk(mu_);
-  if (poisoned_) throw CollectiveError(poison_msg_);
-  const std::uint64_t my_round = round_;
-  if (blobs_.empty()) blobs_.resize(static_cast<size_t>(world_));
-  blobs_[static_cast<size_t>(rank)] = std::move(mine);
-  if (++arrived_ == world_) {
-    last_ = std::move(blobs_);
-    blobs_.clear();
-    arrived_ = 0;
-    ++round_;
-    cv_.notify_all();
-  } else {
-    cv_.wait(lk, [&] { return round_ != my_round || poisoned_; });
-    if (round_ == my_round) throw CollectiveError(poison_msg_);
-  }
-  return last_;
-}
-
-void InProcessFabric::run(const std::function<void(int)>& body) {
-  std::vector<std::exception_ptr> errs(static_cast<size_t>(world_));
-  std::vector<std::thread> th;
-  for (int r = 0; r < world_; ++r) {
-    th.emplace_back([&, r] {
-      try {
-        cuda_ok(cudaSetDevice(eps_[static_cast<size_t>(r)]->device_));
-        body(r);
-      } catch (...) {
-        errs[static_cast<size_t>(r)] = std::current_exception();
-        poison("rank " + std::to_string(r) + " failed");
-      }
-    });
-  }
-  for (auto& t : th) t.join();
-  for (auto& e : errs)
-    if (e) std::rethrow_exception(e);
-}
-
-}  // namespace comm
+}  // namespace jagged_detail
 
 // ---- embedding -----------------------------------------------------------------------
 namespace embedding {
@@ -435,6 +417,61 @@ std::vector<std::uint8_t> checkpoint_bytes(const TableGeometry& geom, std::span<
   return out;
 }
 
+// ---- routing (embedding.cpp:185-231) ---------------------------------------------------
+ShardRouting route_to_shard_major(comm::Communicator& comm, const TableGeometry& geom, const IdJagged& batch_ids,
+                                  const comm::CollectiveOptions& opts) {
+  const int p = comm.world_size();
+  ShardRouting r;
+  r.batch_ids = batch_ids;
+  const auto& flat = batch_ids.values();
+  const std::size_t n = flat.size();
+  r.occ_shard.resize(n);
+  r.send_positions.resize(static_cast<std::size_t>(p));
+  r.send_ids.resize(static_cast<std::size_t>(p));
+  r.unique_per_shard.resize(static_cast<std::size_t>(p));
+  fsx_ctx* ctx = comm.transport().ctx() ? comm.transport().ctx() : thread_ctx();
+  if (n) {
+    // stable owner partition on the GPU; range errors raise the reference's text
+    Dev<std::uint64_t> d_ids(n), d_send(n);
+    Dev<std::uint32_t> d_pos(n);
+    h2d(d_ids.p, flat.data(), n);
+    std::vector<std::uint64_t> counts(static_cast<std::size_t>(p));
+    fsx_ok(fsx_route_by_owner(ctx, d_ids.p, n, geom.total_rows, p, d_send.p, d_pos.p, counts.data(), nullptr));
+    std::vector<std::uint64_t> send(n);
+    std::vector<std::uint32_t> pos(n);
+    d2h(send.data(), d_send.p, n);
+    d2h(pos.data(), d_pos.p, n);
+    std::size_t at = 0;
+    for (int s = 0; s < p; ++s) {
+      const std::size_t c = counts[static_cast<std::size_t>(s)];
+      auto& sp = r.send_positions[static_cast<std::size_t>(s)];
+      auto& si = r.send_ids[static_cast<std::size_t>(s)];
+      sp.assign(pos.begin() + static_cast<std::ptrdiff_t>(at), pos.begin() + static_cast<std::ptrdiff_t>(at + c));
+      si.assign(send.begin() + static_cast<std::ptrdiff_t>(at), send.begin() + static_cast<std::ptrdiff_t>(at + c));
+      for (std::size_t q : sp) r.occ_shard[q] = s;
+      r.unique_per_shard[static_cast<std::size_t>(s)] = sorted_unique_dev(si);
+      at += c;
+    }
+  }
+  std::vector<comm::Bytes> payloads(static_cast<std::size_t>(p));
+  for (int s = 0; s < p; ++s) payloads[static_cast<std::size_t>(s)] = comm::pack_u64s(r.send_ids[static_cast<std::size_t>(s)]);
+  const auto got = comm.all_to_all(payloads, opts);
+  std::vector<std::uint64_t> values;
+  std::vector<std::size_t> lengths(static_cast<std::size_t>(p));
+  r.recv_unique_per_src.resize(static_cast<std::size_t>(p));
+  for (int src = 0; src < p; ++src) {
+    const auto ids = comm::unpack_u64s(got[static_cast<std::size_t>(src)]);
+    for (std::uint64_t id : ids)
+      if (geom.owner(id) != comm.rank())
+        throw ProtocolError("embedding: received row " + std::to_string(id) + " that this shard does not own");
+    lengths[static_cast<std::size_t>(src)] = ids.size();
+    r.recv_unique_per_src[static_cast<std::size_t>(src)] = sorted_unique_dev(ids);
+    values.insert(values.end(), ids.begin(), ids.end());
+  }
+  r.shard_ids = IndexSet::shard_major(IdJagged(std::move(values), std::move(lengths)));
+  return r;
+}
+
 }  // namespace embedding
 
 // ---- partition / sim --------------------------------------------------------------------
@@ -576,16 +613,53 @@ double plan_max_weight(const PartitionPlan& plan, std::span<const GlobalSampleMe
   return mx;
 }
 
+// Every split into `segments` non-empty contiguous runs (cut positions
+// strictly increasing in (0, m)), the smallest maximum run sum; sequential
+// prefix sums as the DP uses. Test oracle of vbs_partition's DP.
+double min_max_contiguous_bruteforce(std::span<const double> weights, int segments) {
+  const std::size_t m = weights.size();
+  std::vector<double> prefix(m + 1, 0.0);
+  for (std::size_t i = 0; i < m; ++i) prefix[i + 1] = prefix[i] + weights[i];
+  if (segments == 1) return prefix[m];
+  const std::size_t ncut = static_cast<std::size_t>(segments) - 1;
+  std::vector<std::size_t> cut(ncut);
+  double best = std::numeric_limits<double>::infinity();
+  std::function<void(std::size_t, std::size_t)> place = [&](std::size_t k, std::size_t first) {
+    if (k == ncut) {
+      double worst = 0;
+      std::size_t from = 0;
+      for (std::size_t c : cut) {
+        worst = std::max(worst, prefix[c] - prefix[from]);
+        from = c;
+      }
+      best = std::min(best, std::max(worst, prefix[m] - prefix[from]));
+      return;
+    }
+    for (std::size_t c = first; c + (ncut - k) <= m; ++c) {
+      cut[k] = c;
+      place(k + 1, c + 1);
+    }
+  };
+  place(0, 1);
+  return best;
+}
+
 }  // namespace partition
 
 namespace sim {
 
-double CostModel::compute_time_for_lengths(std::span<const std::uint64_t> lengths) const {
-  Dev<std::uint64_t> d(lengths.size() + 1);
-  h2d(d.p, lengths.data(), lengths.size());
-  const std::uint64_t off[2] = {0, lengths.size()};
-  double out = 0;
-  fsx_ok(fsx_cost_estimate(thread_ctx(), d.p, off, 1, c0, c1, c2, &out, nullptr));
+std::vector<double> CostModel::compute_times(const std::vector<std::vector<std::uint64_t>>& batches) const {
+  std::vector<std::uint64_t> flat, off{0};
+  for (const auto& b : batches) {
+    flat.insert(flat.end(), b.begin(), b.end());
+    off.push_back(flat.size());
+  }
+  std::vector<double> out(batches.size());
+  if (batches.empty()) return out;
+  Dev<std::uint64_t> d(flat.size() + 1);
+  h2d(d.p, flat.data(), flat.size());
+  fsx_ok(fsx_cost_estimate(thread_ctx(), d.p, off.data(), static_cast<int>(batches.size()), c0, c1, c2, out.data(),
+                           nullptr));
   return out;
 }
 

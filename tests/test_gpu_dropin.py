@@ -19,3 +19,28 @@ def test_reference_cases_through_cpp_dropin(cuda):
     print(r.stdout[-4000:], r.stderr[-2000:])
     assert r.returncode == 0, r.stdout[-2000:]
     assert "0 failed" in r.stdout
+
+
+# The reference's own unit suites (tests/test_{comm,partition,jagged}.cpp),
+# compiled unchanged against the drop-in headers by cpp/Makefile in the
+# container that has /root/reference (the binaries travel to the GPU box).
+# Excluded: the reference simulator's logical-clock cost model and its TCP
+# mesh — not part of the B200 build (cpp/include/freescale/comm.hpp, tcp.hpp).
+REF_SUITES = {
+    "comm": "simulated logical timestamps*,staged hops pay the copy cost*,tcp transport*",
+    "partition": "",
+    "jagged": "",
+}
+
+
+@pytest.mark.parametrize("suite", sorted(REF_SUITES))
+def test_reference_unit_suite_unchanged(cuda, suite):
+    exe = os.path.join(CPP, "build", f"ref_test_{suite}")
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built (needs /root/reference at build time)")
+    env = dict(os.environ, CUDA_MODULE_LOADING="EAGER", CUDA_DEVICE_MAX_CONNECTIONS="32")
+    args = [exe] + ([f"-tce={REF_SUITES[suite]}"] if REF_SUITES[suite] else [])
+    r = subprocess.run(args, capture_output=True, text=True, timeout=900, env=env)
+    print(r.stdout[-6000:], r.stderr[-3000:])
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert " 0 failed" in r.stdout
