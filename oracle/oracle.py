@@ -409,6 +409,49 @@ class Reference(_Lib):
         self._check(f(n, sizes, ema_local, C.byref(eg), step, delta, decay, times, times.size // n))
         return sizes, ema_local, eg.value
 
+    def pipeline_samples(self, spec):
+        """generate_all of a uniform-length WorkloadSpec (dict: world, batch,
+        max_uih, lo, hi, table_rows, target (None or float), seed, iters), sample
+        by sample: dict of per-sample uih_len / n_cand / label and the flat uih
+        ids, candidate lengths, candidate ids (iteration, rank, sample order)."""
+        args = [spec["world"], spec["batch"], spec["max_uih"], spec["lo"], spec["hi"], spec["table_rows"],
+                float(spec["target"] or 0.0), int(spec["target"] is not None), spec["seed"], spec["iters"]]
+        n = np.zeros(4, np.uint64)
+        vp = C.c_void_p
+        f = self._fn("pipeline_samples", [C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
+                                          C.c_double, C.c_int, C.c_uint64, C.c_int, vp, vp, vp, vp, vp, vp, u64p])
+        self._check(f(*args, None, None, None, None, None, None, n))
+        ns, ni, nc, nci = (int(x) for x in n)
+        out = {"uih_len": np.zeros(max(ns, 1), np.uint64), "n_cand": np.zeros(max(ns, 1), np.uint64),
+               "label": np.zeros(max(ns, 1), np.float64), "ids": np.zeros(max(ni, 1), np.uint64),
+               "cand_len": np.zeros(max(nc, 1), np.uint64), "cand_ids": np.zeros(max(nci, 1), np.uint64)}
+        self._check(f(*args, out["uih_len"].ctypes.data, out["n_cand"].ctypes.data, out["label"].ctypes.data,
+                      out["ids"].ctypes.data, out["cand_len"].ctypes.data, out["cand_ids"].ctypes.data, n))
+        return {"uih_len": out["uih_len"][:ns], "n_cand": out["n_cand"][:ns], "label": out["label"][:ns],
+                "ids": out["ids"][:ni], "cand_len": out["cand_len"][:nc], "cand_ids": out["cand_ids"][:nci]}
+
+    def pipeline_run(self, spec, cfg):
+        """pipeline::run (pipeline.cpp:118-323) on the spec's workload; cfg keys:
+        prioritized, balancer, partition ('fbs'|'vbs'|'none'), alpha, dim,
+        table_rows, lr_emb, lr_dense, model_seed, c0, c1, c2. Returns
+        (full_checkpoint bytes, losses, final dense weights)."""
+        args = [spec["world"], spec["batch"], spec["max_uih"], spec["lo"], spec["hi"], spec["table_rows"],
+                float(spec["target"] or 0.0), int(spec["target"] is not None), spec["seed"], spec["iters"],
+                int(cfg["prioritized"]), int(cfg["balancer"]), {"fbs": 0, "vbs": 1, "none": 2}[cfg["partition"]],
+                float(cfg["alpha"]), int(cfg["dim"]), int(cfg["table_rows"]), float(cfg["lr_emb"]),
+                float(cfg["lr_dense"]), int(cfg["model_seed"]), float(cfg["c0"]), float(cfg["c1"]), float(cfg["c2"])]
+        cap = 64 + int(cfg["table_rows"]) * int(cfg["dim"]) * 8 + int(cfg["dim"]) * 8
+        ckpt = np.zeros(cap, np.uint8)
+        n = C.c_uint64()
+        losses = np.zeros(max(spec["iters"], 1), np.float64)
+        dense = np.zeros(max(int(cfg["dim"]), 1), np.float64)
+        f = self._fn("pipeline_run", [C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_double,
+                                      C.c_int, C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_uint32,
+                                      C.c_uint64, C.c_double, C.c_double, C.c_uint64, C.c_double, C.c_double,
+                                      C.c_double, C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64), f64p, f64p])
+        self._check(f(*args, ckpt.ctypes.data, cap, C.byref(n), losses, dense))
+        return ckpt[:n.value].tobytes(), losses[:spec["iters"]], dense[:int(cfg["dim"])]
+
     def bench_engine(self, prioritized, world, batches_per_iter, total_rows, dim, lr, seed):
         iters = len(batches_per_iter)
         lens = _u64([len(b) for it in batches_per_iter for b in it])

@@ -21,6 +21,7 @@
 #include "freescale/comm.hpp"
 #include "freescale/embedding.hpp"
 #include "freescale/partition.hpp"
+#include "freescale/pipeline.hpp"
 #include "freescale/rng.hpp"
 #include "freescale/sim.hpp"
 #include "freescale/workload.hpp"
@@ -450,6 +451,97 @@ int fsref_load_workload(const char* path, std::uint64_t* ids_out, std::uint64_t*
     }
   *n_ids = ni;
   *n_samples = ns;
+  SHIM_CATCH
+}
+
+// ---- pipeline::run (pipeline.cpp:118-323) -----------------------------------------
+// The workload is the reference's own generator (generate_all of a uniform-
+// length spec); pipeline_samples exports it sample by sample so the B200
+// harness runs the same batches: per sample (iteration, rank order) its uih
+// length, candidate-list count, label; then all uih ids; then the candidate
+// list lengths; then all candidate ids. Sizing: with ids == nullptr only the
+// totals are written (n[0] samples, n[1] uih ids, n[2] candidate lists,
+// n[3] candidate ids).
+namespace {
+workload::WorkloadSpec pipeline_spec(int world, int batch, std::uint64_t max_uih, std::uint64_t lo,
+                                     std::uint64_t hi, std::uint64_t table_rows, double target, int has_target,
+                                     std::uint64_t seed, int iters) {
+  workload::WorkloadSpec spec;
+  spec.num_ranks = world;
+  spec.batch_size = batch;
+  spec.max_uih = max_uih;
+  spec.dist = workload::DistSpec::uniform(lo, hi);
+  spec.table_rows = table_rows;
+  if (has_target) spec.target_collision = target;
+  spec.seed = seed;
+  spec.num_iterations = iters;
+  return spec;
+}
+}  // namespace
+
+int fsref_pipeline_samples(int world, int batch, std::uint64_t max_uih, std::uint64_t lo, std::uint64_t hi,
+                           std::uint64_t table_rows, double target, int has_target, std::uint64_t seed, int iters,
+                           std::uint64_t* uih_len, std::uint64_t* n_cand, double* label, std::uint64_t* ids,
+                           std::uint64_t* cand_len, std::uint64_t* cand_ids, std::uint64_t* n) {
+  SHIM_TRY
+  const auto spec = pipeline_spec(world, batch, max_uih, lo, hi, table_rows, target, has_target, seed, iters);
+  std::uint64_t ns = 0, ni = 0, nc = 0, nci = 0;
+  for (const auto& it : workload::generate_all(spec))
+    for (const auto& b : it)
+      for (const auto& smp : b.samples) {
+        if (ids) {
+          uih_len[ns] = smp.uih.size();
+          n_cand[ns] = smp.candidates.size();
+          label[ns] = smp.label;
+          for (auto x : smp.uih) ids[ni++] = x;
+          for (const auto& c : smp.candidates) {
+            cand_len[nc++] = c.size();
+            for (auto x : c) cand_ids[nci++] = x;
+          }
+        } else {
+          ni += smp.uih.size();
+          nc += smp.candidates.size();
+          for (const auto& c : smp.candidates) nci += c.size();
+        }
+        ++ns;
+      }
+  n[0] = ns;
+  n[1] = ni;
+  n[2] = nc;
+  n[3] = nci;
+  SHIM_CATCH
+}
+
+// pipeline::run over that workload. partition: 0 fbs, 1 vbs, 2 none.
+// Outputs: the full checkpoint (table checkpoint + dense weights; ckpt_len
+// bytes, capacity ckpt_cap), per-iteration losses, final dense weights.
+int fsref_pipeline_run(int world, int batch, std::uint64_t max_uih, std::uint64_t lo, std::uint64_t hi,
+                       std::uint64_t wl_table_rows, double target, int has_target, std::uint64_t seed, int iters,
+                       int prioritized, int balancer, int partition, double alpha, std::uint32_t dim,
+                       std::uint64_t table_rows, double lr_emb, double lr_dense, std::uint64_t model_seed,
+                       double c0, double c1, double c2, std::uint8_t* ckpt, std::uint64_t ckpt_cap,
+                       std::uint64_t* ckpt_len, double* losses, double* dense) {
+  SHIM_TRY
+  const auto spec = pipeline_spec(world, batch, max_uih, lo, hi, wl_table_rows, target, has_target, seed, iters);
+  pipeline::RunConfig cfg;
+  cfg.mode = prioritized ? pipeline::Mode::Prioritized : pipeline::Mode::Synchronized;
+  cfg.balancer_enabled = balancer != 0;
+  cfg.partition = partition == 0 ? "fbs" : partition == 1 ? "vbs" : "none";
+  cfg.alpha = alpha;
+  cfg.dim = dim;
+  cfg.table_rows = table_rows;
+  cfg.lr_embedding = lr_emb;
+  cfg.lr_dense = lr_dense;
+  cfg.model_seed = model_seed;
+  cfg.cost.c0 = c0;
+  cfg.cost.c1 = c1;
+  cfg.cost.c2 = c2;
+  const auto res = pipeline::run(workload::generate_all(spec), spec, cfg);
+  *ckpt_len = res.full_checkpoint.size();
+  if (ckpt && ckpt_cap >= res.full_checkpoint.size())
+    std::memcpy(ckpt, res.full_checkpoint.data(), res.full_checkpoint.size());
+  for (std::size_t i = 0; i < res.losses.size(); ++i) losses[i] = res.losses[i];
+  for (std::size_t d = 0; d < res.final_dense.size(); ++d) dense[d] = res.final_dense[d];
   SHIM_CATCH
 }
 
