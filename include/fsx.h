@@ -232,6 +232,11 @@ int fsx_engine_exposed_ms(fsx_engine* e, double* ms);
 #define FSX_PHASE_EXPOSED 13  /* C: compute stream stalled on embedding traffic   */
 #define FSX_NUM_PHASES 14
 int fsx_engine_set_profiling(fsx_engine* e, int on);
+/* Collision chain's E_co delivery (prioritized engine, between iterations, the
+ * same on every rank): 0 (default) = staged + copy-engine all-to-all (0 SMs);
+ * 1 = the collision update kernel stores each updated row straight into the
+ * requesters' windows over NVLink (one hop less; SM-issued communication). */
+int fsx_engine_set_eco_direct(fsx_engine* e, int on);
 /* timeline of the recorded spans: out[3k..3k+2] = (phase, start ms, end ms)
  * relative to the earliest span; consumes them (synchronizes) */
 int fsx_engine_spans(fsx_engine* e, double* out, uint64_t max_spans, uint64_t* n_spans);

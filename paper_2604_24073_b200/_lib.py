@@ -75,6 +75,7 @@ _SIGS = {
     "fsx_engine_set_profiling": ([vp, i32], i32),
     "fsx_engine_set_ids_ready": ([vp, i32], i32),
     "fsx_engine_join": ([vp, vp], i32),
+    "fsx_engine_set_eco_direct": ([vp, i32], i32),
     "fsx_pooled_create": ([vp, u64, u64, u32, P(vp)], i32),
     "fsx_pooled_destroy": ([vp], i32),
     "fsx_pooled_forward": ([vp, vp, vp, u64, u64, vp, vp], i32),

@@ -465,8 +465,29 @@ struct SideLane {
   }
 };
 
+// FSX_HOST_PROF=1 (diagnostic): host nanoseconds per category, printed when
+// the engine is destroyed — where a host-bound step's enqueue time goes
+enum HostProfSlot { HP_FWD, HP_BWD, HP_WAIT_SIDE, HP_SIDE_JOB, HP_SIZES, HP_FETCH, HP_A2A, HP_N };
+
 struct Engine {
   Ctx* ctx = nullptr;
+  bool host_prof = std::getenv("FSX_HOST_PROF") != nullptr;
+  std::atomic<uint64_t> hp_ns[HP_N] = {};
+  std::atomic<uint64_t> hp_calls[HP_N] = {};
+  struct HostTimer {
+    Engine* e;
+    int slot;
+    std::chrono::steady_clock::time_point t0;
+    HostTimer(Engine* en, int k) : e(en->host_prof ? en : nullptr), slot(k) {
+      if (e) t0 = std::chrono::steady_clock::now();
+    }
+    ~HostTimer() {
+      if (!e) return;
+      e->hp_ns[slot] += static_cast<uint64_t>(
+          std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0).count());
+      ++e->hp_calls[slot];
+    }
+  };
   std::unique_ptr<SideLane> side;  // p > 1 only
   std::mutex ev_mu;                // event pools are shared by both host threads
   Table* t = nullptr;
@@ -643,6 +664,7 @@ struct Engine {
   }
 
   std::vector<uint64_t> fetch(const uint64_t* d, int n, cudaStream_t s) {
+    HostTimer ht(this, HP_FETCH);
     if (debug)
       std::fprintf(stderr, "[fsx r%d] fetch on %s\n", me, s == lo ? "L" : s == hi ? "H" : "C");
     std::vector<uint64_t> h(n);
@@ -724,6 +746,7 @@ struct Engine {
   bool presum() const { return (cfg.flags & FSX_ENGINE_PRESUM) != 0; }
 
   void a2a_ce(int ch, int par, const std::vector<uint64_t>& bytes, cudaStream_t s) {
+    HostTimer ht(this, HP_A2A);
     const uint32_t v = seq[ch];
     if (debug)
       std::fprintf(stderr, "[fsx r%d] a2a ch=%d seq=%u par=%d stream=%s\n", me, ch, v, par,
@@ -1469,9 +1492,9 @@ struct Engine {
     };
     cudaEvent_t ex_ready_cur = cur_ex_ready;  // E_ex(i), recorded by the previous prep
     if (side) {
-      ticket_mask = side->post(prep1);
-      ticket_pack = side->post(prep2a);
-      ticket_next = side->post(prep2);
+      ticket_mask = side->post([this, prep1] { HostTimer ht(this, HP_SIDE_JOB); prep1(); });
+      ticket_pack = side->post([this, prep2a] { HostTimer ht(this, HP_SIDE_JOB); prep2a(); });
+      ticket_next = side->post([this, prep2] { HostTimer ht(this, HP_SIDE_JOB); prep2(); });
     } else {
       prep1();
       prep2a();
@@ -1495,9 +1518,11 @@ struct Engine {
   cudaEvent_t cur_ex_ready = nullptr, cur_co_ready = nullptr, rn_ex_ready = nullptr;
   uint64_t ticket_mask = 0, ticket_pack = 0, ticket_next = 0;  // side-lane jobs of the last forward
   void wait_pack_ready() {
+    HostTimer ht(this, HP_WAIT_SIDE);
     if (side) side->wait_for(ticket_pack);
   }
   void wait_next_ready() {
+    HostTimer ht(this, HP_WAIT_SIDE);
     if (side) side->wait_for(ticket_next);
   }
   bool has_next = false;
@@ -1530,7 +1555,10 @@ struct Engine {
     if (d.hchain) wait(ux, d.hchain);
     if (p > 1) {
       std::vector<uint64_t> bytes(p);
-      rp.sizes(p);
+      {
+        HostTimer ht(this, HP_SIZES);
+        rp.sizes(p);
+      }
       for (int d2 = 0; d2 < p; ++d2) bytes[d2] = kHdr + rb * rp.h_split[2 * d2];
       a2a(CH_EXG, d.par, bytes, ux);
     }
@@ -1540,7 +1568,10 @@ struct Engine {
 
   void prio_backward(const void* grads, cudaStream_t c) {
     if (!forward_done) raise(FSX_ERR_PROTOCOL, "embedding: backward before forward");
-    if (side) side->wait_for(ticket_mask);  // masks + split counts of this iteration are issued
+    if (side) {
+      HostTimer ht(this, HP_WAIT_SIDE);
+      side->wait_for(ticket_mask);  // masks + split counts of this iteration are issued
+    }
     const int i = iter;
     ReqBatch& rc = R(i);
     OwnBatch& oc = O(i);
@@ -1588,7 +1619,10 @@ struct Engine {
         if (presum()) {
           if (p > 1) {
             std::vector<uint64_t> bytes(p);
-            rc.sizes(p);
+            {
+              HostTimer ht(this, HP_SIZES);
+              rc.sizes(p);
+            }
             for (int d = 0; d < p; ++d) bytes[d] = kHdr + rb * rc.h_slots[d];
             a2a(CH_COG, cog, bytes, hi);
           }
@@ -1604,7 +1638,10 @@ struct Engine {
         } else {
           if (p > 1) {
             std::vector<uint64_t> bytes(p);
-            rc.sizes(p);
+            {
+              HostTimer ht(this, HP_SIZES);
+              rc.sizes(p);
+            }
             for (int d = 0; d < p; ++d) bytes[d] = kHdr + rb * rc.h_split[2 * d + 1];
             a2a(CH_COG, cog, bytes, hi);
           }
@@ -1697,6 +1734,15 @@ struct Engine {
   }
 
   ~Engine() {
+    if (host_prof) {
+      static const char* names[HP_N] = {"forward", "backward", "wait_side", "side_jobs", "sizes_sync", "fetch_sync",
+                                        "a2a_issue"};
+      std::fprintf(stderr, "[fsx host r%d]", me);
+      for (int k = 0; k < HP_N; ++k)
+        std::fprintf(stderr, " %s %.3f ms/%llu", names[k], 1e-6 * static_cast<double>(hp_ns[k].load()),
+                     static_cast<unsigned long long>(hp_calls[k].load()));
+      std::fprintf(stderr, "\n");
+    }
     side.reset();
     cudaDeviceSynchronize();
     for (int d = 0; d < kMaxRanks; ++d)
@@ -1919,6 +1965,7 @@ int fsx_engine_forward(fsx_engine* e, const uint64_t* d_ids_cur, uint64_t n_cur,
   FSX_API_BEGIN
   DeviceGuard dg(e->ctx->device);
   e->cur_c = S(stream);
+  Engine::HostTimer ht(e, HP_FWD);
   if (e->cfg.mode == FSX_MODE_SYNC)
     e->sync_forward(d_ids_cur, n_cur, d_out, S(stream));
   else
@@ -1930,6 +1977,7 @@ int fsx_engine_backward(fsx_engine* e, const void* d_grads, void* stream) {
   FSX_API_BEGIN
   DeviceGuard dg(e->ctx->device);
   e->cur_c = S(stream);
+  Engine::HostTimer ht(e, HP_BWD);
   if (e->cfg.mode == FSX_MODE_SYNC)
     e->sync_backward(d_grads, S(stream));
   else
@@ -2016,6 +2064,13 @@ int fsx_engine_join(fsx_engine* e, void* stream) {
 int fsx_engine_set_ids_ready(fsx_engine* e, int ready) {
   FSX_API_BEGIN
   e->ids_ready = ready != 0;
+  FSX_API_END
+}
+
+int fsx_engine_set_eco_direct(fsx_engine* e, int on) {
+  FSX_API_BEGIN
+  if (e->forward_done) raise(FSX_ERR_PROTOCOL, "fsx: E_co mode changes between iterations only");
+  e->eco_direct = on != 0;
   FSX_API_END
 }
 

@@ -319,6 +319,11 @@ class _Engine:
         """Device id tensors passed to forward are complete when passed."""
         _lib.call("fsx_engine_set_ids_ready", self.h, int(ready))
 
+    def set_eco_direct(self, on: bool) -> None:
+        """E_co by direct NVLink stores from the collision update (SM-issued)
+        instead of the copy engines; between iterations, on every rank."""
+        _lib.call("fsx_engine_set_eco_direct", self.h, int(on))
+
     def join(self, stream=None) -> None:
         """Order every lane's issued work before `stream` (timing regions)."""
         _lib.call("fsx_engine_join", self.h, _stream(stream))
