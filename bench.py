@@ -795,12 +795,14 @@ def main():
             e1.record(stream)
             barrier()
             res["prio_ce"] = (e0.elapsed_time(e1) / K, eng.exposed_ms() / K)
-            # (B') the same with E_co stored by the collision update straight
-            # into the requesters' windows (one hop less; SM-issued stores)
+            # (B') the same with the collision chain's transfers stored by its
+            # kernels straight into the peers' windows: the pre-sum into the
+            # owners' CO_G slots, the collision update into the requesters'
+            # E_co slots (SM-issued NVLink stores; no copy-engine hop)
             if world > 1:
                 eng.join(stream)
                 stream.synchronize()
-                eng.set_eco_direct(True)
+                eng.set_eco_direct(True, cog=True)
                 eng.exposed_ms()
                 barrier()
                 it1 = it0 + K
@@ -813,7 +815,7 @@ def main():
                 eng.join(stream)
                 e1.record(stream)
                 barrier()
-                res["prio_ce_eco_direct"] = (e0.elapsed_time(e1) / K, eng.exposed_ms() / K)
+                res["prio_direct"] = (e0.elapsed_time(e1) / K, eng.exposed_ms() / K)
                 eng.set_eco_direct(False)
         # (A) the blocking baseline: synchronized engine, NCCL all-to-all (N>1)
         base_tr = "nccl" if world > 1 else "ce"
@@ -855,9 +857,9 @@ def main():
         exp_b_ns = max_over_ranks(max(0.0, res[b_key][1] - skew))
         exp_p_ns = max_over_ranks(max(0.0, res["prio_ce"][1] - skew))
         exp_d = exp_d_ns = None
-        if "prio_ce_eco_direct" in res:
-            exp_d = max_over_ranks(res["prio_ce_eco_direct"][1])
-            exp_d_ns = max_over_ranks(max(0.0, res["prio_ce_eco_direct"][1] - skew))
+        if "prio_direct" in res:
+            exp_d = max_over_ranks(res["prio_direct"][1])
+            exp_d_ns = max_over_ranks(max(0.0, res["prio_direct"][1] - skew))
         exp_b_sum = sum_over_ranks(res[b_key][1])
         exp_p_sum = sum_over_ranks(res["prio_ce"][1])
         cfg5_out = {
@@ -871,13 +873,17 @@ def main():
             "exposed_ms_per_iter_max_over_ranks": {b_key: round(exp_b, 4), "prio_ce": round(exp_p, 4)},
             "exposed_ms_per_iter_sum_over_ranks": {b_key: round(exp_b_sum, 4), "prio_ce": round(exp_p_sum, 4)},
             "exposed_reduction_pct": round(100.0 * (1 - exp_p / exp_b), 2) if exp_b > 0 else None,
-            # E_co by SM-issued NVLink stores from the collision update (one hop less)
-            "prio_ce_eco_direct": ({"exposed_ms_per_iter_max_over_ranks": round(exp_d, 4),
-                                    "exposed_reduction_pct": round(100.0 * (1 - exp_d / exp_b), 2),
-                                    "exposed_reduction_pct_beyond_victim_skew":
-                                        round(100.0 * (1 - exp_d_ns / exp_b_ns), 2) if exp_b_ns > 0 else None,
-                                    "comm_sms": "E_co stores issued by the collision-update kernel's SMs"}
-                                   if exp_d is not None else None),
+            # the collision chain's CO_G and E_co by SM-issued NVLink stores
+            # from the pre-sum and collision-update kernels (no copy-engine hop)
+            "prio_direct": ({"exposed_ms_per_iter_max_over_ranks": round(exp_d, 4),
+                             "exposed_reduction_pct": round(100.0 * (1 - exp_d / exp_b), 2),
+                             "exposed_reduction_pct_beyond_victim_skew":
+                                 round(100.0 * (1 - exp_d_ns / exp_b_ns), 2) if exp_b_ns > 0 else None,
+                             "step_ms": round(max_over_ranks(res["prio_direct"][0]), 4),
+                             "comm_sms": ("CO_G / E_co rows stored by the pre-sum and collision-update "
+                                          "kernels' own SMs (no extra kernel); the other all-to-alls on "
+                                          "the copy engines")}
+                            if exp_d is not None else None),
             "exposed_ms_per_iter_beyond_victim_skew_max_over_ranks": {b_key: round(exp_b_ns, 4),
                                                                        "prio_ce": round(exp_p_ns, 4)},
             "exposed_reduction_pct_beyond_victim_skew": (round(100.0 * (1 - exp_p_ns / exp_b_ns), 2)

@@ -232,14 +232,22 @@ int fsx_engine_exposed_ms(fsx_engine* e, double* ms);
 #define FSX_PHASE_EXPOSED 13  /* C: compute stream stalled on embedding traffic   */
 #define FSX_NUM_PHASES 14
 int fsx_engine_set_profiling(fsx_engine* e, int on);
-/* Collision chain's E_co delivery (prioritized engine, between iterations, the
- * same on every rank): 0 (default) = staged + copy-engine all-to-all (0 SMs);
- * 1 = the collision update kernel stores each updated row straight into the
- * requesters' windows over NVLink (one hop less; SM-issued communication). */
+/* Collision chain's transfers (prioritized engine, between iterations, the
+ * same on every rank), a bit mask: 0 (default) = staged + copy-engine
+ * all-to-alls (0 SMs); bit 0 = the collision update kernel stores each updated
+ * E_co row straight into the requesters' windows over NVLink; bit 1 (PRESUM) =
+ * the pre-sum kernel stores the collision gradients straight into the owners'
+ * windows. Direct stores are SM-issued communication riding the compute
+ * kernels (no extra kernel, one hop less, no copy-engine serialisation). */
 int fsx_engine_set_eco_direct(fsx_engine* e, int on);
 /* timeline of the recorded spans: out[3k..3k+2] = (phase, start ms, end ms)
  * relative to the earliest span; consumes them (synchronizes) */
 int fsx_engine_spans(fsx_engine* e, double* out, uint64_t max_spans, uint64_t* n_spans);
+/* the same spans with their lane and host issue time: out[6k..6k+5] =
+ * (phase, lane (0 caller, 1 L, 2 H, 3 X, 4 top-priority, 5 a copy stream),
+ * all-to-all channel (one copy: 1000 + 16 * channel + destination) or -1, GPU start ms, GPU end ms relative to the earliest span, host issue
+ * time in CLOCK_MONOTONIC ms); consumes them */
+int fsx_engine_trace(fsx_engine* e, double* out, uint64_t max_spans, uint64_t* n_spans);
 /* device ids handed to forward are complete (no pending writes on any stream) */
 /* Orders everything the engine has issued on its own lanes (side-lane jobs,
  * priority lanes, copy-engine streams) before `stream`. No protocol effect:

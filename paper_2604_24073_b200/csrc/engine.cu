@@ -296,6 +296,9 @@ struct ReqBatch {  // requester view of one iteration's ids
   uint64_t* hp_sizes = nullptr;
   cudaEvent_t ev_sizes = nullptr;
   bool sizes_pending = false, sizes_slots = false;
+  // PRESUM, direct CO_G: the pre-sum kernel stores each (owner, row) sum
+  // straight into the owner's receive window (fixed when the masks are built)
+  bool cog_direct = false;
   void sizes(int p) {
     if (!sizes_pending) return;
     FSX_CUDA(cudaEventSynchronize(ev_sizes));
@@ -472,6 +475,7 @@ enum HostProfSlot { HP_FWD, HP_BWD, HP_WAIT_SIDE, HP_SIDE_JOB, HP_SIZES, HP_FETC
 struct Engine {
   Ctx* ctx = nullptr;
   bool host_prof = std::getenv("FSX_HOST_PROF") != nullptr;
+  bool trace_copies = std::getenv("FSX_TRACE_COPIES") != nullptr;
   std::atomic<uint64_t> hp_ns[HP_N] = {};
   std::atomic<uint64_t> hp_calls[HP_N] = {};
   struct HostTimer {
@@ -550,7 +554,15 @@ struct Engine {
   size_t timing_next = 0;
   // live phase timing (fsx_engine_set_profiling)
   bool prof = false;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> spans[FSX_NUM_PHASES];
+  // one span: its events, the lane it ran on (0 caller, 1 L, 2 H, 3 X, 4 the
+  // top-priority lane), the channel of an all-to-all (-1 otherwise) and the
+  // host time it was issued (timeline traces: fsx_engine_trace)
+  struct SpanRec {
+    cudaEvent_t first, second;
+    int lane, ch;
+    int64_t host_ns;
+  };
+  std::vector<SpanRec> spans[FSX_NUM_PHASES];
   std::vector<cudaEvent_t> prof_pool;
   size_t prof_next = 0;
   cudaEvent_t prof_event() {
@@ -562,13 +574,26 @@ struct Engine {
     }
     return prof_pool[prof_next++];
   }
+  int lane_code(cudaStream_t s) const {
+    if (s == lo) return 1;
+    if (s == hi) return 2;
+    if (s == ux) return 3;
+    if (us && s == us) return 4;
+    for (int l = 0; l < kLanes; ++l)
+      for (int d = 0; d < p; ++d)
+        if (cstream[l][d] && s == cstream[l][d]) return 5;
+    return 0;
+  }
   struct Span {
     Engine* e;
-    int phase;
+    int phase, ch;
     cudaStream_t s;
     cudaEvent_t a = nullptr;
-    Span(Engine* eng, int ph, cudaStream_t st) : e(eng), phase(ph), s(st) {
-      if (e->prof) {
+    int64_t hns = 0;
+    Span(Engine* eng, int ph, cudaStream_t st, int chan = -1) : e(eng), phase(ph), ch(chan), s(st) {
+      if (e->prof && (ch < 1000 || st)) {
+        hns = std::chrono::duration_cast<std::chrono::nanoseconds>(
+                  std::chrono::steady_clock::now().time_since_epoch()).count();
         a = e->prof_event();
         FSX_CUDA(cudaEventRecord(a, s));
       }
@@ -578,7 +603,7 @@ struct Engine {
         cudaEvent_t b = e->prof_event();
         cudaEventRecord(b, s);
         std::lock_guard<std::mutex> lk(e->ev_mu);
-        e->spans[phase].emplace_back(a, b);
+        e->spans[phase].push_back(SpanRec{a, b, e->lane_code(s), ch, hns});
       }
     }
   };
@@ -702,7 +727,7 @@ struct Engine {
 
   void a2a_nccl(int ch, int par, const std::vector<uint64_t>& bytes,
                 const std::vector<uint64_t>* recv_bytes, cudaStream_t s) {
-    Span sp(this, FSX_PHASE_A2A, s);
+    Span sp(this, FSX_PHASE_A2A, s, ch);
     NcclApi& N = NcclApi::get();
     std::vector<uint64_t> rb_local;
     if (!recv_bytes) {
@@ -751,7 +776,7 @@ struct Engine {
     if (debug)
       std::fprintf(stderr, "[fsx r%d] a2a ch=%d seq=%u par=%d stream=%s\n", me, ch, v, par,
                    s == lo ? "L" : s == hi ? "H" : "C");
-    Span sp(this, FSX_PHASE_A2A, s);
+    Span sp(this, FSX_PHASE_A2A, s, ch);
     // fork: each peer's copy + flag on its own copy stream (parallel copy
     // engines), join back into `s` below
     cudaEvent_t fork = record(s);
@@ -762,7 +787,11 @@ struct Engine {
       cudaStream_t cs = cstream[lane_of(s)][d];
       wait(cs, fork);
       char* dst = pv.base + ch_off[ch] + (static_cast<size_t>(par) * p + me) * ch_slot[ch];
-      if (bytes[d]) FSX_CUDA(cudaMemcpyAsync(dst, stage_slot(ch, par, d), bytes[d], cudaMemcpyDefault, cs));
+      {
+        // FSX_TRACE_COPIES: a span per copy for fsx_engine_trace (not in the phase sums)
+        Span cp(this, FSX_PHASE_A2A, trace_copies ? cs : nullptr, 1000 + 16 * ch + d);
+        if (bytes[d]) FSX_CUDA(cudaMemcpyAsync(dst, stage_slot(ch, par, d), bytes[d], cudaMemcpyDefault, cs));
+      }
       if (pv.local) {
         cudaEvent_t ev;
         FSX_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -1128,6 +1157,7 @@ struct Engine {
   // (embedding.cpp:392-408, 524-536)
   void masks_and_split(OwnBatch& oc, ReqBatch& rc, bool with_co, cudaStream_t s) {
     Span sp(this, FSX_PHASE_MASKS, s);
+    rc.cog_direct = false;
     if (p == 1 && !presum()) {
       // one rank: the update needs no masks or split plan (it runs whole on
       // the caller's stream); only the statistics need the totals
@@ -1135,9 +1165,11 @@ struct Engine {
       FSX_LAUNCH(ctx, k_self_split_totals, 1, 32, 0, s, oc.srt.d_n(), oc.misc.p, with_co ? 1 : 0, rc.split_tot.p,
                  oc.occ_tot());
       rc.has_flags = false;
+      rc.cog_direct = false;
       return;
     }
     if (with_co && presum()) {
+      rc.cog_direct = cog_direct && p > 1;
       // GRP messages: each source's collision occurrences grouped by row
       const int par = next_par(CH_GRP);
       Slots send = send_slots(CH_GRP, par);
@@ -1165,7 +1197,8 @@ struct Engine {
       CSlots grp = recv_slots(CH_GRP, par);
       FSX_LAUNCH(ctx, k_grp_bases, 1, 32, 0, s, grp, p, rc.bases.p);
       FSX_LAUNCH(ctx, k_grp_flatten, grid_for(ctx, static_cast<uint64_t>(p) * (cap + 1), 256, 8), 256, 0, s,
-                 grp, p, cap, rc.bases.p, rc.send_off(), rc.send_pos.p, send_slots(CH_COG, cog_par_next()),
+                 grp, p, cap, rc.bases.p, rc.send_off(), rc.send_pos.p,
+                 cog_direct && p > 1 ? remote_slots(CH_COG, cog_par_next()) : send_slots(CH_COG, cog_par_next()),
                  rb, rc.flag.p, rc.seg_flat.p, rc.perm_flat.p, rc.out_ptr.p);
       // the pre-sum's work lists: the segments and the caller's gradient
       // positions are known now, the gradients only at the backward
@@ -1229,7 +1262,13 @@ struct Engine {
   // FSX_ECO_DIRECT=1 (opt-in): the collision update stores E_co rows straight
   // into the peers' windows over NVLink — SM-issued communication. Off by
   // default: every byte between ranks then moves on the copy engines (0 SMs).
+  // FSX_COG_DIRECT=1 (opt-in, PRESUM): likewise the pre-sum kernel stores the
+  // collision gradients into the owners' windows. The copy engines run one
+  // copy at a time per GPU (measured: a rank's p-1 copies of an all-to-all
+  // serialise), so on the collision chain the fused stores cut the transfer
+  // to the kernels' own NVLink stores and one flag round.
   bool eco_direct = false;
+  bool cog_direct = false;
   Slots remote_slots(int ch, int par) const {
     Slots r{};
     for (int d = 0; d < p; ++d)
@@ -1240,7 +1279,7 @@ struct Engine {
   // flags of a channel whose payload the sender's kernels already stored into
   // the peers' windows (ordered by `s`), then wait for every peer's
   void signal_direct(int ch, cudaStream_t s) {
-    Span sp(this, FSX_PHASE_A2A, s);
+    Span sp(this, FSX_PHASE_A2A, s, ch);
     const uint32_t v = seq[ch];
     for (int k = 1; k < p; ++k) {
       const int d = (me + k) % p;
@@ -1304,7 +1343,7 @@ struct Engine {
   // half, which overlaps the collision all-to-all
   void split_co(ReqBatch& r, const void* d_grads, int cog_par, cudaStream_t s) {
     Span sp(this, FSX_PHASE_SPLIT, s);
-    Slots co = send_slots(CH_COG, cog_par);
+    Slots co = r.cog_direct ? remote_slots(CH_COG, cog_par) : send_slots(CH_COG, cog_par);
     if (!r.has_flags) {
       FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, co, p, r.split_tot.p + 1, 2, cap, ctx->d_err);
       return;
@@ -1617,7 +1656,9 @@ struct Engine {
         // collision chain, high priority (embedding.cpp:539-557)
         wait(hi, ev_chain_start);
         if (presum()) {
-          if (p > 1) {
+          if (p > 1 && rc.cog_direct) {
+            signal_direct(CH_COG, hi);  // the pre-sum already stored the rows
+          } else if (p > 1) {
             std::vector<uint64_t> bytes(p);
             {
               HostTimer ht(this, HP_SIZES);
@@ -1805,6 +1846,7 @@ int fsx_engine_create(fsx_ctx* ctx, fsx_table* table, const fsx_engine_config* c
   e->cap = std::max<uint64_t>(cfg->max_occurrences, 1);
   e->rb = table->row_bytes();
   if (const char* v = std::getenv("FSX_ECO_DIRECT")) e->eco_direct = std::atoi(v) != 0;
+  if (const char* v = std::getenv("FSX_COG_DIRECT")) e->cog_direct = std::atoi(v) != 0;
   const bool prio = cfg->mode == FSX_MODE_PRIO;
   const uint64_t cap = e->cap, rb = e->rb;
   auto round256 = [](uint64_t x) { return (x + 255) & ~uint64_t(255); };
@@ -2054,6 +2096,46 @@ int fsx_engine_spans(fsx_engine* e, double* out, uint64_t max_spans, uint64_t* n
   FSX_API_END
 }
 
+// Timeline trace: per span (phase, lane, channel, GPU start ms, GPU end ms,
+// host issue ms), GPU times relative to the earliest span start and host
+// issue times in CLOCK_MONOTONIC ms; consumes the spans like fsx_engine_spans.
+int fsx_engine_trace(fsx_engine* e, double* out, uint64_t max_spans, uint64_t* n_out) {
+  FSX_API_BEGIN
+  DeviceGuard dg(e->ctx->device);
+  if (e->side) e->side->drain();
+  FSX_CUDA(cudaDeviceSynchronize());
+  cudaEvent_t base = nullptr;
+  float best = 0;
+  for (auto& v : e->spans)
+    for (auto& sp : v) {
+      if (!base) { base = sp.first; continue; }
+      float x = 0;
+      FSX_CUDA(cudaEventElapsedTime(&x, base, sp.first));
+      if (x < best) best = x;
+    }
+  uint64_t k = 0;
+  for (int ph = 0; ph < FSX_NUM_PHASES; ++ph) {
+    for (auto& sp : e->spans[ph]) {
+      if (k >= max_spans) break;
+      float a = 0, b = 0;
+      FSX_CUDA(cudaEventElapsedTime(&a, base, sp.first));
+      FSX_CUDA(cudaEventElapsedTime(&b, base, sp.second));
+      double* o = out + 6 * k;
+      o[0] = ph;
+      o[1] = sp.lane;
+      o[2] = sp.ch;
+      o[3] = a - best;
+      o[4] = b - best;
+      o[5] = sp.host_ns * 1e-6;  // CLOCK_MONOTONIC ms
+      ++k;
+    }
+    e->spans[ph].clear();
+  }
+  e->prof_next = 0;
+  *n_out = k;
+  FSX_API_END
+}
+
 int fsx_engine_join(fsx_engine* e, void* stream) {
   FSX_API_BEGIN
   DeviceGuard dg(e->ctx->device);
@@ -2070,7 +2152,8 @@ int fsx_engine_set_ids_ready(fsx_engine* e, int ready) {
 int fsx_engine_set_eco_direct(fsx_engine* e, int on) {
   FSX_API_BEGIN
   if (e->forward_done) raise(FSX_ERR_PROTOCOL, "fsx: E_co mode changes between iterations only");
-  e->eco_direct = on != 0;
+  e->eco_direct = (on & 1) != 0;
+  e->cog_direct = (on & 2) != 0;
   FSX_API_END
 }
 
@@ -2086,14 +2169,17 @@ int fsx_engine_phase_ms(fsx_engine* e, int phase, double* total_ms, uint64_t* co
   if (e->side) e->side->drain();
   if (phase < 0 || phase >= FSX_NUM_PHASES) raise(FSX_ERR_OUT_OF_RANGE, "fsx: bad phase");
   double t = 0;
+  uint64_t c = 0;
   for (auto& sp : e->spans[phase]) {
+    if (sp.ch >= 1000) continue;  // per-copy trace spans
     FSX_CUDA(cudaEventSynchronize(sp.second));
     float x = 0;
     FSX_CUDA(cudaEventElapsedTime(&x, sp.first, sp.second));
     t += x;
+    ++c;
   }
   *total_ms = t;
-  *count = e->spans[phase].size();
+  *count = c;
   e->spans[phase].clear();
   bool any = false;
   for (auto& v : e->spans) any = any || !v.empty();

@@ -320,8 +320,12 @@ constexpr uint32_t kSgdSingleChunk = 0x80000000u;
 // k_sgd_stream work split: cost = ring entries + kStreamItemCost per item
 constexpr uint64_t kStreamItemCost = 2;
 
+#ifndef FSX_PLAN_IPT
+#define FSX_PLAN_IPT 2
+#endif
 struct SgdPlanOp {
   static constexpr int NC = 4;
+  static constexpr int kIPT = FSX_PLAN_IPT;  // tens of thousands of rows: spread over every SM
   RowSegments rs;
   uint32_t chunk;
   SgdItem* singles;     // one-occurrence rows

@@ -16,13 +16,31 @@
 // tiles beyond *d_n exit early, so chains of these never need a host sync.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace fsx {
 
 constexpr int kScanThreads = 256;
-constexpr int kScanIPT = 8;
+#ifndef FSX_SCAN_IPT
+#define FSX_SCAN_IPT 8
+#endif
+constexpr int kScanIPT = FSX_SCAN_IPT;  // items per thread unless the Op says otherwise
 constexpr int kScanTile = kScanThreads * kScanIPT;
+
+// Items per thread of an Op's scan: Op::kIPT when it declares one. Ops whose
+// live count is small next to the GPU (a few tens of thousands of rows) use
+// fewer items per thread so their tiles spread over every SM: these scans are
+// latency-bound chains of dependent loads, not bandwidth-bound.
+template <class Op, class = void>
+struct ScanIPT {
+  static constexpr int v = kScanIPT;
+};
+template <class Op>
+struct ScanIPT<Op, std::void_t<decltype(Op::kIPT)>> {
+  static constexpr int v = Op::kIPT;
+};
 
 __device__ __forceinline__ uint64_t scan_n(uint64_t n_cap, const uint64_t* d_n) {
   if (d_n == nullptr) return n_cap;
@@ -72,15 +90,16 @@ static __global__ void __launch_bounds__(kScanThreads) k_tile_reduce(Op op, uint
                                                               const uint64_t* d_n,
                                                               uint32_t* tile_sums) { FSX_PDL_ENTER();
   constexpr int NC = Op::NC;
+  constexpr int IPT = ScanIPT<Op>::v;
   const uint64_t n = scan_n(n_cap, d_n);
-  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile;
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * (kScanThreads * IPT);
   uint32_t acc[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) acc[c] = 0;
   if (base < n) {
-    const uint64_t first = base + static_cast<uint64_t>(threadIdx.x) * kScanIPT;
+    const uint64_t first = base + static_cast<uint64_t>(threadIdx.x) * IPT;
 #pragma unroll
-    for (int q = 0; q < kScanIPT; ++q) {
+    for (int q = 0; q < IPT; ++q) {
       const uint64_t i = first + q;
       if (i < n) {
         uint32_t cnt[NC];
@@ -152,9 +171,10 @@ static __global__ void __launch_bounds__(kScanThreads) k_tile_emit(Op op, uint64
                                                                    unsigned tiles,
                                                                    uint64_t* d_totals) { FSX_PDL_ENTER();
   constexpr int NC = Op::NC;
+  constexpr int IPT = ScanIPT<Op>::v;
   __shared__ uint32_t s_pre[NC], s_tot[NC];
   const uint64_t n = scan_n(n_cap, d_n);
-  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile;
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * (kScanThreads * IPT);
   if (base >= n && blockIdx.x != 0) return;  // whole CTA exits together
   // prefix of this tile and grand totals, straight from the tile sums (L2)
   {
@@ -192,12 +212,12 @@ static __global__ void __launch_bounds__(kScanThreads) k_tile_emit(Op op, uint64
     __syncthreads();
   }
   if (base >= n) return;  // CTA 0 of an empty input: totals stored, nothing to emit
-  const uint64_t first = base + static_cast<uint64_t>(threadIdx.x) * kScanIPT;
+  const uint64_t first = base + static_cast<uint64_t>(threadIdx.x) * IPT;
   uint32_t run[NC], tot[NC];
 #pragma unroll
   for (int c = 0; c < NC; ++c) { run[c] = 0; tot[c] = s_tot[c]; }
 #pragma unroll
-  for (int q = 0; q < kScanIPT; ++q) {
+  for (int q = 0; q < IPT; ++q) {
     const uint64_t i = first + q;
     if (i < n) {
       uint32_t cnt[NC];
@@ -211,7 +231,7 @@ static __global__ void __launch_bounds__(kScanThreads) k_tile_emit(Op op, uint64
 #pragma unroll
   for (int c = 0; c < NC; ++c) run[c] += s_pre[c];
 #pragma unroll
-  for (int q = 0; q < kScanIPT; ++q) {
+  for (int q = 0; q < IPT; ++q) {
     const uint64_t i = first + q;
     if (i < n) {
       uint32_t cnt[NC];
@@ -226,8 +246,8 @@ static __global__ void __launch_bounds__(kScanThreads) k_tile_emit(Op op, uint64
 // Scratch for one scan of up to `n_cap` items with NC counters.
 struct ScanScratch {
   DevBuf<uint32_t> tiles;
-  void ensure(uint64_t n_cap, int nc) {
-    tiles.ensure(static_cast<size_t>(ceil_div(n_cap > 0 ? n_cap : 1, kScanTile)) * nc);
+  void ensure(uint64_t n_cap, int nc, int tile = kScanTile) {
+    tiles.ensure(static_cast<size_t>(ceil_div(n_cap > 0 ? n_cap : 1, tile)) * nc);
   }
 };
 
@@ -241,8 +261,9 @@ void run_scan(Ctx* ctx, const Op& op, uint64_t n_cap, const uint64_t* d_n, ScanS
     if (d_totals) FSX_CUDA(cudaMemsetAsync(d_totals, 0, sizeof(uint64_t) * NC, stream));
     return;
   }
-  s.ensure(n_cap, NC);
-  const unsigned tiles = ceil_div(n_cap, kScanTile);
+  constexpr int kTile = kScanThreads * ScanIPT<Op>::v;
+  s.ensure(n_cap, NC, kTile);
+  const unsigned tiles = ceil_div(n_cap, kTile);
   FSX_LAUNCH(ctx, k_tile_reduce<Op>, tiles, kScanThreads, 0, stream, op, n_cap, d_n, s.tiles.p);
   FSX_LAUNCH(ctx, k_tile_emit<Op>, tiles, kScanThreads, 0, stream, op, n_cap, d_n, s.tiles.p, tiles,
              d_totals);

@@ -303,6 +303,9 @@ __global__ void __launch_bounds__(128, MINB) k_sgd_stream(SgdArgs<T> a, uint32_t
       }
     }
   }
+  // reduce-only outputs may be peer windows (direct CO_G): visible system-wide
+  // before the stream's flag write that follows the kernel
+  if (!table_mode) __threadfence_system();
   if (span && lane == 0) atomicMax(span + 1, global_ns());
 }
 

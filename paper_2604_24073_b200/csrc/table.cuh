@@ -113,12 +113,15 @@ template <class T, int NV, int R, int MINB, bool kBulk, bool kFused>
 void launch_sgd_stream(Ctx* ctx, const SgdArgs<T>& a, uint32_t rb, uint32_t* done, cudaStream_t stream) {
   constexpr int kWarps = 4;
   const size_t smem = ((kWarps * R * 8 + 127) & ~static_cast<size_t>(127)) + static_cast<size_t>(kWarps) * R * rb;
+  // function attributes are per device: one entry per (device, ring size)
+  // (in-process ranks on several GPUs each set them on their own device)
   static std::mutex m;
   static std::unordered_map<size_t, int>* occ = new std::unordered_map<size_t, int>();
   int per_sm;
   {
     std::lock_guard<std::mutex> g(m);
-    auto it = occ->find(smem);
+    const size_t key = smem * 1024 + static_cast<size_t>(ctx->device);
+    auto it = occ->find(key);
     if (it == occ->end()) {
       if (smem > 48 * 1024)
         FSX_CUDA(cudaFuncSetAttribute(k_sgd_stream<T, NV, R, MINB, kBulk, kFused>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -131,7 +134,7 @@ void launch_sgd_stream(Ctx* ctx, const SgdArgs<T>& a, uint32_t rb, uint32_t* don
       if (std::getenv("FSX_DEBUG"))
         std::fprintf(stderr, "[fsx] k_sgd_stream<%d,%d,%d> smem %zu B/CTA: %d CTAs/SM\n", static_cast<int>(sizeof(T)),
                      NV, R, smem, b);
-      it = occ->emplace(smem, b > 0 ? b : 1).first;
+      it = occ->emplace(key, b > 0 ? b : 1).first;
     }
     per_sm = it->second;
   }
@@ -140,7 +143,7 @@ void launch_sgd_stream(Ctx* ctx, const SgdArgs<T>& a, uint32_t rb, uint32_t* don
   // global times per launch, summed into ctx->stream_span_ns
   static unsigned long long* span = nullptr;  // device: [0] min start, [1] max end
   static const bool want_span = std::getenv("FSX_STREAM_SPAN") != nullptr;
-  if (want_span) {
+  if (want_span && ctx->device == 0) {  // (debug span: device 0 only)
     const unsigned long long init[2] = {~0ull, 0ull};
     if (!span) {
       FSX_CUDA(cudaMalloc(&span, sizeof(init)));
@@ -157,7 +160,7 @@ void launch_sgd_stream(Ctx* ctx, const SgdArgs<T>& a, uint32_t rb, uint32_t* don
     FSX_CUDA(cudaStreamSynchronize(stream));
   }
   FSX_LAUNCH(ctx, (k_sgd_stream<T, NV, R, MINB, kBulk, kFused>), static_cast<unsigned>(ctx->num_sms * per_sm), kWarps * 32, smem,
-             stream, a, rb, done, span);
+             stream, a, rb, done, ctx->device == 0 ? span : nullptr);
 }
 
 template <class T>

@@ -319,10 +319,12 @@ class _Engine:
         """Device id tensors passed to forward are complete when passed."""
         _lib.call("fsx_engine_set_ids_ready", self.h, int(ready))
 
-    def set_eco_direct(self, on: bool) -> None:
-        """E_co by direct NVLink stores from the collision update (SM-issued)
-        instead of the copy engines; between iterations, on every rank."""
-        _lib.call("fsx_engine_set_eco_direct", self.h, int(on))
+    def set_eco_direct(self, on, cog: bool = False) -> None:
+        """Collision chain transfers by direct NVLink stores from the compute
+        kernels (SM-issued) instead of the copy engines: E_co from the
+        collision update (`on`), and with `cog` (PRESUM) the collision
+        gradients from the pre-sum; between iterations, on every rank."""
+        _lib.call("fsx_engine_set_eco_direct", self.h, (1 if on else 0) | (2 if cog else 0))
 
     def join(self, stream=None) -> None:
         """Order every lane's issued work before `stream` (timing regions)."""
@@ -346,6 +348,16 @@ class _Engine:
         n = C.c_uint64()
         _lib.call("fsx_engine_spans", self.h, buf.ctypes.data, max_spans, C.byref(n))
         return [(_lib.PHASES[int(buf[3 * k])], buf[3 * k + 1], buf[3 * k + 2]) for k in range(n.value)]
+
+    def trace(self, max_spans: int = 100000):
+        """[(phase, lane, channel, gpu_start_ms, gpu_end_ms, host_issue_ms)] of every
+        recorded span (synchronizes; consumes them). Lanes: C L H X S, K = a copy
+        stream (its channel = 1000 + 16 * all-to-all channel + destination)."""
+        buf = np.zeros(6 * max_spans, np.float64)
+        n = C.c_uint64()
+        _lib.call("fsx_engine_trace", self.h, buf.ctypes.data, max_spans, C.byref(n))
+        return [(_lib.PHASES[int(buf[6 * k])], "CLHXSK"[int(buf[6 * k + 1])], int(buf[6 * k + 2]),
+                 buf[6 * k + 3], buf[6 * k + 4], buf[6 * k + 5]) for k in range(n.value)]
 
     def exposed_ms(self) -> float:
         v = C.c_double()

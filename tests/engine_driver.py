@@ -8,9 +8,12 @@ from paper_2604_24073_b200.comm import DeviceFabric
 
 
 def run_engine(prioritized, batches, geom, lr, seed, dtype="f64", reduce_chunk=0,
-               grad_scale=0.125, grad_shift=0.0625, devices=None, with_stats=False, presum=False):
+               grad_scale=0.125, grad_shift=0.0625, devices=None, with_stats=False, presum=False,
+               direct=0, direct_from=0):
     """batches[i][r] = rank r's ids of iteration i. Returns the final table
-    (f64, global order) and rank 0's IterationStats (prioritized)."""
+    (f64, global order) and rank 0's IterationStats (prioritized).
+    direct (prioritized): collision-chain transfer mask (1 = E_co, 2 = CO_G by
+    direct stores), switched on between iterations direct_from - 1 and direct_from."""
     world = geom.num_shards
     iters = len(batches)
     cap = max([len(b) for it in batches for b in it] + [1])
@@ -32,6 +35,8 @@ def run_engine(prioritized, batches, geom, lr, seed, dtype="f64", reduce_chunk=0
         with torch.cuda.stream(stream):
             for i in range(iters):
                 cur = batches[i][rank]
+                if prioritized and direct and i == direct_from:
+                    eng.set_eco_direct(direct & 1, cog=bool(direct & 2))
                 if prioritized:
                     nxt = batches[i + 1][rank] if i + 1 < iters else None
                     rows = eng.forward(cur, nxt, stream=stream)

@@ -27,7 +27,7 @@ from paper_2604_24073_b200.comm import ProcessGroupFabric  # noqa: E402
 OVERSUB = os.environ.get("FSX_MP_OVERSUB") == "1"
 
 
-def run(prio, dtype, batches, geom, rank, world, dev, chunk, presum=False, transport="ce"):
+def run(prio, dtype, batches, geom, rank, world, dev, chunk, presum=False, transport="ce", direct=0):
     fabric = ProcessGroupFabric(rank, world, dev)
     ctx = E.Context(dev, rank, world)
     shard = E.ShardView(geom, rank, 0.05, 3, dtype=dtype, ctx=ctx)
@@ -35,6 +35,8 @@ def run(prio, dtype, batches, geom, rank, world, dev, chunk, presum=False, trans
     cls = E.PrioritizedEmbedding if prio else E.SynchronizedEmbedding
     kw = {"presum": True} if (prio and presum) else {}
     eng = cls(shard, fabric.communicator(), max_occurrences=cap, reduce_chunk=chunk, transport=transport, **kw)
+    if prio and direct:
+        eng.set_eco_direct(direct & 1, cog=bool(direct & 2))
     s = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(s):
         for i in range(len(batches)):
@@ -85,7 +87,8 @@ def main():
     # produce the same table bit for bit
     sync_tr = "nccl" if "nccl" in sys.argv[2:] and not OVERSUB else "ce"
     t_sync, _ = run(False, dtype, batches, geom, rank, world, dev, chunk, transport=sync_tr)
-    t_prio, stats = run(True, dtype, batches, geom, rank, world, dev, chunk, presum)
+    direct = 3 if "direct" in sys.argv[2:] else 0
+    t_prio, stats = run(True, dtype, batches, geom, rank, world, dev, chunk, presum, direct=direct)
     ok = True
     if rank == 0:
         from oracle import Oracle
@@ -101,7 +104,8 @@ def main():
         ok_p = np.array_equal(t_prio.view(np.uint64), want_p.view(np.uint64))
         got_stats = np.array([[s.collision_rows, s.unique_next_rows, s.blocking_bytes] for s in stats], np.uint64)
         st_ok = np.array_equal(got_stats, want_stats)
-        print(f"[mp] world={world} dtype={dtype} chunk={chunk} presum={presum} sync transport={sync_tr}: "
+        print(f"[mp] world={world} dtype={dtype} chunk={chunk} presum={presum} direct={direct} "
+              f"sync transport={sync_tr}: "
               f"sync bit-exact vs oracle {ok_s}, "
               f"prio bit-exact vs oracle {ok_p}, stats equal {st_ok}")
         ok &= ok_s and ok_p and st_ok

@@ -17,11 +17,12 @@ def _ngpus():
 
 
 @pytest.mark.parametrize("dtype,flags", [("f64", []), ("f32", []), ("f32", ["presum"]), ("f64", ["nccl"]),
-                                         ("f32", ["presum", "nccl"])])
+                                         ("f32", ["presum", "nccl"]), ("f32", ["presum", "direct"])])
 def test_multiprocess_engine_parity(dtype, flags):
     """One process per GPU: the blocking engine (copy engines, or NCCL with
     "nccl") and the prioritized engine (PRESUM with "presum") bit-exact
-    against the oracle's model of the same numeric path."""
+    against the oracle's model of the same numeric path ("direct": the
+    collision chain's CO_G and E_co by direct NVLink stores)."""
     n = _ngpus()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")

@@ -6,6 +6,7 @@ Prints every rank's spans (phase, start, end, length; ms from the rank's
 first span) to gpurun_out/timeline_r<rank>.txt and a per-phase summary."""
 import argparse
 import os
+import time
 import sys
 
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
@@ -64,6 +65,7 @@ s = torch.cuda.Stream()
 d = [torch.from_numpy(b.view(np.int64)).to(dev) for b in batches]
 g = torch.full((cap, 256), 1e-3, device=dev)
 out = torch.empty((cap, 256), device=dev)
+hmarks = []
 with torch.cuda.stream(s):
     for i in range(cli.iters):
         if i == cli.profile_from:
@@ -73,16 +75,37 @@ with torch.cuda.stream(s):
             eng.set_profiling(True)
             eng.spans()
         n = batches[i].size
+        hmarks.append(("fwd>", i, time.monotonic_ns() * 1e-6))
         eng.forward(d[i], d[i + 1], out=out[:n], stream=s)
+        hmarks.append(("fwd<", i, time.monotonic_ns() * 1e-6))
         if victim:
             victim.run(blens[i])
+        hmarks.append(("bwd>", i, time.monotonic_ns() * 1e-6))
         eng.backward(g[:n], stream=s)
+        hmarks.append(("bwd<", i, time.monotonic_ns() * 1e-6))
 torch.cuda.synchronize()
-sp = eng.spans()
+tr = eng.trace()
+CH = ["ids", "rows", "grads", "ex", "mask", "cog", "exg", "cor", "idx", "grp", "ag"]
 os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+# host clock aligned so that the earliest span's issue == its GPU start
+# (the profiled window starts on an idle GPU, after a synchronize)
+first = min(tr, key=lambda x: x[3])
+h0 = first[5] - first[3]
 with open(os.path.join(ROOT, "gpurun_out", f"timeline_r{rank}.txt"), "w") as f:
-    for ph, a, b in sorted(sp, key=lambda x: x[1]):
-        f.write(f"{ph:10s} {a:8.3f} {b:8.3f} {b - a:7.3f}\n")
+    f.write("phase      lane ch     gpu_start  gpu_end    len   host_issue  gpu_start-host\n")
+    def chname(ch):
+        if ch < 0:
+            return "-"
+        if ch >= 1000:  # one copy of an all-to-all: channel, destination
+            return f"{CH[(ch - 1000) // 16]}>{(ch - 1000) % 16}"
+        return CH[ch]
+    rows = [(a, f"{ph:10s} {lane}    {chname(ch):6s} {a:8.3f} {b:8.3f} {b - a:7.3f}  {h - h0:8.3f}  {a - h + h0:8.3f}")
+            for ph, lane, ch, a, b, h in tr]
+    rows += [(t - h0, f"HOST {m} {i:3d}                                      {t - h0:8.3f}")
+             for m, i, t in hmarks if t - h0 >= -1.0]
+    for _, line in sorted(rows):
+        f.write(line + "\n")
+sp = [(ph, a, b) for ph, lane, ch, a, b, h in tr if ch < 1000]
 tot = {}
 for ph, a, b in sp:
     tot[ph] = tot.get(ph, 0.0) + (b - a)
