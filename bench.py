@@ -628,7 +628,7 @@ def main():
 
     W, K = max(args.warmup, 3), args.steps
     cfg5 = args.cfg5 if args.cfg5 >= 0 else int(world > 1)
-    iters = W + 3 * K + 4 + (2 * K + 4 if cfg5 else 0)
+    iters = W + 3 * K + 4 + (4 * K + 4 if cfg5 else 0)
     t_gen = time.time()
     batches, blens = batches_for(args, rank, world, iters, with_lens=True)
     ctx = E.Context(local, rank, world)
@@ -783,40 +783,48 @@ def main():
             vt1.record(stream)
             barrier()
             victim_alone = vt0.elapsed_time(vt1) / K
-            # (B) prioritized + copy engines, victim between forward and backward
-            eng.exposed_ms()
-            barrier()
-            e0.record(stream)
-            for i in range(it0, it0 + K):
-                n = batches[i].size
-                eng.forward(d_ids[i], d_ids[i + 1], out=out[:n], stream=stream)
-                victim.run(blens[i])
-                eng.backward(grads_full[:n], stream=stream)
-            e1.record(stream)
-            barrier()
-            res["prio_ce"] = (e0.elapsed_time(e1) / K, eng.exposed_ms() / K)
-            # (B') the same with the collision chain's transfers stored by its
-            # kernels straight into the peers' windows: the pre-sum into the
-            # owners' CO_G slots, the collision update into the requesters'
-            # E_co slots (SM-issued NVLink stores; no copy-engine hop)
-            if world > 1:
+            # dense synchronisation of a data-parallel step (the model's
+            # gradient all-reduce, 1 MiB here) after the victim, before the
+            # embedding backward — the synchronized variant of every arm:
+            # ranks leave the dense part together, so the exposed embedding
+            # time no longer carries the wait for the slowest rank's victim
+            dense = torch.zeros(1 << 18, dtype=torch.float32, device=dev)
+
+            def dense_sync():
+                if world > 1:
+                    dist.all_reduce(dense)
+
+            def prio_loop(first, sync):
                 eng.join(stream)
                 stream.synchronize()
-                eng.set_eco_direct(True, cog=True)
                 eng.exposed_ms()
                 barrier()
-                it1 = it0 + K
                 e0.record(stream)
-                for i in range(it1, it1 + K):
+                for i in range(first, first + K):
                     n = batches[i].size
                     eng.forward(d_ids[i], d_ids[i + 1], out=out[:n], stream=stream)
                     victim.run(blens[i])
+                    if sync:
+                        dense_sync()
                     eng.backward(grads_full[:n], stream=stream)
                 eng.join(stream)
                 e1.record(stream)
                 barrier()
-                res["prio_direct"] = (e0.elapsed_time(e1) / K, eng.exposed_ms() / K)
+                return e0.elapsed_time(e1) / K, eng.exposed_ms() / K
+
+            # (B) prioritized + copy engines, victim between forward and backward
+            res["prio_ce"] = prio_loop(it0, False)
+            if world > 1:
+                # (B') the same with the collision chain's transfers stored by
+                # its kernels straight into the peers' windows: the pre-sum
+                # into the owners' CO_G slots, the collision update into the
+                # requesters' E_co slots (SM-issued NVLink stores, no copy-engine
+                # hop); then both prioritized arms with the dense sync
+                eng.set_eco_direct(True, cog=True)
+                res["prio_direct"] = prio_loop(it0 + K, False)
+                res["prio_direct_sync"] = prio_loop(it0 + 2 * K, True)
                 eng.set_eco_direct(False)
+                res["prio_ce_sync"] = prio_loop(it0 + 3 * K, True)
         # (A) the blocking baseline: synchronized engine, NCCL all-to-all (N>1)
         base_tr = "nccl" if world > 1 else "ce"
         sync_eng = E.SynchronizedEmbedding(shard, comm, max_occurrences=cap,
@@ -827,17 +835,25 @@ def main():
                 sync_eng.forward(d_ids[i], out=out[:n], stream=stream)
                 victim.run(blens[i])
                 sync_eng.backward(grads_full[:n], stream=stream)
-            barrier()
-            sync_eng.exposed_ms()
-            e0.record(stream)
-            for i in range(it0, it0 + K):
-                n = batches[i].size
-                sync_eng.forward(d_ids[i], out=out[:n], stream=stream)
-                victim.run(blens[i])
-                sync_eng.backward(grads_full[:n], stream=stream)
-            e1.record(stream)
-            barrier()
-            res["sync_" + base_tr] = (e0.elapsed_time(e1) / K, sync_eng.exposed_ms() / K)
+
+            def base_loop(sync):
+                barrier()
+                sync_eng.exposed_ms()
+                e0.record(stream)
+                for i in range(it0, it0 + K):
+                    n = batches[i].size
+                    sync_eng.forward(d_ids[i], out=out[:n], stream=stream)
+                    victim.run(blens[i])
+                    if sync:
+                        dense_sync()
+                    sync_eng.backward(grads_full[:n], stream=stream)
+                e1.record(stream)
+                barrier()
+                return e0.elapsed_time(e1) / K, sync_eng.exposed_ms() / K
+
+            res["sync_" + base_tr] = base_loop(False)
+            if world > 1:
+                res["sync_" + base_tr + "_sync"] = base_loop(True)
         sync_eng.close()
         cont = None
         if world > 1:
@@ -862,6 +878,21 @@ def main():
             exp_d_ns = max_over_ranks(max(0.0, res["prio_direct"][1] - skew))
         exp_b_sum = sum_over_ranks(res[b_key][1])
         exp_p_sum = sum_over_ranks(res["prio_ce"][1])
+        sync_out = None
+        if world > 1:
+            # every arm with the dense all-reduce between the victim and the
+            # embedding backward: exposed embedding time from a synchronized start
+            sb = max_over_ranks(res[b_key + "_sync"][1])
+            sync_out = {"dense_sync": "1 MiB NCCL all-reduce after the victim, before the embedding backward "
+                                      "(not counted as embedding exposed time), in every arm",
+                        "exposed_ms_per_iter_max_over_ranks": {b_key: round(sb, 4)},
+                        "exposed_reduction_pct": {},
+                        "step_ms": {b_key: round(max_over_ranks(res[b_key + "_sync"][0]), 4)}}
+            for k in ("prio_ce_sync", "prio_direct_sync"):
+                x = max_over_ranks(res[k][1])
+                sync_out["exposed_ms_per_iter_max_over_ranks"][k] = round(x, 4)
+                sync_out["exposed_reduction_pct"][k] = round(100.0 * (1 - x / sb), 2) if sb > 0 else None
+                sync_out["step_ms"][k] = round(max_over_ranks(res[k][0]), 4)
         cfg5_out = {
             "load_balancer": ("FBS (partition.cpp:157-176) over the global batch of each iteration, on the GPU"
                               if world > 1 else "none (1 rank)"),
@@ -897,6 +928,7 @@ def main():
             # (FSX_ECO_DIRECT is off: no kernel stores to a peer window)
             "comm_sms": {b_key: "NCCL kernels (SM-resident)" if base_tr == "nccl" else 0, "prio_ce": 0},
             "contention": cont,
+            "synchronized_step": sync_out,
             "notes": ("the NCCL baseline's ids all-to-all needs host-known counts: its 8-byte size round "
                       "(comm.cpp:328-341) is followed by one stream sync, inside the baseline's exposed window"),
         }

@@ -139,7 +139,7 @@ __global__ void k_collide_count(const uint64_t* __restrict__ a, const uint64_t* 
                                 const uint64_t* __restrict__ b, const uint64_t* d_nb,
                                 const uint32_t* __restrict__ seg_a, uint8_t* __restrict__ flag_a,
                                 uint8_t* __restrict__ flag_b, uint32_t* __restrict__ partner_a,
-                                unsigned long long* misc) { FSX_PDL_ENTER();
+                                unsigned long long* misc, uint32_t* __restrict__ co_rows) { FSX_PDL_ENTER();
   const uint64_t na = *d_na, nb = *d_nb;
   const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
   const uint64_t n_round = (na + 31) & ~uint64_t{31};
@@ -163,10 +163,15 @@ __global__ void k_collide_count(const uint64_t* __restrict__ a, const uint64_t* 
     }
     const unsigned ballot = __ballot_sync(0xffffffffu, hit);
     for (int o = 16; o > 0; o >>= 1) occ += __shfl_xor_sync(0xffffffffu, occ, o);
+    unsigned long long base = 0;
     if ((threadIdx.x & 31u) == 0 && ballot) {
-      atomicAdd(misc, static_cast<unsigned long long>(__popc(ballot)));
+      base = atomicAdd(misc, static_cast<unsigned long long>(__popc(ballot)));
       atomicAdd(misc + 1, occ);
     }
+    // the collision rows as a list (warp-aggregated append; the collision
+    // update's rows are independent, so their order is immaterial)
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (hit) co_rows[base + __popc(ballot & ((1u << (threadIdx.x & 31u)) - 1u))] = static_cast<uint32_t>(i);
   }
 }
 
@@ -329,6 +334,7 @@ struct OwnBatch {  // owner view: occurrences received for this shard
   DevBuf<uint32_t> rank_us;  // [unique row][kMaxRanks] position in each source's message
   DevBuf<uint32_t> slot_us;  // PRESUM: [unique row][kMaxRanks] slot in the GRP message
   DevBuf<uint32_t> partner;  // collision row -> its row in the next owner batch
+  DevBuf<uint32_t> co_rows;  // the collision rows (any order; count misc[0])
   SortedIds srt;
   ScanScratch scan;
   SgdScratch plan;               // one rank: the update's work lists, built on L
@@ -345,6 +351,7 @@ struct OwnBatch {  // owner view: occurrences received for this shard
     rank_us.alloc(cap * kMaxRanks);
     slot_us.alloc(cap * kMaxRanks);
     partner.alloc(cap);
+    co_rows.alloc(cap);
     srt.reserve(cap);
   }
   uint64_t* pack_tot() { return misc.p + 8; }
@@ -1086,7 +1093,7 @@ struct Engine {
     FSX_CUDA(cudaMemsetAsync(oc.misc.p, 0, 16, s));
     FSX_LAUNCH(ctx, k_collide_count, grid_for(ctx, oc.m_cap, 256, 8), 256, 0, s, oc.srt.uniq_g.p,
                oc.srt.d_u(), on.srt.uniq_g.p, on.srt.d_u(), oc.srt.seg_start.p, oc.co.p, on.co.p, oc.partner.p,
-               reinterpret_cast<unsigned long long*>(oc.misc.p));
+               reinterpret_cast<unsigned long long*>(oc.misc.p), oc.co_rows.p);
     oc.has_co = true;
     on.has_co = false;
   }
@@ -1322,7 +1329,7 @@ struct Engine {
     const bool v16 = rb % 16 == 0;
 #define FSX_CO_APPLY_P(T, VE, P)                                                                     \
   FSX_LAUNCH(ctx, (k_co_apply<T, VE, P>), grid, 128, 0, s, static_cast<T*>(t->values), t->g, t->lr,   \
-             oc.srt.uniq.p, oc.srt.d_u(), oc.co.p, oc.bits.p, oc.slot_us.p, cog, p, eco, ctx->d_err)
+             oc.srt.uniq.p, oc.misc.p, oc.co_rows.p, oc.bits.p, oc.slot_us.p, cog, p, eco, ctx->d_err)
 #define FSX_CO_APPLY(T, VE)                                    \
   do {                                                         \
     if (p <= 2) FSX_CO_APPLY_P(T, VE, 2);                      \

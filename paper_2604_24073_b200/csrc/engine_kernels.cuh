@@ -555,18 +555,18 @@ struct EcoOut {
 template <class T, int VE, int P>  // P >= p: per-source registers
 __global__ void __launch_bounds__(128) k_co_apply(T* __restrict__ table, ShardGeom g, double lr,
                                                    const uint64_t* __restrict__ uniq_local,
-                                                   const uint64_t* d_u, const uint8_t* __restrict__ co,
+                                                   const uint64_t* d_nco, const uint32_t* __restrict__ co_rows,
                                                    const uint32_t* __restrict__ bits,
                                                    const uint32_t* __restrict__ slot_us, CSlots cog,
                                                    int p, EcoOut eco, DevErr* err) { FSX_PDL_ENTER();
   using V = VecOf<T, VE>;
-  const uint64_t U = *d_u;
+  const uint64_t n_co = *d_nco;  // collision rows (k_collide_count's list)
   const uint64_t warps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
   const uint64_t wid = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const unsigned lane = threadIdx.x & 31u;
   const uint32_t rb = g.dim * sizeof(T);
-  for (uint64_t u = wid; u < U; u += warps) {
-    if (!co[u]) continue;
+  for (uint64_t k = wid; k < n_co; k += warps) {
+    const uint64_t u = co_rows[k];
     const uint32_t b = bits[u];
     const uint64_t l = uniq_local[u];
     if (l >= g.local_rows) continue;
