@@ -244,7 +244,7 @@ int fsx_engine_set_eco_direct(fsx_engine* e, int on);
  * relative to the earliest span; consumes them (synchronizes) */
 int fsx_engine_spans(fsx_engine* e, double* out, uint64_t max_spans, uint64_t* n_spans);
 /* the same spans with their lane and host issue time: out[6k..6k+5] =
- * (phase, lane (0 caller, 1 L, 2 H, 3 X, 4 top-priority, 5 a copy stream),
+ * (phase, lane (0 caller, 1 L, 2 H, 3 X, 4 top-priority, 5 a copy stream, 6 L2),
  * all-to-all channel (one copy: 1000 + 16 * channel + destination) or -1, GPU start ms, GPU end ms relative to the earliest span, host issue
  * time in CLOCK_MONOTONIC ms); consumes them */
 int fsx_engine_trace(fsx_engine* e, double* out, uint64_t max_spans, uint64_t* n_spans);

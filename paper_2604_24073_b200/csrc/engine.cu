@@ -528,6 +528,14 @@ struct Engine {
   }
   uint32_t seq[NCH] = {};
   cudaStream_t lo = nullptr, hi = nullptr, ux = nullptr;  // ux: deferred exclusive updates
+  // lo2: the side lane's part 2 (pack lists, E_ex prefetch, IDX) on its own
+  // stream, forked from L after the collision: the next iteration's part 1
+  // (route, ids all-to-all, dedup) then overlaps it instead of queueing
+  // behind its transfers. FSX_SPLIT_LANE=0: part 2 back on L (A/B).
+  cudaStream_t lo2 = nullptr;
+  bool split_lane = true;
+  cudaStream_t l2() const { return split_lane && lo2 ? lo2 : lo; }
+  cudaEvent_t ev_collided = nullptr;  // L: after the collision of (i, i+1)
   // us: the caller's-stream row movers re-issued at the highest priority
   // (FSX_C_PRIO: 1 = the one-rank update, 2 = + the merge), so the side lane
   // (mid priority) does not take the SMs those kernels' CTAs wait for
@@ -545,14 +553,16 @@ struct Engine {
   // per-(lane, peer) copy streams: a lane's copies never queue behind another
   // lane's (the collision chain must not wait for prefetch or deferred
   // traffic issued earlier on the same peer)
-  static constexpr int kLanes = 4;  // L, H, ux, caller
+  static constexpr int kLanes = 5;  // L, H, ux, caller, L2
   cudaStream_t cstream[kLanes][kMaxRanks] = {};
   // copy-stream set of a lane: the prioritized engine's caller stream runs no
   // all-to-all of its own (raw fsx_a2a_ce / all-gather calls borrow H's set),
   // the blocking engine uses only the caller's — fewer streams keep every
   // used stream on its own hardware queue at 8 ranks (CUDA_DEVICE_MAX_CONNECTIONS)
-  int lane_map[kLanes] = {0, 1, 2, 3};
-  int lane_of(cudaStream_t s) const { return lane_map[s == lo ? 0 : s == hi ? 1 : s == ux ? 2 : 3]; }
+  int lane_map[kLanes] = {0, 1, 2, 3, 4};
+  int lane_of(cudaStream_t s) const {
+    return lane_map[s == lo ? 0 : s == hi ? 1 : s == ux ? 2 : (lo2 && s == lo2) ? 4 : 3];
+  }
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_next = 0;
   // exposed-wait timing on the compute stream
@@ -586,6 +596,7 @@ struct Engine {
     if (s == hi) return 2;
     if (s == ux) return 3;
     if (us && s == us) return 4;
+    if (lo2 && s == lo2) return 6;
     for (int l = 0; l < kLanes; ++l)
       for (int d = 0; d < p; ++d)
         if (cstream[l][d] && s == cstream[l][d]) return 5;
@@ -1499,15 +1510,21 @@ struct Engine {
     auto prep1 = [this, i, bootstrap, with_next, n_next]() {
       ReqBatch& rc2 = R(i);
       OwnBatch& oc2 = O(i);
+      // part 2 of the previous prep (on L2) still reads O(i) (its collision
+      // flags and scan scratch), which the collision / masks below rewrite
+      const cudaEvent_t prev2 = split_lane ? ev_next_ready : nullptr;
       if (with_next) {
         ReqBatch& rn = R(i + 1);
         OwnBatch& on = O(i + 1);
         const int par = route(rn, rn.ids.p, n_next, lo, false);
         receive(on, par, lo, false);
         rn.cor_par = -1;
+        wait(lo, prev2);
         collide(oc2, on, lo);
+        ev_collided = record(lo);
         if (!bootstrap) masks_and_split(oc2, rc2, true, lo);
       } else {
+        wait(lo, prev2);
         oc2.has_co = false;
         if (!bootstrap) masks_and_split(oc2, rc2, false, lo);
       }
@@ -1520,16 +1537,20 @@ struct Engine {
       // the deferred exclusive update of i-1 after the masks: it has a whole
       // iteration of slack and would only slow the chain the backward waits on
       apply_deferred(dfr);
-      if (with_next) prefetch_pack(O(i + 1), lo);
-      else ev_pack = nullptr;
+      if (with_next) {
+        if (l2() != lo) wait(l2(), ev_collided);
+        prefetch_pack(O(i + 1), l2());
+      } else {
+        ev_pack = nullptr;
+      }
     };
     auto prep2 = [this, i, with_next]() {
       if (with_next) {
         ReqBatch& rn = R(i + 1);
         OwnBatch& on = O(i + 1);
-        prefetch(on, rn, lo);
-        if (self_plan()) plan_self(on, lo);
-        ev_next_ready = record(lo);
+        prefetch(on, rn, l2());
+        if (self_plan()) plan_self(on, l2());
+        ev_next_ready = record(l2());
         rn_ex_ready = ev_next_ready;
       } else {
         ev_next_ready = nullptr;
@@ -1736,7 +1757,7 @@ struct Engine {
   // only when the engine is idle
   void join(cudaStream_t c) {
     if (side) side->drain();
-    for (cudaStream_t s : {lo, hi, ux, us})
+    for (cudaStream_t s : {lo, hi, ux, us, lo2})
       if (s) wait(c, record(s));
     for (int l = 0; l < kLanes; ++l)
       for (int d = 0; d < p; ++d)
@@ -1747,6 +1768,7 @@ struct Engine {
     if (side) side->drain();
     apply_deferred(take_deferred());
     wait(c, record(lo));
+    if (lo2) wait(c, record(lo2));
     wait(c, record(hi));
     wait(c, record(ux));
   }
@@ -1800,6 +1822,7 @@ struct Engine {
     for (auto e : timing_pool) cudaEventDestroy(e);
     for (auto e : prof_pool) cudaEventDestroy(e);
     if (lo) cudaStreamDestroy(lo);
+    if (lo2) cudaStreamDestroy(lo2);
     if (hi) cudaStreamDestroy(hi);
     if (ux) cudaStreamDestroy(ux);
     if (us) cudaStreamDestroy(us);
@@ -1890,6 +1913,10 @@ int fsx_engine_create(fsx_ctx* ctx, fsx_table* table, const fsx_engine_config* c
   FSX_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
   const int mid = greatest < least ? greatest + 1 : greatest;
   FSX_CUDA(cudaStreamCreateWithPriority(&e->lo, cudaStreamNonBlocking, mid));
+  // (one rank: no transfers in part 2, measured neutral — kept on L)
+  e->split_lane = e->p > 1;
+  if (const char* v = std::getenv("FSX_SPLIT_LANE")) e->split_lane = std::atoi(v) != 0;
+  if (prio && e->split_lane) FSX_CUDA(cudaStreamCreateWithPriority(&e->lo2, cudaStreamNonBlocking, mid));
   FSX_CUDA(cudaStreamCreateWithPriority(&e->hi, cudaStreamNonBlocking, greatest));
   FSX_CUDA(cudaStreamCreateWithPriority(&e->ux, cudaStreamNonBlocking, least));
   FSX_CUDA(cudaStreamCreateWithPriority(&e->us, cudaStreamNonBlocking, greatest));
@@ -1898,6 +1925,7 @@ int fsx_engine_create(fsx_ctx* ctx, fsx_table* table, const fsx_engine_config* c
   // one copy stream per peer: outgoing copies of an all-to-all run on
   // several copy engines at once instead of queueing on one
   for (int l = 0; l < Engine::kLanes; ++l) e->lane_map[l] = prio ? (l == 3 ? 1 : l) : 3;
+  if (!e->lo2) e->lane_map[4] = e->lane_map[0];
   for (int l = 0; l < Engine::kLanes; ++l) {
     if (prio ? l == 3 : l != 3) continue;
     for (int d = 0; d < e->p; ++d)

@@ -352,11 +352,12 @@ class _Engine:
     def trace(self, max_spans: int = 100000):
         """[(phase, lane, channel, gpu_start_ms, gpu_end_ms, host_issue_ms)] of every
         recorded span (synchronizes; consumes them). Lanes: C L H X S, K = a copy
-        stream (its channel = 1000 + 16 * all-to-all channel + destination)."""
+        stream (its channel = 1000 + 16 * all-to-all channel + destination),
+        M = the side lane's part 2 (L2)."""
         buf = np.zeros(6 * max_spans, np.float64)
         n = C.c_uint64()
         _lib.call("fsx_engine_trace", self.h, buf.ctypes.data, max_spans, C.byref(n))
-        return [(_lib.PHASES[int(buf[6 * k])], "CLHXSK"[int(buf[6 * k + 1])], int(buf[6 * k + 2]),
+        return [(_lib.PHASES[int(buf[6 * k])], "CLHXSKM"[int(buf[6 * k + 1])], int(buf[6 * k + 2]),
                  buf[6 * k + 3], buf[6 * k + 4], buf[6 * k + 5]) for k in range(n.value)]
 
     def exposed_ms(self) -> float:
