@@ -739,15 +739,18 @@ def main():
         # not inside the timed region above
         prof_lo = W + K
         phases = {}
+        span_us = span_n = None
         if args.profile_phases and hasattr(eng, "set_profiling"):
             eng.set_profiling(True)
             eng.phase_ms()  # reset
+            ctx.kernel_span(True)  # the row-update kernel's own device-side span
         for i in range(prof_lo, prof_lo + K):
             step(i)
         barrier()
         if args.profile_phases and hasattr(eng, "set_profiling"):
             phases = eng.phase_ms()
             eng.set_profiling(False)
+            span_us, span_n = ctx.kernel_span(False)
         eng.exposed_ms()
         # end-to-end: host ids -> device each step, stats read back (two
         # untimed steps first: the switch from resident to host ids)
@@ -997,6 +1000,12 @@ def main():
                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                     "peak_source": peak_src, "launch_ms": round(per_launch_ms, 4),
                     "algorithmic_bytes_per_launch": int(per_launch_bytes)}
+            if name == "co_update" and world == 1 and span_n == spans and span_us:
+                # the same launches timed by the kernel itself (first CTA start
+                # -> last CTA end, device globaltimer): the event window above
+                # also holds the wait for SMs the concurrent side lane occupies
+                roof["kernel_span_us"] = round(span_us, 2)
+                roof["kernel_span_frac"] = round(per_launch_bytes / (span_us * 1e-6) / 1e9 / peak, 4)
 
     cfg1_out = cfg2_out = cfg3_out = None
     if rank == 0 and world == 1 and (args.cfg1 if args.cfg1 >= 0 else 1):

@@ -70,6 +70,11 @@ int fsx_ctx_destroy(fsx_ctx* ctx);
 int fsx_ctx_sync(fsx_ctx* ctx);
 /* number of kernels this context has launched (for bench gpu_launches) */
 uint64_t fsx_ctx_launches(const fsx_ctx* ctx);
+/* The row-update kernel's own span (first CTA start -> last CTA end, device
+ * globaltimer) per launch, recorded without host synchronisation while on:
+ * returns the mean (us) and count of the launches since the last call, then
+ * switches recording on / off (measurement only; synchronizes when reading). */
+int fsx_ctx_kernel_span(fsx_ctx* ctx, int on, double* mean_us, uint64_t* n);
 
 /* ---- primitives (hot-path kernels, exposed for parity tests) -------------- */
 

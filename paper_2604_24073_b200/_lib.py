@@ -49,6 +49,7 @@ _SIGS = {
     "fsx_ctx_destroy": ([vp], i32),
     "fsx_ctx_sync": ([vp], i32),
     "fsx_ctx_launches": ([vp], u64),
+    "fsx_ctx_kernel_span": ([vp, i32, P(C.c_double), P(u64)], i32),
     "fsx_sort_unique_u64": ([vp, vp, u64, vp, vp, P(u64), vp], i32),
     "fsx_collision_split": ([vp, vp, u64, vp, u64, vp, vp, vp, P(u64), vp], i32),
     "fsx_route_by_owner": ([vp, vp, u64, u64, i32, vp, vp, P(u64), vp], i32),

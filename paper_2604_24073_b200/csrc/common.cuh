@@ -108,7 +108,11 @@ struct Ctx {
   bool sgd_stream = true;
   unsigned stream_per_sm = 8;
   unsigned stream_variant = 0;
-  unsigned long long stream_span_ns = 0, stream_span_n = 0;  // FSX_STREAM_SPAN (debug)  // FSX_STREAM_VARIANT (tuning): ring depth / CTAs per SM
+  // k_sgd_stream's own span per launch (fsx_ctx_kernel_span): device ring
+  static constexpr uint64_t kSpanSlots = 4096;
+  unsigned long long* d_span = nullptr;
+  uint64_t span_next = 0;
+  bool span_on = false;  // FSX_STREAM_VARIANT (tuning): ring depth / CTAs per SM
   unsigned warp_variant = 0;  // FSX_WARP_VARIANT (tuning): k_sgd_warp unroll / min CTAs per SM
   bool pdl = true;       // programmatic dependent launches (FSX_PDL=0: plain launches)
   bool onesweep = true;  // decoupled look-back radix passes (FSX_ONESWEEP=0: 3 launches per pass)

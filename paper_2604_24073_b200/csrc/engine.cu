@@ -483,6 +483,7 @@ struct Engine {
   Ctx* ctx = nullptr;
   bool host_prof = std::getenv("FSX_HOST_PROF") != nullptr;
   bool trace_copies = std::getenv("FSX_TRACE_COPIES") != nullptr;
+  bool ce_fork = std::getenv("FSX_CE_FORK") == nullptr || std::atoi(std::getenv("FSX_CE_FORK")) != 0;
   std::atomic<uint64_t> hp_ns[HP_N] = {};
   std::atomic<uint64_t> hp_calls[HP_N] = {};
   struct HostTimer {
@@ -795,15 +796,19 @@ struct Engine {
       std::fprintf(stderr, "[fsx r%d] a2a ch=%d seq=%u par=%d stream=%s\n", me, ch, v, par,
                    s == lo ? "L" : s == hi ? "H" : "C");
     Span sp(this, FSX_PHASE_A2A, s, ch);
-    // fork: each peer's copy + flag on its own copy stream (parallel copy
-    // engines), join back into `s` below
-    cudaEvent_t fork = record(s);
+    // Each peer's copy + flag on its own copy stream, joined back into `s`.
+    // A GPU's copy engine runs one peer copy at a time anyway (measured: the
+    // p-1 copies of an all-to-all serialise even on separate streams), but
+    // the fork keeps `s` free for work that does not need the copies.
+    // FSX_CE_FORK=0: the copies straight on `s` (3 host calls per peer fewer;
+    // A/B at N=2/4 within run-to-run spread: profiles/r2_split_lane_ab.txt).
+    cudaEvent_t fork = ce_fork ? record(s) : nullptr;
     for (int k = 1; k < p; ++k) {
       const int d = (me + k) % p;  // stagger destinations across the NVSwitch
       const PeerView& pv = peer[d];
       if (!pv.base) raise(FSX_ERR_COLLECTIVE, "all_to_all: peer " + std::to_string(d) + " not connected");
-      cudaStream_t cs = cstream[lane_of(s)][d];
-      wait(cs, fork);
+      cudaStream_t cs = ce_fork ? cstream[lane_of(s)][d] : s;
+      if (ce_fork) wait(cs, fork);
       char* dst = pv.base + ch_off[ch] + (static_cast<size_t>(par) * p + me) * ch_slot[ch];
       {
         // FSX_TRACE_COPIES: a span per copy for fsx_engine_trace (not in the phase sums)
@@ -822,7 +827,7 @@ struct Engine {
       }
       // the sender's staging slot is reused two uses later: `s` must not run
       // ahead of this copy
-      wait(s, record(cs));
+      if (ce_fork) wait(s, record(cs));
     }
     for (int k = 1; k < p; ++k) {
       const int src = (me + p - k) % p;
@@ -1155,18 +1160,19 @@ struct Engine {
       Span sp2(this, FSX_PHASE_PREFETCH, s);
       launch_copy_rows(ctx, pm, on.m_cap * static_cast<uint64_t>(p), on.misc.p + 2, rb, s);
     }
+    // IDX: per-occurrence row positions for the next merge, packed before
+    // the E_ex copies are queued on this stream (the copies run in its order)
+    const int ipar = next_par(CH_IDX);
+    Slots isend = send_slots(CH_IDX, ipar);
+    FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, isend, p, on.cnt.p + 2, 1, cap, ctx->d_err);
+    FSX_LAUNCH(ctx, k_idx_pack, grid_for(ctx, on.m_cap, 256, 8), 256, 0, s, on.srt.inverse.p, on.occ_src.p,
+               on.occ_idx.p, on.srt.d_n(), on.rank_us.p, on.co.p, isend, me);
     {
       std::vector<uint64_t> bytes(p);
       for (int d = 0; d < p; ++d) bytes[d] = idrows_rows_off(on.h_pack[2 * d]) + rb * on.h_pack[2 * d];
       a2a(CH_EX, par, bytes, s);
     }
     rn.ex_par = par;
-    // IDX: per-occurrence row positions for the next merge
-    const int ipar = next_par(CH_IDX);
-    Slots isend = send_slots(CH_IDX, ipar);
-    FSX_LAUNCH(ctx, k_write_headers, 1, 32, 0, s, isend, p, on.cnt.p + 2, 1, cap, ctx->d_err);
-    FSX_LAUNCH(ctx, k_idx_pack, grid_for(ctx, on.m_cap, 256, 8), 256, 0, s, on.srt.inverse.p, on.occ_src.p,
-               on.occ_idx.p, on.srt.d_n(), on.rank_us.p, on.co.p, isend, me);
     a2a(CH_IDX, ipar, occ_msg_bytes(on, 4), s);
     rn.idx_par = ipar;
   }

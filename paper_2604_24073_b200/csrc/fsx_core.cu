@@ -183,9 +183,7 @@ int fsx_ctx_destroy(fsx_ctx* ctx) {
   FSX_API_BEGIN
   if (!ctx) return FSX_OK;
   DeviceGuard dg(ctx->device);
-  if (ctx->stream_span_n)
-    std::fprintf(stderr, "[fsx] k_sgd_stream: %llu launches, mean span %.1f us\n", ctx->stream_span_n,
-                 1e-3 * static_cast<double>(ctx->stream_span_ns) / static_cast<double>(ctx->stream_span_n));
+  if (ctx->d_span) cudaFree(ctx->d_span);
   cudaFree(ctx->d_err);
   cudaFreeHost(ctx->h_err);
   delete ctx;
@@ -201,6 +199,35 @@ int fsx_ctx_sync(fsx_ctx* ctx) {
 }
 
 uint64_t fsx_ctx_launches(const fsx_ctx* ctx) { return ctx ? ctx->launches.load() : 0; }
+
+int fsx_ctx_kernel_span(fsx_ctx* ctx, int on, double* mean_us, uint64_t* n) {
+  FSX_API_BEGIN
+  DeviceGuard dg(ctx->device);
+  double tot = 0;
+  uint64_t k = 0;
+  if (ctx->span_on && ctx->span_next) {
+    // every launch of the window has run: read the slots
+    FSX_CUDA(cudaDeviceSynchronize());
+    std::vector<unsigned long long> h(2 * ctx->span_next);
+    FSX_CUDA(cudaMemcpy(h.data(), ctx->d_span, h.size() * 8, cudaMemcpyDeviceToHost));
+    for (uint64_t j = 0; j < ctx->span_next; ++j) {
+      const unsigned long long a = ~h[2 * j], b = h[2 * j + 1];
+      if (h[2 * j] && b > a) {
+        tot += 1e-3 * static_cast<double>(b - a);
+        ++k;
+      }
+    }
+  }
+  if (mean_us) *mean_us = k ? tot / static_cast<double>(k) : 0.0;
+  if (n) *n = k;
+  ctx->span_on = on != 0;
+  ctx->span_next = 0;
+  if (ctx->span_on) {
+    if (!ctx->d_span) FSX_CUDA(cudaMalloc(&ctx->d_span, 2 * 8 * fsx::Ctx::kSpanSlots));
+    FSX_CUDA(cudaMemset(ctx->d_span, 0, 2 * 8 * fsx::Ctx::kSpanSlots));
+  }
+  FSX_API_END
+}
 
 int fsx_sort_unique_u64(fsx_ctx* ctx, const uint64_t* d_keys, uint64_t n, uint64_t* d_unique,
                         uint32_t* d_inverse, uint64_t* h_num_unique, void* stream) {

@@ -131,8 +131,8 @@ template <class T, int NV, int R, int MINB, bool kBulk, bool kFused>
 __global__ void __launch_bounds__(128, MINB) k_sgd_stream(SgdArgs<T> a, uint32_t rb, uint32_t* __restrict__ done,
                                                          unsigned long long* span) {
   FSX_PDL_ENTER();
-  // span (debug, FSX_STREAM_SPAN): [0] first warp start, [1] last warp end (ns)
-  if (span && (threadIdx.x & 31u) == 0) atomicMin(span, global_ns());
+  // span (fsx_ctx_kernel_span): [0] ~first warp start, [1] last warp end (ns)
+  if (span && (threadIdx.x & 31u) == 0) atomicMax(span, ~global_ns());
   constexpr int VE = static_cast<int>(16 / sizeof(T));
   using V = VecOf<T, VE>;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(128, MINB) k_sgd_stream(SgdArgs<T> a, uint32_t
   // slot k: shared address slot0 + k * rb; lane l reads 16-byte vectors
   // l, l + 32, ... of the row (conflict-free)
   auto take = [&](V (&g)[NV]) {
-    const uint32_t slot = consumed & (R - 1);
+    const uint32_t slot = consumed % R;
     mbar_wait(bar0 + 8 * slot, (consumed / R) & 1u);
     const uint32_t addr = slot0 + slot * rb + lane * 16u;
 #pragma unroll

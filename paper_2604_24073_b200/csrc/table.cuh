@@ -139,28 +139,13 @@ void launch_sgd_stream(Ctx* ctx, const SgdArgs<T>& a, uint32_t rb, uint32_t* don
     per_sm = it->second;
   }
   per_sm = std::min<int>(per_sm, static_cast<int>(ctx->stream_per_sm));
-  // FSX_STREAM_SPAN=1 (debug): the kernel's own first-start / last-end
-  // global times per launch, summed into ctx->stream_span_ns
-  static unsigned long long* span = nullptr;  // device: [0] min start, [1] max end
-  static const bool want_span = std::getenv("FSX_STREAM_SPAN") != nullptr;
-  if (want_span && ctx->device == 0) {  // (debug span: device 0 only)
-    const unsigned long long init[2] = {~0ull, 0ull};
-    if (!span) {
-      FSX_CUDA(cudaMalloc(&span, sizeof(init)));
-    } else {
-      unsigned long long h[2];
-      FSX_CUDA(cudaMemcpyAsync(h, span, sizeof(h), cudaMemcpyDeviceToHost, stream));
-      FSX_CUDA(cudaStreamSynchronize(stream));
-      if (h[1] > h[0] && h[0] != ~0ull) {
-        ctx->stream_span_ns += h[1] - h[0];
-        ++ctx->stream_span_n;
-      }
-    }
-    FSX_CUDA(cudaMemcpyAsync(span, init, sizeof(init), cudaMemcpyHostToDevice, stream));
-    FSX_CUDA(cudaStreamSynchronize(stream));
-  }
+  // kernel span (fsx_ctx_kernel_span): each launch gets a slot of the
+  // context's ring; the kernel stores ~first start and last end (globaltimer
+  // ns) with atomicMax, so a zeroed slot needs no per-launch initialisation
+  unsigned long long* span = nullptr;
+  if (ctx->span_on && ctx->span_next < Ctx::kSpanSlots) span = ctx->d_span + 2 * ctx->span_next++;
   FSX_LAUNCH(ctx, (k_sgd_stream<T, NV, R, MINB, kBulk, kFused>), static_cast<unsigned>(ctx->num_sms * per_sm), kWarps * 32, smem,
-             stream, a, rb, done, ctx->device == 0 ? span : nullptr);
+             stream, a, rb, done, span);
 }
 
 template <class T>
@@ -192,7 +177,8 @@ void sgd_apply(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_cap, uin
     // SM for the side lane's latency-bound kernels (route / dedup / collide
     // of the next iteration), which the update otherwise starves.
     // FSX_STREAM_VARIANT (tuning): 1 = 8-row rings at 5 CTAs per SM,
-    // 2 = separate k_sgd_combine, 3 = LDGSTS instead of bulk copies.
+    // 2 = separate k_sgd_combine, 3 = LDGSTS instead of bulk copies,
+    // 4 = 12-row rings at 4 CTAs per SM.
     const unsigned var = ctx->stream_variant;
     const bool fused = var != 2;
     uint32_t* done = s.done.p;
@@ -202,6 +188,8 @@ void sgd_apply(Ctx* ctx, Table& t, const RowSegments& rs, uint64_t rows_cap, uin
       launch_sgd_stream<T, 2, 8, 5, true, true>(ctx, a, rb, done, stream);
     else if (vpl == 2 && var == 2)
       launch_sgd_stream<T, 2, 16, 3, true, false>(ctx, a, rb, done, stream);
+    else if (vpl == 2 && var == 4)
+      launch_sgd_stream<T, 2, 12, 4, true, true>(ctx, a, rb, done, stream);
     else if (vpl == 2 && var == 3)
       launch_sgd_stream<T, 2, 16, 3, false, true>(ctx, a, rb, done, stream);
     else if (vpl == 2)

@@ -78,6 +78,13 @@ class Context:
     def launches(self) -> int:
         return int(_lib.lib().fsx_ctx_launches(self.h))
 
+    def kernel_span(self, on: bool) -> tuple[float, int]:
+        """Mean own span (us) and count of the row-update kernel's launches
+        since the last call, then switch recording on / off (measurement)."""
+        m, n = C.c_double(), C.c_uint64()
+        _lib.call("fsx_ctx_kernel_span", self.h, int(on), C.byref(m), C.byref(n))
+        return m.value, n.value
+
     def close(self) -> None:
         if self.h:
             _lib.lib().fsx_ctx_destroy(self.h)

@@ -21,7 +21,7 @@ def test_reference_cases_through_cpp_dropin(cuda):
     assert "0 failed" in r.stdout
 
 
-# The reference's own unit suites (tests/test_{comm,partition,jagged}.cpp),
+# The reference's own unit suites (tests/test_{comm,partition,jagged,embedding}.cpp),
 # compiled unchanged against the drop-in headers by cpp/Makefile in the
 # container that has /root/reference (the binaries travel to the GPU box).
 # Excluded: the reference simulator's logical-clock cost model and its TCP
@@ -30,6 +30,7 @@ REF_SUITES = {
     "comm": "simulated logical timestamps*,staged hops pay the copy cost*,tcp transport*",
     "partition": "",
     "jagged": "",
+    "embedding": "",
 }
 
 
