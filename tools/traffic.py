@@ -4,13 +4,14 @@ and dram__bytes_write.sum per launch (tools/gpu_prof3.sh), write
   a per-kernel summary (stdout): launches, time share, DRAM bytes per launch.
 Phase -> kernels (one rank): merge = k_copy_rows<MergeMap> (one span per launch);
 co_update = the whole update of one iteration (k_grad_ptrs, SgdPlanOp scan,
-k_sgd_single, k_sgd_flat, k_sgd_combine; one span per iteration)."""
+k_sgd_single, k_sgd_flat, k_sgd_combine, or the stream kernel k_sgd_stream;
+one span per iteration)."""
 import collections
 import csv
 import json
 import sys
 
-UPDATE = ("k_grad_ptrs", "k_sgd_single", "k_sgd_flat", "k_sgd_warp", "k_sgd_combine")  # the plan scan runs on L (one rank)
+UPDATE = ("k_grad_ptrs", "k_sgd_single", "k_sgd_flat", "k_sgd_warp", "k_sgd_combine", "k_sgd_stream")  # the plan scan runs on L (one rank)
 
 
 def load(path):
@@ -45,7 +46,9 @@ def main(path, out_json="profiles/traffic.json", key="n1"):
         print(f"{v[0]:8d} {v[1]:10.1f} {100 * v[1] / tot:5.1f}% {v[2] / v[0] / 1e6:15.2f}  {n[:90]}")
     merge = [k for k in ks if "MergeMap" in k["name"]]
     upd = [k for k in ks if any(u in k["name"] for u in UPDATE)]
-    iters = sum(1 for k in ks if "k_sgd_single" in k["name"])
+    # one update per iteration: the stream kernel's launches (else the older
+    # single + warp pair, one k_sgd_single per iteration)
+    iters = sum(1 for k in ks if "k_sgd_stream" in k["name"]) or sum(1 for k in ks if "k_sgd_single" in k["name"])
     dram = lambda L: sum(k.get("dram__bytes_read.sum", 0) + k.get("dram__bytes_write.sum", 0) for k in L)  # noqa: E731
     res = {}
     if merge:
