@@ -95,3 +95,15 @@ def test_reader_errors_match_reference_texts(tool, reference):
         open(bad, "wb").write(b"XXXXXXXX" + data[8:])
         r = subprocess.run([tool, "load", bad], capture_output=True, text=True)
         assert r.returncode == 1 and "workload: bad magic in" in r.stderr
+
+
+@pytest.mark.parametrize("suite", ["workload", "sim"])
+def test_reference_host_suites_unchanged(suite):
+    """The reference's test_workload.cpp / test_sim.cpp (host-only code: the
+    generator, file codec, statistics, Timeline, metric records, cost model)
+    compiled unchanged against the drop-in headers (cpp/Makefile)."""
+    exe = os.path.join(CPP, "build", f"ref_test_{suite}")
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built (needs /root/reference at build time)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and " 0 failed" in r.stdout, r.stdout[-3000:] + r.stderr[-2000:]
