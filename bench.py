@@ -25,7 +25,10 @@ import threading
 import time
 
 os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
-os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep NCCL's version banner off stdout (one JSON line)
+# keep NCCL's version banner off stdout (the bench prints one JSON line); an
+# explicit NCCL_DEBUG=INFO / TRACE request is kept
+if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+    os.environ["NCCL_DEBUG"] = "WARN"
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 import numpy as np  # noqa: E402
