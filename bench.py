@@ -313,8 +313,8 @@ def reference_arm(args, world, rank):
 def contention(eng, victim, lens, dev, world, per_peer_bytes=32 << 20, reps=4):
     """The victim's own duration (CUDA events on its stream) alone, then with
     all-to-all traffic running concurrently on another stream: (a) the
-    copy-engine all-to-all (fsx_a2a_ce over the engine's windows: cudaMemcpyAsync
-    peer copies + stream memory-op flags, no kernels), (b) NCCL's all-to-all
+    copy-engine all-to-all (fsx_engine_a2a_staged: the engine's windows,
+    cudaMemcpyAsync peer copies + stream memory-op flags, no kernels), (b) NCCL's all-to-all
     (torch.distributed.all_to_all_single: SM-resident kernels). Also the
     transfers' own rate (bytes out per GPU / time) while the victim runs and
     alone. Collective: every rank calls it."""
@@ -331,8 +331,9 @@ def contention(eng, victim, lens, dev, world, per_peer_bytes=32 << 20, reps=4):
     got = (C.c_uint64 * world)()
 
     def ce_once():
-        _lib.call("fsx_a2a_ce", eng.h, C.c_void_p(send.data_ptr()), offs, nb, C.c_void_p(recv.data_ptr()),
-                  per_peer_bytes, got, C.c_void_p(side.cuda_stream))
+        # the engine's exchange as its protocol runs it: payload already in
+        # the staging windows, copy-engine peer copies + flags, no host sync
+        _lib.call("fsx_engine_a2a_staged", eng.h, per_peer_bytes, C.c_void_p(side.cuda_stream))
 
     def nccl_once():
         with torch.cuda.stream(side):

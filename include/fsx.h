@@ -294,6 +294,11 @@ int fsx_autotune_update(int n, int32_t* sizes, double* ema_local, double* ema_gl
                         double delta, double decay, const double* local_times);
 
 /* ---- raw copy-engine all-to-all (comm.cpp:308-365 analogue) ---------------- */
+/* The engine's copy-engine all-to-all of bytes_per_peer from its GRADS
+ * staging slots to every peer, exactly as the protocol's exchanges run
+ * (enqueue only, no host synchronisation; collective) — a measurement entry
+ * point for comparisons with other transports (tools/nccl_ce_compare.py). */
+int fsx_engine_a2a_staged(fsx_engine* e, uint64_t bytes_per_peer, void* stream);
 /* Each engine also exposes its transport as a plain byte all-to-all over the
  * engine's windows: send_bytes[d] bytes from d_send + send_offsets[d] go to
  * rank d; on return d_recv + d * slot_bytes holds what rank d sent here and

@@ -83,6 +83,7 @@ _SIGS = {
     "fsx_pooled_backward": ([vp, vp, vp], i32),
     "fsx_engine_spans": ([vp, vp, u64, P(u64)], i32),
     "fsx_engine_trace": ([vp, vp, u64, P(u64)], i32),
+    "fsx_engine_a2a_staged": ([vp, u64, vp], i32),
     "fsx_engine_phase_ms": ([vp, i32, P(dbl), P(u64)], i32),
     "fsx_cost_estimate": ([vp, vp, vp, i32, dbl, dbl, dbl, vp, vp], i32),
     "fsx_fbs_partition": ([vp, vp, vp, vp, u64, i32, vp, vp, vp], i32),

@@ -2307,4 +2307,21 @@ int fsx_a2a_ce(fsx_engine* e, const void* d_send, const uint64_t* h_send_offsets
   FSX_API_END
 }
 
+// The engine's copy-engine all-to-all alone (measurement, e.g. against NCCL's
+// copy-engine collectives): bytes_per_peer from each staging slot of the
+// GRADS channel to every peer, as the protocol's own exchanges move them
+// (kernels have written the staging slots; here they hold whatever they
+// hold). Enqueue only — no host synchronisation; collective.
+int fsx_engine_a2a_staged(fsx_engine* e, uint64_t bytes_per_peer, void* stream) {
+  FSX_API_BEGIN
+  DeviceGuard dg(e->ctx->device);
+  if (bytes_per_peer + kHdr > e->ch_slot[CH_GRADS])
+    raise(FSX_ERR_COLLECTIVE, "all_to_all: payload of " + std::to_string(bytes_per_peer) +
+                                  " bytes exceeds the slot capacity");
+  const int par = e->next_par(CH_GRADS);
+  std::vector<uint64_t> bytes(e->p, kHdr + bytes_per_peer);
+  e->a2a(CH_GRADS, par, bytes, static_cast<cudaStream_t>(stream));
+  FSX_API_END
+}
+
 }  // extern "C"
