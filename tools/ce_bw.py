@@ -11,14 +11,16 @@ import torch
 from cuda.bindings import runtime as rt
 
 
-def time_copies(pairs, nbytes, k, reps=20):
-    """pairs: [(src, dst)]. Returns ms per round (max over source devices)."""
+def time_copies(pairs, nbytes, k, reps=20, pull=False):
+    """pairs: [(src, dst)]. Returns ms per round (max over issuing devices).
+    pull: the copy is issued on a stream of the destination device (its copy
+    engine reads from the peer) instead of the source's (writes to the peer)."""
     bufs = {}
     streams = {}
     for s, d in pairs:
         bufs[(s, d)] = (torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{s}"),
                         torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{d}"))
-        streams[(s, d)] = [torch.cuda.Stream(device=s) for _ in range(k)]
+        streams[(s, d)] = [torch.cuda.Stream(device=d if pull else s) for _ in range(k)]
     chunk = (nbytes + k - 1) // k
 
     def round_():
@@ -65,6 +67,20 @@ def main():
     for a, b in itertools.permutations(range(n), 2):
         rt.cudaSetDevice(a)
         rt.cudaDeviceEnablePeerAccess(b, 0)
+    if len(sys.argv) > 1 and sys.argv[1] == "fanout":
+        # does one GPU run copies to several peers at once? push (its engine
+        # writes) vs pull (each peer's engine reads); then the all-to-all both ways
+        for mb in (2, 8, 32):
+            for pull in (False, True):
+                ms = time_copies([(0, d) for d in range(1, n)], mb << 20, 1, pull=pull)
+                print(f"fan-out 0->{n - 1} peers {mb:3d} MiB {'pull' if pull else 'push'}: {ms * 1e3:8.1f} us "
+                      f"{(n - 1) * (mb << 20) / ms / 1e6:8.1f} GB/s", flush=True)
+            for pull in (False, True):
+                pairs = [(s, d) for s in range(n) for d in range(n) if s != d]
+                ms = time_copies(pairs, mb << 20, 1, pull=pull)
+                print(f"a2a x{n} {mb:3d} MiB/peer {'pull' if pull else 'push'}: {ms * 1e3:8.1f} us "
+                      f"{(n - 1) * (mb << 20) / ms / 1e6:8.1f} GB/s out per GPU", flush=True)
+        return 0
     for mb in (1, 4, 16, 64):
         for k in (1, 2, 4, 8):
             ms = time_copies([(0, 1)], mb << 20, k)
