@@ -59,6 +59,12 @@ def parse():
     ap.add_argument("--seed", type=int, default=20261018)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-phases", type=int, default=1)
+    ap.add_argument("--cfg5-direct", type=int, default=0,
+                    help="config 5: also the arms with the collision chain's transfers as direct NVLink stores "
+                         "(fsx_engine_set_eco_direct mask 3; opt-in, see DESIGN.md §6)")
+    ap.add_argument("--cfg5-partition", choices=("vbs", "fbs"), default="fbs",
+                    help="config 5 load balancer: FBS (default) or VBS")
+    ap.add_argument("--cfg5-alpha", type=float, default=2.0, help="VBS weight exponent (uih_len^alpha)")
     ap.add_argument("--cfg5", type=int, default=-1,
                     help="also run config 5 (embedding + HSTU-style victim; blocking NCCL vs "
                          "prioritized copy-engine); default: on when N > 1")
@@ -91,11 +97,14 @@ def batches_for(args, rank, world, iters, with_lens=False):
 
 
 def balance_batches(args, world, rank, iters, first, ctx):
-    """Config 5's load-balancing stage (partition.cpp:157-176, FBS on the
-    GPU): for every iteration >= first, the global batch (every rank's UIH
-    samples, regenerated deterministically here) is partitioned across ranks
-    by uih length — equal sample counts, snake order — and this rank keeps
-    its assigned samples in receive order. Replaces batches/lens in place."""
+    """Config 5's load-balancing stage on the GPU: for every iteration >=
+    first, the global batch (every rank's UIH samples, regenerated
+    deterministically here) is partitioned across ranks by uih length and
+    this rank keeps its assigned samples in receive order. --cfg5-partition
+    vbs (default): variable batch sizes, min-max cut of uih_len^alpha
+    (partition.cpp:178-209, alpha 2: the cost model's quadratic term
+    dominates at these lengths), so every rank's compute is close to equal;
+    fbs: equal sample counts, snake order (partition.cpp:157-176)."""
     from paper_2604_24073_b200 import partition as P
     from paper_2604_24073_b200 import workload
     tables = args.tables_per_rank * world
@@ -104,7 +113,10 @@ def balance_batches(args, world, rank, iters, first, ctx):
         per = [workload.cfg_tokens(args.seed, i, r, args.samples, tables, args.rows_per_table)
                for r in range(world)]
         metas = [P.GlobalSampleMeta(r, k, int(l)) for r in range(world) for k, l in enumerate(per[r][0])]
-        plan = P.fbs_partition(metas, world, ctx=ctx)
+        if getattr(args, "cfg5_partition", "vbs") == "fbs":
+            plan = P.fbs_partition(metas, world, ctx=ctx)
+        else:
+            plan = P.vbs_partition(metas, world, args.cfg5_alpha, ctx=ctx)
         offs = [np.concatenate([[0], np.cumsum(per[r][0].astype(np.int64))]) for r in range(world)]
         ids, lens = [], []
         for g in plan.receive_order[rank]:
@@ -823,16 +835,21 @@ def main():
             # (B) prioritized + copy engines, victim between forward and backward
             res["prio_ce"] = prio_loop(it0, False)
             if world > 1:
-                # (B') the same with the collision chain's transfers stored by
-                # its kernels straight into the peers' windows: the pre-sum
-                # into the owners' CO_G slots, the collision update into the
-                # requesters' E_co slots (SM-issued NVLink stores, no copy-engine
-                # hop); then both prioritized arms with the dense sync
-                eng.set_eco_direct(True, cog=True)
-                res["prio_direct"] = prio_loop(it0 + K, False)
-                res["prio_direct_sync"] = prio_loop(it0 + 2 * K, True)
-                eng.set_eco_direct(False)
-                res["prio_ce_sync"] = prio_loop(it0 + 3 * K, True)
+                # (B') with --cfg5-direct: the same with the collision chain's
+                # transfers stored by its kernels straight into the peers'
+                # windows — the pre-sum into the owners' CO_G slots, the
+                # collision update into the requesters' E_co slots (SM-issued
+                # NVLink stores, no copy-engine hop); then the prioritized
+                # arm(s) with the dense sync
+                nxt = it0 + K
+                if args.cfg5_direct:
+                    mask = int(os.environ.get("FSX_BENCH_DIRECT_MASK", "3"))  # (A/B: 1 = E_co only, 2 = CO_G only)
+                    eng.set_eco_direct(bool(mask & 1), cog=bool(mask & 2))
+                    res["prio_direct"] = prio_loop(nxt, False)
+                    res["prio_direct_sync"] = prio_loop(nxt + K, True)
+                    nxt += 2 * K
+                    eng.set_eco_direct(False)
+                res["prio_ce_sync"] = prio_loop(nxt, True)
         # (A) the blocking baseline: synchronized engine, NCCL all-to-all (N>1)
         base_tr = "nccl" if world > 1 else "ce"
         sync_eng = E.SynchronizedEmbedding(shard, comm, max_occurrences=cap,
@@ -897,12 +914,16 @@ def main():
                         "exposed_reduction_pct": {},
                         "step_ms": {b_key: round(max_over_ranks(res[b_key + "_sync"][0]), 4)}}
             for k in ("prio_ce_sync", "prio_direct_sync"):
+                if k not in res:
+                    continue
                 x = max_over_ranks(res[k][1])
                 sync_out["exposed_ms_per_iter_max_over_ranks"][k] = round(x, 4)
                 sync_out["exposed_reduction_pct"][k] = round(100.0 * (1 - x / sb), 2) if sb > 0 else None
                 sync_out["step_ms"][k] = round(max_over_ranks(res[k][0]), 4)
         cfg5_out = {
-            "load_balancer": ("FBS (partition.cpp:157-176) over the global batch of each iteration, on the GPU"
+            "load_balancer": (("FBS (partition.cpp:157-176)" if args.cfg5_partition == "fbs" else
+                               f"VBS alpha {args.cfg5_alpha} (partition.cpp:178-209)") +
+                              " over the global batch of each iteration, on the GPU"
                               if world > 1 else "none (1 rank)"),
             "workload": ("config 5: config-4 embeddings + synthetic HSTU-style compute between forward and "
                          f"backward, per-rank cost c0+c1*sum(L)+c2*sum(L^2) = {victim.c0}+{victim.c1}*sum(L)+"

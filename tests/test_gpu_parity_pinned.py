@@ -84,20 +84,22 @@ def test_cfg1_full_size_bitwise(drv, oracle, iters):
     _report(f"cfg1_iters{iters}", rep)
 
 
-@pytest.mark.parametrize("world,direct,direct_from", [(2, 0, 0), (4, 0, 0), (2, 3, 0), (4, 3, 2), (4, 2, 1)])
-def test_cfg4_shape_presum_bitwise(drv, oracle, world, direct, direct_from):
+@pytest.mark.parametrize("world,direct,direct_from,skew", [(2, 0, 0, 0), (4, 0, 0, 0), (2, 3, 0, 0), (4, 3, 2, 0),
+                                                          (4, 2, 1, 0), (4, 0, 0, 1), (4, 3, 0, 1)])
+def test_cfg4_shape_presum_bitwise(drv, oracle, world, direct, direct_from, skew):
     """Reduced config 4: 64 tables x 20,000 rows x 256 fp32, fused gid =
     t * rows + scramble(t, row), row ~ Zipf(1.1), power-law UIH lengths,
     row-wise gid mod p over `world` in-process ranks, PRESUM on,
     reduce_chunk 64 — the bench's numeric path at N > 1. direct: the
     collision chain's transfers by direct stores (1 = E_co, 2 = CO_G),
-    switched on before iteration direct_from."""
+    switched on before iteration direct_from. skew: ranks get 1x .. 4x the
+    samples (variable batch sizes, as a cost-balancing partitioner makes)."""
     from paper_2604_24073_b200 import workload
     from paper_2604_24073_b200.embedding import TableGeometry
     tables, rpt, dim, lr, seed, samples, iters = 64, 20_000, 256, 0.05, 20261018, 96, 4
     rows = tables * rpt
-    batches = [[workload.cfg_tokens(seed, i, r, samples, tables, rpt)[1] for r in range(world)]
-               for i in range(iters)]
+    batches = [[workload.cfg_tokens(seed, i, r, samples * (1 + r % 4 if skew else 1), tables, rpt)[1]
+                for r in range(world)] for i in range(iters)]
     geom = TableGeometry(rows, dim, world)
     got, st = drv.run_engine(True, batches, geom, lr, seed, dtype="f32", reduce_chunk=64, presum=True,
                              with_stats=True, direct=direct, direct_from=direct_from)
@@ -107,7 +109,7 @@ def test_cfg4_shape_presum_bitwise(drv, oracle, world, direct, direct_from):
     want64, stats = oracle.run_engine(world, batches, rows, dim, lr, seed, with_stats=True)
     got_st = np.array([[s.collision_rows, s.unique_next_rows, s.blocking_bytes] for s in st], np.uint64)
     assert np.array_equal(got_st, stats)
-    if direct:
+    if direct or skew:
         return
     ids = np.concatenate([b for it in batches for b in it])
     _report(f"cfg4shape_p{world}", {
