@@ -51,3 +51,19 @@ def test_multiprocess_more_ranks_than_gpus(dtype, presum):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     print(r.stdout[-3000:], r.stderr[-3000:])
     assert r.returncode == 0 and "MP_OK" in r.stdout
+
+
+def test_multiprocess_direct_stores_equal_copy_engine_tables():
+    """One process per GPU, config-4-scale skewed batches (1x / 2x the
+    per-rank share, 32 tables x 1M x 256 fp32, PRESUM): the collision chain by
+    direct stores (mask 3) leaves tables bit-identical to the copy-engine run."""
+    n = _ngpus()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(n, 4)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", "--master-port=29537", os.path.join(ROOT, "tests", "mp_stress_direct.py"),
+           "8", "3"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    print(r.stdout[-3000:], r.stderr[-3000:])
+    assert r.returncode == 0 and "STRESS_OK" in r.stdout
