@@ -113,10 +113,10 @@ def balance_batches(args, world, rank, iters, first, ctx):
         per = [workload.cfg_tokens(args.seed, i, r, args.samples, tables, args.rows_per_table)
                for r in range(world)]
         metas = [P.GlobalSampleMeta(r, k, int(l)) for r in range(world) for k, l in enumerate(per[r][0])]
-        if getattr(args, "cfg5_partition", "vbs") == "fbs":
+        if getattr(args, "cfg5_partition", "fbs") == "fbs":
             plan = P.fbs_partition(metas, world, ctx=ctx)
         else:
-            plan = P.vbs_partition(metas, world, args.cfg5_alpha, ctx=ctx)
+            plan = P.vbs_partition(metas, world, getattr(args, "cfg5_alpha", 2.0), ctx=ctx)
         offs = [np.concatenate([[0], np.cumsum(per[r][0].astype(np.int64))]) for r in range(world)]
         ids, lens = [], []
         for g in plan.receive_order[rank]:
