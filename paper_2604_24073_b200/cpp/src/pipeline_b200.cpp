@@ -354,69 +354,69 @@ using comm::Bytes;
 
 Balancer::Balancer(comm::Communicator& comm, BalancerConfig config,
                    std::function<const workload::Batch*(int)> raw_batches, int num_iterations)
-    : comm_(comm), config_(std::move(config)), raw_batches_(std::move(raw_batches)), num_iterations_(num_iterations) {
-  if (config_.lead < 1) throw ConfigError("balancer: lead must be >= 1");
-  tune_.step = config_.autotune_step;
-  tune_.delta = config_.autotune_delta;
-  tune_.decay = config_.autotune_decay;
+    : comm_(comm), cfg_(std::move(config)), source_(std::move(raw_batches)), iterations_(num_iterations) {
+  if (cfg_.lead < 1) throw ConfigError("balancer: lead must be >= 1");
+  tune_.step = cfg_.autotune_step;
+  tune_.delta = cfg_.autotune_delta;
+  tune_.decay = cfg_.autotune_decay;
 }
 
-Balancer::Pending* Balancer::pending_for(int index, bool create) {
-  for (Pending& p : pending_)
-    if (p.index == index) return &p;
-  if (!create || index >= num_iterations_) return nullptr;
-  Pending p;
-  p.index = index;
-  p.raw = raw_batches_(index);
-  if (!p.raw) throw ProtocolError("balancer: no raw batch for iteration " + std::to_string(index));
-  pending_.push_back(std::move(p));
-  return &pending_.back();
+Balancer::Work* Balancer::find(int index, bool create) {
+  for (Work& p : work_)
+    if (p.iteration == index) return &p;
+  if (!create || index >= iterations_) return nullptr;
+  Work p;
+  p.iteration = index;
+  p.source = source_(index);
+  if (!p.source) throw ProtocolError("balancer: no raw batch for iteration " + std::to_string(index));
+  work_.push_back(std::move(p));
+  return &work_.back();
 }
 
-void Balancer::run_stage_for(int index, int stage) {
-  if (index < 0 || index >= num_iterations_) return;
-  Pending* p = pending_for(index, stage == 0);
+void Balancer::fire(int index, int stage) {
+  if (index < 0 || index >= iterations_) return;
+  Work* p = find(index, stage == 0);
   if (!p) return;
-  ++stage_fires_[stage];
-  if (stage == 0) stage1_gather_lengths(*p);
-  else if (stage == 1) stage2_gather_candidate_lengths_and_plan(*p);
-  else stage3_shuffle(*p);
+  ++fired_[stage];
+  if (stage == 0) gather_lengths(*p);
+  else if (stage == 1) gather_candidates_and_plan(*p);
+  else exchange_samples(*p);
 }
 
 void Balancer::install_hooks(pipeline::HookRegistry& hooks) {
-  const int lead = config_.lead;
+  const int lead = cfg_.lead;
   hooks.add(pipeline::HookPoint::DataLoad, [this, lead](const pipeline::HookContext& c) {
     if (c.iteration != 0) return;
-    for (int j = 0; j < lead && j < num_iterations_; ++j)
-      for (int s = 0; s < 3; ++s) run_stage_for(j, s);
-    run_stage_for(lead, 0);
+    for (int j = 0; j < lead && j < iterations_; ++j)
+      for (int s = 0; s < 3; ++s) fire(j, s);
+    fire(lead, 0);
   });
-  hooks.add(pipeline::HookPoint::PreForward, [this, lead](const pipeline::HookContext& c) { run_stage_for(c.iteration + lead, 1); });
-  hooks.add(pipeline::HookPoint::PostForward, [this, lead](const pipeline::HookContext& c) { run_stage_for(c.iteration + lead, 2); });
+  hooks.add(pipeline::HookPoint::PreForward, [this, lead](const pipeline::HookContext& c) { fire(c.iteration + lead, 1); });
+  hooks.add(pipeline::HookPoint::PostForward, [this, lead](const pipeline::HookContext& c) { fire(c.iteration + lead, 2); });
   hooks.add(pipeline::HookPoint::OptimizerStep,
-            [this, lead](const pipeline::HookContext& c) { run_stage_for(c.iteration + lead + 1, 0); });
+            [this, lead](const pipeline::HookContext& c) { fire(c.iteration + lead + 1, 0); });
 }
 
-void Balancer::stage1_gather_lengths(Pending& p) {
-  if (p.stage != Stage::Idle) throw ProtocolError("balancer: stage 1 fired out of order");
+void Balancer::gather_lengths(Work& p) {
+  if (p.at != Stage::Idle) throw ProtocolError("balancer: stage 1 fired out of order");
   // [B, uih lengths, candidate counts] as u64, then the last compute time (f64)
-  std::vector<std::uint64_t> v{p.raw->samples.size()};
-  for (const auto& s : p.raw->samples) v.push_back(s.uih.size());
-  for (const auto& s : p.raw->samples) v.push_back(s.candidates.size());
+  std::vector<std::uint64_t> v{p.source->samples.size()};
+  for (const auto& s : p.source->samples) v.push_back(s.uih.size());
+  for (const auto& s : p.source->samples) v.push_back(s.candidates.size());
   Bytes msg = comm::pack_u64s(v);
   const std::size_t at = msg.size();
   msg.resize(at + 8);
-  std::memcpy(msg.data() + at, &last_compute_us_, 8);
-  const auto all = comm_.all_gather(msg, {Channel::Side, Category::Balancer, config_.mode, false});
+  std::memcpy(msg.data() + at, &compute_us_, 8);
+  const auto all = comm_.all_gather(msg, {Channel::Side, Category::Balancer, cfg_.mode, false});
   const int world = comm_.world_size();
   p.metas.clear();
-  p.world_num_candidates.clear();
-  p.world_times.assign(static_cast<std::size_t>(world), 0.0);
+  p.candidate_counts.clear();
+  p.rank_compute_us.assign(static_cast<std::size_t>(world), 0.0);
   for (int r = 0; r < world; ++r) {
     const Bytes& b = all[static_cast<std::size_t>(r)];
     if (b.size() < 16) throw ProtocolError("balancer: short stage-1 payload");
     const auto u = comm::unpack_u64s(Bytes(b.begin(), b.end() - 8));
-    std::memcpy(&p.world_times[static_cast<std::size_t>(r)], b.data() + b.size() - 8, 8);
+    std::memcpy(&p.rank_compute_us[static_cast<std::size_t>(r)], b.data() + b.size() - 8, 8);
     const std::size_t B = static_cast<std::size_t>(u.at(0));
     if (u.size() != 1 + 2 * B) throw ProtocolError("balancer: stage-1 payload shape mismatch");
     for (std::size_t k = 0; k < B; ++k) {
@@ -426,18 +426,18 @@ void Balancer::stage1_gather_lengths(Pending& p) {
       m.uih_len = u[1 + k];
       m.num_candidates = static_cast<std::uint32_t>(u[1 + B + k]);
       p.metas.push_back(std::move(m));
-      p.world_num_candidates.push_back(u[1 + B + k]);
+      p.candidate_counts.push_back(u[1 + B + k]);
     }
   }
-  p.stage = Stage::LengthsGathered;
+  p.at = Stage::LengthsGathered;
 }
 
-void Balancer::stage2_gather_candidate_lengths_and_plan(Pending& p) {
-  if (p.stage != Stage::LengthsGathered) throw ProtocolError("balancer: stage 2 before stage 1");
+void Balancer::gather_candidates_and_plan(Work& p) {
+  if (p.at != Stage::LengthsGathered) throw ProtocolError("balancer: stage 2 before stage 1");
   std::vector<std::uint64_t> mine;
-  for (const auto& s : p.raw->samples)
+  for (const auto& s : p.source->samples)
     for (const auto& c : s.candidates) mine.push_back(c.size());
-  const auto all = comm_.all_gather(comm::pack_u64s(mine), {Channel::Side, Category::Balancer, config_.mode, false});
+  const auto all = comm_.all_gather(comm::pack_u64s(mine), {Channel::Side, Category::Balancer, cfg_.mode, false});
   std::size_t m = 0;
   for (int r = 0; r < comm_.world_size(); ++r) {
     const auto lens = comm::unpack_u64s(all[static_cast<std::size_t>(r)]);
@@ -455,16 +455,16 @@ void Balancer::stage2_gather_candidate_lengths_and_plan(Pending& p) {
     }
   }
   const int world = comm_.world_size();
-  const std::string& part = config_.partition;
+  const std::string& part = cfg_.partition;
   if (part == "fbs") {
     p.plan = partition::fbs_partition(p.metas, world);
   } else if (part == "vbs") {
-    if (tune_.initialized && std::any_of(p.world_times.begin(), p.world_times.end(), [](double t) { return t > 0; })) {
-      std::vector<double> t(p.world_times);
+    if (tune_.initialized && std::any_of(p.rank_compute_us.begin(), p.rank_compute_us.end(), [](double t) { return t > 0; })) {
+      std::vector<double> t(p.rank_compute_us);
       for (double& x : t) x = std::max(x, 1e-9);
       partition::autotune_update(tune_, t);
     }
-    p.plan = partition::vbs_partition(p.metas, world, config_.alpha, &tune_);
+    p.plan = partition::vbs_partition(p.metas, world, cfg_.alpha, &tune_);
   } else if (part == "none") {
     p.plan = partition::identity_partition(p.metas, world);
   } else if (part.rfind("custom:", 0) == 0) {
@@ -475,11 +475,11 @@ void Balancer::stage2_gather_candidate_lengths_and_plan(Pending& p) {
     throw ConfigError("balancer: unknown partition '" + part + "'");
   }
   p.plan.validate(p.metas.size(), part == "fbs");
-  p.stage = Stage::CandidatesGathered;
+  p.at = Stage::CandidatesGathered;
 }
 
-void Balancer::stage3_shuffle(Pending& p) {
-  if (p.stage != Stage::CandidatesGathered) throw ProtocolError("balancer: stage 3 before stage 2");
+void Balancer::exchange_samples(Work& p) {
+  if (p.at != Stage::CandidatesGathered) throw ProtocolError("balancer: stage 3 before stage 2");
   const auto lists = p.plan.exchange_lists(p.metas);
   const auto& sends = lists[static_cast<std::size_t>(comm_.rank())];
   std::vector<Bytes> out(static_cast<std::size_t>(comm_.world_size()));
@@ -487,29 +487,29 @@ void Balancer::stage3_shuffle(Pending& p) {
   for (std::size_t dst = 0; dst < out.size(); ++dst)
     for (int local : sends[dst]) {
       rec.clear();
-      workload::encode_sample(p.raw->samples.at(static_cast<std::size_t>(local)), rec);
+      workload::encode_sample(p.source->samples.at(static_cast<std::size_t>(local)), rec);
       const std::uint32_t n = static_cast<std::uint32_t>(rec.size());
       const std::size_t at = out[dst].size();
       out[dst].resize(at + 4 + n);
       std::memcpy(out[dst].data() + at, &n, 4);
       std::memcpy(out[dst].data() + at + 4, rec.data(), n);
     }
-  p.shuffled.value = comm_.all_to_all(out, {Channel::Side, Category::Balancer, config_.mode, false});
-  p.shuffled.category = Category::Balancer;
-  p.shuffled.ready_time = comm_.clock() ? comm_.clock()->side_time() : 0.0;
-  p.shuffled.bytes = 0;
-  for (const Bytes& b : p.shuffled.value) p.shuffled.bytes += b.size();
-  p.stage = Stage::Shuffled;
+  p.records.value = comm_.all_to_all(out, {Channel::Side, Category::Balancer, cfg_.mode, false});
+  p.records.category = Category::Balancer;
+  p.records.ready_time = comm_.clock() ? comm_.clock()->side_time() : 0.0;
+  p.records.bytes = 0;
+  for (const Bytes& b : p.records.value) p.records.bytes += b.size();
+  p.at = Stage::Shuffled;
 }
 
-workload::Batch Balancer::assemble(Pending& p) {
+workload::Batch Balancer::build_batch(Work& p) {
   const int me = comm_.rank();
-  std::vector<std::size_t> at(p.shuffled.value.size(), 0);
+  std::vector<std::size_t> at(p.records.value.size(), 0);
   workload::Batch out;
   out.rank = me;
   for (std::size_t g : p.plan.receive_order[static_cast<std::size_t>(me)]) {
     const std::size_t src = static_cast<std::size_t>(p.metas[g].origin_rank);
-    const Bytes& blob = p.shuffled.value[src];
+    const Bytes& blob = p.records.value[src];
     if (at[src] + 4 > blob.size()) throw ProtocolError("balancer: stage-3 payload shorter than the plan");
     std::uint32_t n = 0;
     std::memcpy(&n, blob.data() + at[src], 4);
@@ -521,28 +521,28 @@ workload::Batch Balancer::assemble(Pending& p) {
     at[src] += n;
   }
   for (std::size_t src = 0; src < at.size(); ++src)
-    if (at[src] != p.shuffled.value[src].size())
+    if (at[src] != p.records.value[src].size())
       throw ProtocolError("balancer: stage-3 payload from rank " + std::to_string(src) + " longer than the plan");
   return out;
 }
 
 workload::Batch Balancer::take(int iteration) {
-  Pending* p = pending_for(iteration, false);
-  if (!p || p->stage != Stage::Shuffled)
+  Work* p = find(iteration, false);
+  if (!p || p->at != Stage::Shuffled)
     throw ProtocolError("balancer: batch " + std::to_string(iteration) + " consumed before stage 3 completed");
-  comm_.wait_handle(p->shuffled);
-  workload::Batch out = p->balanced ? std::move(*p->balanced) : assemble(*p);
-  while (!pending_.empty() && pending_.front().index <= iteration) pending_.pop_front();
+  comm_.wait_handle(p->records);
+  workload::Batch out = p->assembled ? std::move(*p->assembled) : build_batch(*p);
+  while (!work_.empty() && work_.front().iteration <= iteration) work_.pop_front();
   return out;
 }
 
 const workload::Batch* Balancer::peek(int iteration) {
-  Pending* p = pending_for(iteration, false);
+  Work* p = find(iteration, false);
   if (!p) return nullptr;
-  if (p->stage != Stage::Shuffled)
+  if (p->at != Stage::Shuffled)
     throw ProtocolError("balancer: peek at batch " + std::to_string(iteration) + " before stage 3 completed");
-  if (!p->balanced) p->balanced = assemble(*p);
-  return &*p->balanced;
+  if (!p->assembled) p->assembled = build_batch(*p);
+  return &*p->assembled;
 }
 
 }  // namespace balancer
